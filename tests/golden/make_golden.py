@@ -1,0 +1,284 @@
+"""Generate golden fixtures by running the REFERENCE implementation itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py [--big]
+
+It imports the unmodified reference package from /root/reference/pkg/src and
+records, for seeded inputs built with ``paper_1810_05231_b200.workloads``:
+
+* ``ops_small.npz``   — operator-level known answers (apply_M, adjoint,
+  operator norm, aproj_psd incl. the ARPACK path, dual step, residuals) on
+  random problems shaped like the reference's own ``conftest.random_problem``;
+* ``lr_small.npz``    — full LR-PD-SDP solves of small problems (with
+  inequalities, so the box projection branch is exercised);
+* ``cfg1.npz``        — BASELINE config 1 (n=100 Max-Cut): iterates at
+  K = 1, 10, 100 and at the stop iteration, per-iteration residual history,
+  final objective / rank path / checkpoints;
+* ``cfgN_sketch.npz`` (``--big``) — configs 2-5 at small K: y, lambda_{r+1},
+  residuals, tr(CX), ||X||_F and the sketch X @ z for a seeded z (sketches
+  keep the fixtures small while pinning the full n x n iterate).
+
+The reference crashes on config 4 iteration 1 (ArpackError -9, SURVEY.md §8c
+quirk 1); for that config only the harness wraps ``truncated_eigen`` with the
+reference's own dense fallback (``symmat.py:200-207``).
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import pdsdp  # noqa: E402  (the reference)
+import pdsdp.lowrank as ref_lowrank  # noqa: E402
+import pdsdp.symmat as ref_symmat  # noqa: E402
+from pdsdp import SdpProblem as RProblem, SparseRow as RRow, SymMatrix as RSym  # noqa: E402
+from scipy.sparse.linalg import ArpackError  # noqa: E402
+
+from paper_1810_05231_b200 import workloads  # noqa: E402
+
+SKETCH_SEED = 777
+
+
+def to_ref(prob):
+    return RProblem(
+        n=prob.n, C=RSym(prob.n, prob.C.data.copy()),
+        A=[RRow(r.indices, r.values) for r in prob.A], b=prob.b.copy(),
+        G=[RRow(r.indices, r.values) for r in prob.G], h=prob.h.copy(),
+        name=prob.name, objective_sign=prob.objective_sign)
+
+
+def to_ref_cfg(cfg, **over):
+    d = dict(cfg.__dict__)
+    d.update(over)
+    return pdsdp.SolverConfig(**d)
+
+
+class LambdaRecorder:
+    """Wraps lowrank.aproj_psd to record lambda_{r+1} per iteration."""
+
+    def __init__(self):
+        self.values = []
+        self.orig = ref_lowrank.aproj_psd
+
+    def __enter__(self):
+        def wrapped(S, r):
+            out = self.orig(S, r)
+            self.values.append(out[1])
+            return out
+        ref_lowrank.aproj_psd = wrapped
+        return self
+
+    def __exit__(self, *a):
+        ref_lowrank.aproj_psd = self.orig
+
+
+class ArpackErrorFallback:
+    def __enter__(self):
+        self.orig = ref_symmat.truncated_eigen
+
+        def wrapped(S, r):
+            try:
+                return self.orig(S, r)
+            except ArpackError:
+                full = ref_symmat.full_eigen(S)
+                return ref_symmat.EigenDecomposition(
+                    full.values[:r].copy(), full.vectors[:, :r].copy(), r)
+        ref_symmat.truncated_eigen = wrapped
+        return self
+
+    def __exit__(self, *a):
+        ref_symmat.truncated_eigen = self.orig
+
+
+def random_problem(n, m, p, rng, nnz=4):
+    """Same construction as the reference's conftest.random_problem."""
+    def entries():
+        pairs = [(i, j) for i in range(n) for j in range(i, n)]
+        idx = rng.choice(len(pairs), size=min(nnz, len(pairs)), replace=False)
+        return [(pairs[k][0], pairs[k][1], float(rng.standard_normal())) for k in idx]
+    R = rng.standard_normal((n, n))
+    C = 0.5 * (R + R.T)
+    A = [pdsdp.SparseRow.from_matrix_entries(n, entries()) for _ in range(m)]
+    G = [pdsdp.SparseRow.from_matrix_entries(n, entries()) for _ in range(p)]
+    return pdsdp.SdpProblem(n=n, C=pdsdp.SymMatrix.from_dense(C), A=A,
+                            b=rng.standard_normal(m), G=G, h=rng.standard_normal(p))
+
+
+def flatten_problem(prefix, prob, out):
+    out[prefix + "n"] = prob.n
+    out[prefix + "C"] = prob.C.data
+    rows = list(prob.A) + list(prob.G)
+    out[prefix + "indptr"] = np.cumsum([0] + [r.indices.size for r in rows])
+    out[prefix + "idx"] = np.concatenate([r.indices for r in rows])
+    out[prefix + "val"] = np.concatenate([r.values for r in rows])
+    out[prefix + "b"] = prob.b
+    out[prefix + "h"] = prob.h
+
+
+def make_ops_small(path):
+    rng = np.random.default_rng(12345)
+    out = {}
+    cases = [(6, 4, 2), (9, 5, 3), (12, 7, 0), (40, 12, 6), (64, 20, 4)]
+    for ci, (n, m, p) in enumerate(cases):
+        prob = random_problem(n, m, p, rng, nnz=5)
+        pre = f"c{ci}_"
+        flatten_problem(pre, prob, out)
+        X = pdsdp.SymMatrix.from_dense((lambda R: R @ R.T)(rng.standard_normal((n, 3))))
+        y = rng.standard_normal(m + p)
+        out[pre + "X"] = X.data
+        out[pre + "y"] = y
+        out[pre + "MX"] = pdsdp.apply_M(prob, X)
+        out[pre + "MTy"] = pdsdp.apply_M_adjoint(prob, y).data
+        out[pre + "opnorm"] = pdsdp.estimate_operator_norm(prob, 0)
+        S = pdsdp.SymMatrix.from_dense((lambda R: 0.5 * (R + R.T))(rng.standard_normal((n, n))))
+        out[pre + "S"] = S.data
+        for r in (1, 3, n // 2, n):
+            P, lam = pdsdp.aproj_psd(S, r)
+            out[pre + f"aproj{r}"] = P.data
+            out[pre + f"aproj{r}_lam"] = lam
+        e = pdsdp.truncated_eigen(S, min(5, n))
+        out[pre + "teig_vals"] = e.values
+        alpha = 0.37
+        Xn = pdsdp.SymMatrix.from_dense((lambda R: R @ R.T)(rng.standard_normal((n, 2))))
+        from pdsdp.pdhg import IterateState, dual_step, residuals
+        from collections import deque
+        yn = dual_step(prob, y, Xn, X, alpha)
+        out[pre + "Xn"] = Xn.data
+        out[pre + "dual"] = yn
+        st = IterateState(Xn, X, yn, y, 1, deque())
+        out[pre + "resid"] = np.array(residuals(st, alpha, prob))
+    np.savez_compressed(path, **out)
+
+
+def make_lr_small(path):
+    rng = np.random.default_rng(2024)
+    out = {}
+    specs = [(8, 5, 0, 1), (10, 6, 4, 1), (16, 8, 6, 2), (36, 20, 10, 2), (48, 48, 0, 3)]
+    for ci, (n, m, p, r0) in enumerate(specs):
+        if ci == 4:   # Max-Cut shaped (diag pins), exercises the ARPACK path
+            prob = to_ref(workloads.maxcut_problem(n, 0.2, 11, signed=True))
+        else:
+            prob = random_problem(n, m, p, rng, nnz=4)
+            # make it well-posed: objective PSD-ish so the LR solve converges
+            R = rng.standard_normal((n, n))
+            prob = pdsdp.SdpProblem(n=n, C=pdsdp.SymMatrix.from_dense(R @ R.T / n),
+                                    A=prob.A, b=np.abs(prob.b) + 0.5, G=prob.G,
+                                    h=np.abs(prob.h) + 0.5)
+        pre = f"c{ci}_"
+        flatten_problem(pre, prob, out)
+        cfg = pdsdp.SolverConfig(eps_tol=1e-4, max_iter=400, initial_rank=r0, window_ell=50,
+                                 time_limit_s=1e9)
+        with LambdaRecorder() as rec:
+            res = pdsdp.solve_lr_pd_sdp(prob, cfg)
+        out[pre + "r0"] = r0
+        out[pre + "status"] = res.status.value
+        out[pre + "iters"] = res.iterations
+        out[pre + "X"] = res.X.data
+        out[pre + "y"] = res.y
+        out[pre + "pobj"] = res.primal_objective
+        out[pre + "dobj"] = res.dual_objective
+        out[pre + "res"] = np.array(res.final_residuals)
+        out[pre + "rank_path"] = np.array(res.rank_path)
+        out[pre + "lam"] = np.array(rec.values)
+        out[pre + "scale"] = res.residual_scale
+    np.savez_compressed(path, **out)
+
+
+def make_cfg1(path):
+    prob, cfg = workloads.config(0)
+    rp = to_ref(prob)
+    out = {}
+    flatten_problem("", rp, out)
+    for K in (1, 10, 100):
+        with LambdaRecorder() as rec:
+            res = pdsdp.solve_lr_pd_sdp(rp, to_ref_cfg(cfg, max_iter=K))
+        out[f"X{K}"] = res.X.data
+        out[f"y{K}"] = res.y
+        out[f"lam{K}"] = rec.values[-1]
+        out[f"res{K}"] = np.array(res.final_residuals)
+    hist = []
+    t0 = time.perf_counter()
+    with LambdaRecorder() as rec:
+        res = pdsdp.solve_lr_pd_sdp(rp, to_ref_cfg(cfg, progress_every=1),
+                                    callback=lambda info: hist.append(tuple(info)))
+    out["wall"] = time.perf_counter() - t0
+    out["status"] = res.status.value
+    out["iters"] = res.iterations
+    out["X_final"] = res.X.data
+    out["y_final"] = res.y
+    out["pobj"] = res.primal_objective
+    out["dobj"] = res.dual_objective
+    out["res_final"] = np.array(res.final_residuals)
+    out["rank_path"] = np.array(res.rank_path)
+    out["checkpoints"] = np.array([(c.rank, c.objective) for c in res.checkpoints])
+    out["scale"] = res.residual_scale
+    out["history"] = np.array(hist)
+    out["lam_hist"] = np.array(rec.values)
+    np.savez_compressed(path, **out)
+    print("cfg1", res.status, res.iterations, res.primal_objective, out["wall"])
+
+
+def make_sketch(path, idx, Ks):
+    prob, cfg = workloads.config(idx)
+    t0 = time.perf_counter()
+    rp = to_ref(prob)
+    out = {"n": prob.n}
+    z = np.random.default_rng(SKETCH_SEED).standard_normal(prob.n)
+    guard = ArpackErrorFallback() if idx == 3 else None
+    if guard:
+        guard.__enter__()
+    try:
+        alpha = None
+        for K in Ks:
+            with LambdaRecorder() as rec:
+                res = pdsdp.solve_lr_pd_sdp(rp, to_ref_cfg(cfg, max_iter=K))
+            Xd = res.X.to_dense()
+            out[f"y{K}"] = res.y
+            out[f"lam{K}"] = np.array(rec.values)
+            out[f"res{K}"] = np.array(res.final_residuals)
+            out[f"pobj{K}"] = res.primal_objective
+            out[f"fro{K}"] = np.linalg.norm(Xd)
+            out[f"Xz{K}"] = Xd @ z
+            out[f"diag{K}"] = np.diag(Xd).copy()
+            out[f"rank_path{K}"] = np.array(res.rank_path)
+            print(f"cfg{idx + 1} K={K} {time.perf_counter() - t0:.1f}s res={res.final_residuals}")
+        from pdsdp.problem import estimate_operator_norm
+        out["opnorm"] = estimate_operator_norm(rp, cfg.seed)
+    finally:
+        if guard:
+            guard.__exit__()
+    out["Ks"] = np.array(Ks)
+    np.savez_compressed(path, **out)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true")
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    jobs = {
+        "ops_small": lambda: make_ops_small(os.path.join(HERE, "ops_small.npz")),
+        "lr_small": lambda: make_lr_small(os.path.join(HERE, "lr_small.npz")),
+        "cfg1": lambda: make_cfg1(os.path.join(HERE, "cfg1.npz")),
+    }
+    if a.big:
+        jobs["cfg2"] = lambda: make_sketch(os.path.join(HERE, "cfg2_sketch.npz"), 1, (1, 5))
+        jobs["cfg4"] = lambda: make_sketch(os.path.join(HERE, "cfg4_sketch.npz"), 3, (1, 5))
+        jobs["cfg5"] = lambda: make_sketch(os.path.join(HERE, "cfg5_sketch.npz"), 4, (1, 10))
+        jobs["cfg3"] = lambda: make_sketch(os.path.join(HERE, "cfg3_sketch.npz"), 2, (1, 2))
+    for name, fn in jobs.items():
+        if a.only and name not in a.only.split(","):
+            continue
+        t = time.perf_counter()
+        fn()
+        print(name, f"{time.perf_counter() - t:.1f}s")
