@@ -1,0 +1,21 @@
+# Builds the sm_100a C-ABI library in-tree (travels to the GPU box with the snapshot).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr
+SRC := paper_1810_05231_b200/csrc/pdsdp_b200.cu
+HDR := $(wildcard paper_1810_05231_b200/csrc/*.cuh) include/pdsdp_b200.h
+LIB := paper_1810_05231_b200/libpdsdp_b200.so
+
+all: $(LIB)
+
+$(LIB): $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -Xptxas -v 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+build/ptxas.log: | build
+build:
+	mkdir -p build
+
+clean:
+	rm -f $(LIB)
+
+.PHONY: all clean

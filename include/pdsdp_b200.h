@@ -1,0 +1,117 @@
+/*
+ * pdsdp_b200 — C ABI of the B200 (sm_100a) LR-PD-SDP hot path.
+ *
+ * The reference (`pdsdp`, pure Python) has no FFI layer; its boundary for
+ * this path is the Python function API re-exported in
+ * pkg/src/pdsdp/__init__.py:29-36.  Each entry point below is the native
+ * replacement of one reference interface (cited per function).  Plain C
+ * types only: host pointers, sizes, an opaque handle.  The library owns its
+ * device memory; it never frees caller memory.  Every function returns 0 on
+ * success or a negative PDSDP_E* code; pdsdp_last_error() describes the most
+ * recent failure of the calling thread.
+ *
+ * Data layout at the boundary is the reference's: symmetric matrices packed
+ * as the upper triangle read row by row, off-diagonal entries scaled by
+ * sqrt(2) (pkg/src/pdsdp/symmat.py:50-101); constraint rows as strictly
+ * increasing packed positions with sqrt(2)-scaled values
+ * (pkg/src/pdsdp/problem.py:29-70), stacked [A; G] (problem.py:119-137).
+ */
+#ifndef PDSDP_B200_H
+#define PDSDP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDSDP_OK 0
+#define PDSDP_EINVAL (-1)   /* invalid argument (reference raises ValueError) */
+#define PDSDP_ECUDA (-2)    /* CUDA runtime / launch failure */
+#define PDSDP_ENOMEM (-3)   /* device or host allocation failure */
+#define PDSDP_ERANK (-4)    /* target rank needs an eigen block above PDSDP_BLOCK_MAX */
+
+#define PDSDP_BLOCK_MAX 64
+#define PDSDP_OUT_LEN 16
+
+/* Output slots of one iteration (doubles, PDSDP_OUT_LEN per instance). */
+enum {
+  PDSDP_OUT_EPS_P = 0,   /* ||dX/alpha - M^T dy||   (pdhg.py:204)          */
+  PDSDP_OUT_EPS_D = 1,   /* ||dy/alpha - M dX||     (pdhg.py:205-207)      */
+  PDSDP_OUT_LAMBDA = 2,  /* lambda_{min(r+1,n)} of the projected argument (symmat.py:242-245) */
+  PDSDP_OUT_FINITE = 3,  /* 1 if X+ and y+ are finite (pdhg.py:217-218)    */
+  PDSDP_OUT_PASSES = 4,  /* eigensolver subspace passes                    */
+  PDSDP_OUT_MATVECS = 5, /* operator applications S*Y (b columns each)     */
+  PDSDP_OUT_EIGCONV = 6, /* 1 converged, 2 rounding floor, 0 pass limit    */
+  PDSDP_OUT_EIGRES = 7,  /* worst unconverged relative Ritz residual       */
+  PDSDP_OUT_DENSE = 8,
+  PDSDP_OUT_CORR = 9,
+  PDSDP_OUT_ED2 = 10,
+  PDSDP_OUT_BLOCK = 11   /* eigen block size b                              */
+};
+
+/* One SDP in the reference's general form (problem.py:73-105). */
+typedef struct pdsdp_problem {
+  int32_t n;                /* matrix dimension                           */
+  int32_t m;                /* equality rows  (len(A))                    */
+  int32_t p;                /* inequality rows (len(G))                   */
+  int32_t reserved;
+  const double* C_packed;   /* [n(n+1)/2] objective, packed               */
+  const int64_t* row_ptr;   /* [m+p+1] stacked [A; G] rows                */
+  const int64_t* row_idx;   /* [nnz] packed positions                     */
+  const double* row_val;    /* [nnz] packed values                        */
+  const double* b;          /* [m]                                        */
+  const double* h;          /* [p]                                        */
+} pdsdp_problem;
+
+typedef struct pdsdp_batch pdsdp_batch;
+
+/* Upload `count` independent problems (SdpProblem.stacked, problem.py:119-137;
+ * the re-indexing into dense coordinates happens here, once). */
+int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** out);
+int pdsdp_batch_destroy(pdsdp_batch* b);
+int pdsdp_batch_info(const pdsdp_batch* b, int inst, int64_t* info /* [8] */);
+/* cudaStream_t the batch launches on (for event timing by the caller). */
+void* pdsdp_batch_stream(pdsdp_batch* b);
+
+/* Operator norm by seeded power iteration (problem.py:157-185).  The start
+ * vector is drawn by the caller with the reference's RNG
+ * (numpy default_rng(seed).standard_normal(P), normalised) and passed
+ * restricted to the touched positions returned by pdsdp_opnorm_positions.
+ * Runs `iters` iterations from x0 (x0 == NULL: continue from the device
+ * state) and writes ||M x|| of each into s_out. */
+int pdsdp_opnorm_positions(pdsdp_batch* b, int inst, int64_t* pos_out, int64_t* count);
+int pdsdp_opnorm_run(pdsdp_batch* b, int inst, const double* x0, int iters, double* s_out);
+
+/* Step size alpha (pdhg.py:211-214) and iterate reset X0 = 0, y0 = 0
+ * (lowrank.py:128-135). */
+int pdsdp_set_alpha(pdsdp_batch* b, int inst, double alpha);
+int pdsdp_reset(pdsdp_batch* b, int inst, double seed);
+
+/* One LR-PDHG iteration (lowrank.py:141-150: approximate_primal_step,
+ * dual_step, residuals) for each listed instance.  rank[i], ypar[i], flags[i]
+ * per listed instance; out: nact * PDSDP_OUT_LEN doubles (host). */
+int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank,
+                  const int32_t* ypar, const int32_t* flags, int32_t maxpass, double* out);
+
+/* tr(C X) (lowrank.py:159,168,191) for X = the newest iterate (which = 0)
+ * or the previous one (which = 1). */
+int pdsdp_objective(pdsdp_batch* b, int inst, int which, double* out);
+
+/* Download X packed (symmat.py:66-86 layout) and y. */
+int pdsdp_download_x(pdsdp_batch* b, int inst, int which, double* packed_out);
+int pdsdp_download_y(pdsdp_batch* b, int inst, int ypar, double* y_out);
+
+/* Op-level entry points (reference problem.py:140-154, symmat.py:229-245). */
+int pdsdp_apply_M(pdsdp_batch* b, int inst, const double* X_packed, double* out);
+int pdsdp_apply_M_adjoint(pdsdp_batch* b, int inst, const double* y, double* out_packed);
+int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_packed_out, double* lambda_out);
+
+const char* pdsdp_strerror(int code);
+const char* pdsdp_last_error(void);
+int pdsdp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDSDP_B200_H */

@@ -1,0 +1,110 @@
+// Shared device-side definitions for the B200 LR-PD-SDP hot path.
+//
+// Layout in HBM (per SDP instance, everything FP64, row-major n x ld blocks):
+//   V, AV        Ritz basis of the current PSD-projection argument and S*V
+//   Yb[0..2]     Chebyshev filter recurrence buffers
+//   F            factor of the current iterate X_k = F diag(lamF) F^T
+//   Z CSR        sparse symmetric matrix  Z = C + M^T(y)  in dense (i, j)
+//                coordinates (both triangles), values refreshed every
+//                iteration by the adjoint gather; pattern = union of the
+//                patterns of C and of every constraint row.
+// The projection argument S = X_k - alpha (C + M^T y) is never formed:
+//     S * Y = F (lamF .* (F^T Y)) - alpha * Z * Y
+// which is exact because X_k is the rank-r truncated projection of the
+// previous step (reference symmat.py:212-220 builds it as sum lam u u^T).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define PDSDP_BMAX 64          // largest eigen block (k = r+1 plus guard vectors)
+#define PDSDP_NTHR 512         // threads per CTA of the cluster kernel
+#define PDSDP_RED_MAX (2 * PDSDP_BMAX * PDSDP_BMAX + 64)
+#define PDSDP_OUT_LEN 16       // doubles per instance in the host-mapped output
+
+namespace pdsdp {
+
+struct State {
+  int b;            // current eigen block size
+  int rF;           // columns of the factor produced by the last iteration
+  int theta_valid;  // theta[0..b) are Ritz values of the current V
+  int iav;          // physical buffer (1..4) holding S*V
+  int rF_used;      // columns of F (= X_k) used by the last iteration
+  int r_cur;        // columns of V (= X_k+1) produced by the last iteration
+  int pad0, pad1;
+  double theta[PDSDP_BMAX];
+  double res[PDSDP_BMAX];
+  double lamF[PDSDP_BMAX];   // eigenvalues of X_k   (clipped)
+  double lamN[PDSDP_BMAX];   // eigenvalues of X_k+1 (clipped)
+  double lo;        // lower bound of spec(S) for the Chebyshev interval
+  double ed2;       // sum (dy/alpha - M dX)^2
+  double corr;      // sparse-support correction of the primal residual
+  double finite;    // 1 when y+ and theta are finite
+  double seed;
+};
+
+// Per-instance descriptor (device resident).  Sizes and pointers only.
+struct Inst {
+  int n, m, p, mp, ld, C;
+  int nz;              // slots of the symmetric Z CSR
+  int group;           // lanes per constraint row in the A-map
+  int pad0;
+  const int* zptr;     // [n+1]
+  const int* zcol;     // [nz]
+  const int* zrow;     // [nz]
+  const double* cval;  // [nz] objective entry C_ij at the slot
+  const int* tptr;     // [nz+1] contributors of M^T y to the slot
+  const int* trow;     // constraint row of each contributor
+  const double* tcoef; // scatter coefficient (packed value / s, s = 1 or sqrt 2)
+  double* zval;        // [nz] current Z values
+  const int* aptr;     // [mp+1] constraint rows in dense coordinates
+  const int* ai;
+  const int* aj;
+  const double* ag;    // gather coefficient (packed value * s)
+  const int* asplit;   // [C+1] constraint-row range of each CTA
+  const double* bv;    // [m]
+  const double* hv;    // [p]
+  double alpha;
+  double* V;
+  double* AV;
+  double* Y0;
+  double* Y1;
+  double* Y2;
+  double* F;
+  double* ybuf0;
+  double* ybuf1;
+  double* dy;
+  double* red;         // [2][C][RED_MAX] cluster reduction scratch
+  double* rpart;       // residual kernel tile partials
+  unsigned int* rcount;
+  State* st;
+  double* out;         // host-mapped [OUT_LEN]
+};
+
+// Per-launch control for one instance.
+struct Ctl {
+  int r;       // target rank for this iteration
+  int ypar;    // y_k lives in ybuf[ypar], y_{k+1} goes to ybuf[ypar^1]
+  int flags;   // bit0: cold start (reset V/theta)
+  int maxpass;
+};
+
+// output slots
+enum { O_EPS_P = 0, O_EPS_D, O_LAM, O_FIN, O_PASSES, O_MATVECS, O_EIGCONV, O_EIGRES,
+       O_DENSE, O_CORR, O_ED2, O_BLK };
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// deterministic counter-based uniform(-1, 1)
+__device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t a, uint64_t b) {
+  uint64_t x = seed * 0x9E3779B97F4A7C15ull ^ (a * 0xBF58476D1CE4E5B9ull) ^ (b * 0x94D049BB133111EBull + 0x632BE59BD9B4E019ull);
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27; x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return ((double)(x >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+}
+
+}  // namespace pdsdp

@@ -1,0 +1,597 @@
+// One LR-PDHG iteration per thread-block cluster (one cluster per SDP
+// instance): the body of the `for k` loop of the reference's
+// solve_lr_pd_sdp (pkg/src/pdsdp/lowrank.py:140-150):
+//
+//   S      = X_k - alpha (C + M^T y_k)                        lowrank.py:97-98
+//   X_k+1  = aproj_psd(S, r)  (top r+1 eigenpairs, clip)      symmat.py:229-245
+//   y_k+1  = u - alpha proj_box(u/alpha), u = y + alpha M(2X_k+1 - X_k)
+//                                                             pdhg.py:185-195
+//   residual pieces (dual part + sparse-support primal part)  pdhg.py:198-208
+//
+// The dense part of the primal residual is finished by residual_kernel
+// (residual.cuh) on the whole GPU.  Cross-CTA reductions go through L2 with
+// one cluster barrier each (release/acquire at cluster scope); every CTA then
+// sums the C partials in the same order, so all CTAs hold bit-identical
+// reduced values and run the small dense algebra redundantly.
+#pragma once
+#include <cooperative_groups.h>
+#include "common.cuh"
+#include "small_dense.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pdsdp {
+
+// tolerances of the eigensolver (relative to the spectral scale)
+#define PDSDP_TOL_KEEP 1e-13
+#define PDSDP_TOL_CERT 1e-8
+#define PDSDP_MMAX 24
+
+struct Sm {
+  double *A, *Q, *L, *M, *T;   // lds x lds each
+  double *scr;                 // NTHR
+  double *theta, *res, *lamF, *lamN, *dsc, *cs, *red1;  // BMAX each (red1: 2*BMAX)
+  int *perm, *pq, *flag;
+  int lds;
+};
+
+struct Cta {
+  int C, c, r0, r1, par;
+};
+
+__device__ __forceinline__ double* red_slot(const Inst& d, const Cta& x, int cc) {
+  return d.red + ((size_t)x.par * x.C + cc) * PDSDP_RED_MAX;
+}
+
+// Finish a cluster reduction whose per-CTA partial (q_sum sums followed by
+// q_max maxima) is already in red_slot(x, x.c).  Result -> dst (smem).
+__device__ void cluster_reduce(const Inst& d, Cta& x, int q_sum, int q_max, double* dst) {
+  cg::this_cluster().sync();
+  const int q = q_sum + q_max;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    double s = (i < q_sum) ? 0.0 : -1.0e308;
+    for (int cc = 0; cc < x.C; ++cc) {
+      double v = red_slot(d, x, cc)[i];
+      s = (i < q_sum) ? s + v : fmax(s, v);
+    }
+    dst[i] = s;
+  }
+  x.par ^= 1;
+  __syncthreads();
+}
+
+// partial[o] = sum over own rows of A[rho, i] * B[rho, j], o = off + i*nb + j.
+// Written to the global reduction slot (deterministic, one finisher per o).
+__device__ void gram_partial(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
+                             int ld, int r0, int r1, double* gout, double* scr) {
+  const int q = na * nb;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (q == 0) return;
+  if (q >= nt / 2) {
+    for (int o = tid; o < q; o += nt) {
+      const int i = o / nb, j = o % nb;
+      double s = 0.0;
+      for (int rho = r0; rho < r1; ++rho) s = fma(A[(size_t)rho * ld + i], B[(size_t)rho * ld + j], s);
+      gout[o] = s;
+    }
+  } else {
+    const int S = nt / q;
+    const int o = tid % q, sl = tid / q;
+    double s = 0.0;
+    if (sl < S) {
+      const int i = o / nb, j = o % nb;
+      for (int rho = r0 + sl; rho < r1; rho += S) s = fma(A[(size_t)rho * ld + i], B[(size_t)rho * ld + j], s);
+    }
+    scr[tid] = s;
+    __syncthreads();
+    if (tid < q) {
+      double t = 0.0;
+      for (int k = 0; k < S; ++k) t += scr[k * q + tid];
+      gout[tid] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// column sums of squares of (P[:, j] - th[j] * Q[:, j]) over own rows
+__device__ void colres_partial(const double* __restrict__ P, const double* __restrict__ Qm,
+                               const double* th, int b, int ld, int r0, int r1, double* gout, double* scr) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int S = nt / b;
+  const int j = tid % b, sl = tid / b;
+  double s = 0.0;
+  if (sl < S) {
+    const double t = th[j];
+    for (int rho = r0 + sl; rho < r1; rho += S) {
+      double v = P[(size_t)rho * ld + j] - t * Qm[(size_t)rho * ld + j];
+      s = fma(v, v, s);
+    }
+  }
+  scr[tid] = s;
+  __syncthreads();
+  if (tid < b) {
+    double t = 0.0;
+    for (int k = 0; k < S; ++k) t += scr[k * b + tid];
+    gout[tid] = t;
+  }
+  __syncthreads();
+}
+
+// out = ca * (S Yin) + cb * Yin + cd * Yprev  on own rows, where
+// S Yin = F (LT) - alpha Z Yin  and LT = diag(lamF) F^T Yin (in smem).
+__device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ Yin,
+                           const double* __restrict__ Yprev, double* __restrict__ out, int b, int rF,
+                           double ca, double cb, double cd) {
+  const int ld = d.ld;
+  const int nl = x.r1 - x.r0;
+  const double alpha = d.alpha;
+  for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
+    const int rho = x.r0 + it / b, j = it % b;
+    double w = 0.0;
+    const double* Fr = d.F + (size_t)rho * ld;
+    for (int l = 0; l < rF; ++l) w = fma(Fr[l], s.T[l * b + j], w);
+    double z = 0.0;
+    const int e1 = d.zptr[rho + 1];
+    for (int e = d.zptr[rho]; e < e1; ++e) z = fma(d.zval[e], Yin[(size_t)d.zcol[e] * ld + j], z);
+    w = fma(-alpha, z, w);
+    double o = ca * w;
+    if (cb != 0.0) o = fma(cb, Yin[(size_t)rho * ld + j], o);
+    if (cd != 0.0) o = fma(cd, Yprev[(size_t)rho * ld + j], o);
+    out[(size_t)rho * ld + j] = o;
+  }
+}
+
+// out = In * Msm (b x b in smem), own rows; In and out must differ.
+__device__ void rotate_rows(const Inst& d, const Cta& x, const double* __restrict__ In, const double* Msm,
+                            int lds, double* __restrict__ out, int b) {
+  const int ld = d.ld;
+  const int nl = x.r1 - x.r0;
+  for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
+    const int rho = x.r0 + it / b, j = it % b;
+    const double* row = In + (size_t)rho * ld;
+    double acc = 0.0;
+    for (int t = 0; t < b; ++t) acc = fma(row[t], Msm[t * lds + j], acc);
+    out[(size_t)rho * ld + j] = acc;
+  }
+}
+
+// T (smem, rF x b) <- lamF .* T  (in place): LT used by apply_rows
+__device__ void scale_T(const Sm& s, int rF, int b) {
+  for (int e = threadIdx.x; e < rF * b; e += blockDim.x) {
+    s.T[e] *= s.lamF[e / b];
+  }
+  __syncthreads();
+}
+
+__device__ int choose_block(int k, int n) {
+  int g = k / 4;
+  if (g < 4) g = 4;
+  int b = k + g;
+  b = (b + 3) & ~3;
+  if (b > PDSDP_BMAX) b = PDSDP_BMAX;
+  if (b > n) b = n;
+  return b;
+}
+
+__global__ void __launch_bounds__(PDSDP_NTHR, 1)
+lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,
+                      const int* __restrict__ active, int lds) {
+  extern __shared__ __align__(16) double smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  Cta x;
+  x.C = (int)cl.num_blocks();
+  x.c = (int)cl.block_rank();
+  const int inst_id = active[blockIdx.x / x.C];
+  const Inst d = insts[inst_id];
+  const Ctl ctl = ctls[inst_id];
+  State* st = d.st;
+  const int n = d.n, ld = d.ld, tid = threadIdx.x;
+  x.r0 = (int)(((long long)n * x.c) / x.C);
+  x.r1 = (int)(((long long)n * (x.c + 1)) / x.C);
+  x.par = 0;
+
+  Sm s;
+  s.lds = lds;
+  {
+    double* p = smem;
+    const int sq = lds * lds;
+    s.A = p; p += sq; s.Q = p; p += sq; s.L = p; p += sq; s.M = p; p += sq; s.T = p; p += sq;
+    s.scr = p; p += PDSDP_NTHR;
+    s.theta = p; p += PDSDP_BMAX; s.res = p; p += PDSDP_BMAX; s.lamF = p; p += PDSDP_BMAX;
+    s.lamN = p; p += PDSDP_BMAX; s.dsc = p; p += PDSDP_BMAX; s.cs = p; p += 2 * PDSDP_BMAX;
+    s.red1 = p; p += 4 * PDSDP_BMAX;
+    int* ip = (int*)p;
+    s.perm = ip; ip += PDSDP_BMAX; s.pq = ip; ip += 2 * PDSDP_BMAX; s.flag = ip; ip += 8;
+  }
+  double* buf[5] = {d.V, d.AV, d.Y0, d.Y1, d.Y2};
+
+  // ---------------- prologue: F <- V[:, :rF] (X_k), block setup ----------------
+  const int r = ctl.r;
+  const int k = (r + 1 < n) ? r + 1 : n;
+  const bool cold = (ctl.flags & 1) || st->b == 0;
+  const int rF = cold ? 0 : st->rF;
+  const int b_old = cold ? 0 : st->b;
+  int b = choose_block(k, n);
+  if (b < b_old) b = b_old;
+  int iav = cold ? 1 : st->iav;   // physical buffer holding AV
+  if (iav < 1 || iav > 4) iav = 1;
+  bool theta_valid = !cold && st->theta_valid && b == b_old;
+  for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
+    double th = (!cold && i < b_old) ? st->theta[i] : 0.0;
+    s.theta[i] = th;
+    s.lamF[i] = (i < rF) ? fmax(th, 0.0) : 0.0;
+    s.res[i] = (!cold && i < b_old) ? st->res[i] : 1.0e300;
+  }
+  const double lo = st->lo;
+  const double alpha = d.alpha;
+  for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
+    const int rho = x.r0 + it / b, j = it % b;
+    double* Vr = d.V + (size_t)rho * ld;
+    if (j < rF) d.F[(size_t)rho * ld + j] = Vr[j];
+    if (j >= b_old) Vr[j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
+  }
+  __syncthreads();
+  if (x.c == 0 && tid < PDSDP_BMAX) st->lamF[tid] = s.lamF[tid];
+  if (x.c == 0 && tid == 0) { st->rF_used = rF; st->r_cur = r; }
+
+  // ---------------- eigensolver: warm-started Chebyshev-filtered subspace iteration ----
+  bool av_valid = false;
+  int passes = 0, matvecs = 0, converged = 0;
+  double prev_maxres = 1.0e300, maxres = 1.0e300;
+  const int maxpass = ctl.maxpass > 0 ? ctl.maxpass : 60;
+  int mfail = 0;
+  for (int pass = 0; pass < maxpass; ++pass) {
+    // ---- filter parameters (identical in every thread) ----
+    int m = 0;
+    double fe = 1.0, fc = 0.0, sig1 = 1.0;
+    if (theta_valid && b < n) {
+      double cut = s.theta[b - 1], top = s.theta[0];
+      double scale = fmax(fmax(fabs(top), fabs(lo)), 1e-300);
+      double lo_ = fmin(lo, cut);
+      fe = 0.5 * (cut - lo_);
+      fc = 0.5 * (cut + lo_);
+      if (fe < 1e-14 * scale) fe = 1e-14 * scale;
+      if (top - fc <= fe) top = fc + 1.0001 * fe;
+      sig1 = fe / (top - fc);
+      // slowest still-needed column and required reduction
+      double rho_need = 1.0, tmin = 1.0e300;
+      for (int i = 0; i < k; ++i) {
+        double tol = (i < r ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) * scale;
+        double ri = s.res[i];
+        bool ok = (ri <= tol) || (s.theta[i] + ri < 0.0) || (fabs(s.theta[i]) + ri <= 1e-10 * scale);
+        if (!ok) {
+          rho_need = fmax(rho_need, ri / tol);
+          double t = (s.theta[i] - fc) / fe;
+          tmin = fmin(tmin, t);
+        }
+      }
+      if (rho_need <= 1.0) { m = 0; }
+      else {
+        double at = (tmin > 1.0 + 1e-6) ? acosh(tmin) : 0.0;
+        m = (at > 0.0) ? (int)ceil(acosh(rho_need) / at) + 1 : 8;
+        double t1 = (top - fc) / fe;
+        double spread = acosh(fmax(t1, 1.0 + 1e-6)) - ((tmin > 1.0 + 1e-6) ? acosh(tmin) : 0.0);
+        double eps_rel = fmin(fmax(maxres / scale, 1e-16), 1.0);
+        if (spread > 1e-3) {
+          int mcap = (int)floor(log(1e4 / eps_rel) / spread);
+          if (mcap < 2) mcap = 2;
+          if (m > mcap) m = mcap;
+        }
+        if (m < 2) m = 2;
+        if (m > PDSDP_MMAX) m = PDSDP_MMAX;
+        if (mfail) m = max(1, m >> mfail);
+      }
+    }
+    // ---- Chebyshev filter  Y_m = p_m(S) V ----
+    int iy = 0;                       // buffer index holding Y_j (0 == V)
+    int iyp = -1;                     // buffer holding Y_{j-1}
+    int fre[3], nf = 0;
+    for (int q = 1; q <= 4; ++q) if (q != iav) fre[nf++] = q;
+    if (m > 0) {
+      double sg = sig1;
+      for (int j = 1; j <= m; ++j) {
+        int io = fre[(j - 1) % 3];
+        if (j == 1) {
+          const double ca = sig1 / fe, cb = -fc * sig1 / fe;
+          if (av_valid) {
+            for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
+              const size_t o = (size_t)(x.r0 + it / b) * ld + it % b;
+              buf[io][o] = fma(ca, buf[iav][o], cb * d.V[o]);
+            }
+          } else {
+            gram_partial(d.F, rF, d.V, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
+            cluster_reduce(d, x, rF * b, 0, s.T);
+            scale_T(s, rF, b);
+            apply_rows(d, x, s, d.V, nullptr, buf[io], b, rF, ca, cb, 0.0);
+            ++matvecs;
+          }
+        } else {
+          const double sn = 1.0 / (2.0 / sig1 - sg);
+          const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
+          gram_partial(d.F, rF, buf[iy], b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
+          cluster_reduce(d, x, rF * b, 0, s.T);
+          scale_T(s, rF, b);
+          apply_rows(d, x, s, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], b, rF, ca, cb, cd);
+          ++matvecs;
+          sg = sn;
+        }
+        iyp = iy;
+        iy = io;
+        __syncthreads();
+      }
+    }
+    // ---- R1: G1 = Y^T Y, T = F^T Y ; W = S Y ----
+    const int iw = (iy == 0) ? fre[0] : fre[(m) % 3];          // free of {Y_m, Y_{m-1}} ring
+    int iw1 = -1;
+    for (int q2 = 0; q2 < 3; ++q2) if (fre[q2] != iy && fre[q2] != iw) { iw1 = fre[q2]; break; }
+    {
+      double* slot = red_slot(d, x, x.c);
+      gram_partial(buf[iy], b, buf[iy], b, ld, x.r0, x.r1, slot, s.scr);
+      gram_partial(d.F, rF, buf[iy], b, ld, x.r0, x.r1, slot + b * b, s.scr);
+      // reduce into A (G1) and T
+      cg::this_cluster().sync();
+      const int q = b * b + rF * b;
+      for (int i = tid; i < q; i += blockDim.x) {
+        double acc = 0.0;
+        for (int cc = 0; cc < x.C; ++cc) acc += red_slot(d, x, cc)[i];
+        if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
+        else s.T[i - b * b] = acc;
+      }
+      x.par ^= 1;
+      __syncthreads();
+    }
+    scale_T(s, rF, b);
+    apply_rows(d, x, s, buf[iy], nullptr, buf[iw], b, rF, 1.0, 0.0, 0.0);
+    ++matvecs;
+    // ---- small: M1 = D L^-T ----
+    bool okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
+    if (!okc) {
+      // breakdown: filtered block lost rank; retry from V with a lower degree
+      mfail += 1;
+      theta_valid = theta_valid && (mfail < 6);
+      if (mfail >= 8) break;
+      __syncthreads();
+      continue;
+    }
+    tri_inv_lower(s.A, s.L, b, lds);
+    for (int e = tid; e < b * b; e += blockDim.x) {
+      int i = e / b, j = e % b;
+      s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
+    }
+    __syncthreads();
+    // Y1 = Y M1 -> buf[iav] ; W1 = W M1 -> buf[iw1]
+    rotate_rows(d, x, buf[iy], s.M, lds, buf[iav], b);
+    rotate_rows(d, x, buf[iw], s.M, lds, buf[iw1], b);
+    __syncthreads();
+    // ---- R2: G2 = Y1^T Y1, H = Y1^T W1 ----
+    {
+      double* slot = red_slot(d, x, x.c);
+      gram_partial(buf[iav], b, buf[iav], b, ld, x.r0, x.r1, slot, s.scr);
+      gram_partial(buf[iav], b, buf[iw1], b, ld, x.r0, x.r1, slot + b * b, s.scr);
+      cg::this_cluster().sync();
+      const int q = 2 * b * b;
+      for (int i = tid; i < q; i += blockDim.x) {
+        double acc = 0.0;
+        for (int cc = 0; cc < x.C; ++cc) acc += red_slot(d, x, cc)[i];
+        if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
+        else { int e = i - b * b; s.Q[(e / b) * lds + (e % b)] = acc; }
+      }
+      x.par ^= 1;
+      __syncthreads();
+    }
+    // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe
+    okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
+    if (!okc) { mfail += 1; if (mfail >= 8) break; continue; }
+    tri_inv_lower(s.A, s.L, b, lds);            // L = L2^-1
+    for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
+      int i = e / b, j = e % b;
+      s.Q[i * lds + j] *= s.dsc[i] * s.dsc[j];
+    }
+    __syncthreads();
+    sm_gemm(s.L, lds, s.Q, lds, s.M, lds, b, b, b);            // M = L^-1 (DHD)
+    for (int e = tid; e < b * b; e += blockDim.x) {           // A = M L^-T
+      int i = e / b, j = e % b;
+      double acc = 0.0;
+      for (int t = 0; t < b; ++t) acc += s.M[i * lds + t] * s.L[j * lds + t];
+      s.A[i * lds + j] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < b * b; e += blockDim.x) {           // symmetrise
+      int i = e / b, j = e % b;
+      if (j > i) { double v = 0.5 * (s.A[i * lds + j] + s.A[j * lds + i]); s.A[i * lds + j] = v; s.A[j * lds + i] = v; }
+    }
+    __syncthreads();
+    jacobi_eig(s.A, s.Q, b, lds, s.cs, s.pq, s.flag);
+    sort_desc(s.A, b, lds, s.theta, s.perm);
+    // B = D L^-T Q[:, perm]  -> s.M
+    for (int e = tid; e < b * b; e += blockDim.x) {
+      int i = e / b, j = e % b;
+      const int pj = s.perm[j];
+      double acc = 0.0;
+      for (int t = i; t < b; ++t) acc += s.L[t * lds + i] * s.Q[t * lds + pj];
+      s.M[i * lds + j] = s.dsc[i] * acc;
+    }
+    __syncthreads();
+    // V = Y1 B ; AV = W1 B  (AV goes to buf[iw], which becomes the AV buffer)
+    rotate_rows(d, x, buf[iav], s.M, lds, d.V, b);
+    rotate_rows(d, x, buf[iw1], s.M, lds, buf[iw], b);
+    iav = iw;
+    av_valid = true;
+    theta_valid = true;
+    __syncthreads();
+    // ---- R3: residual norms ----
+    colres_partial(buf[iav], d.V, s.theta, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
+    cluster_reduce(d, x, b, 0, s.red1);
+    ++passes;
+    {
+      double scale = fmax(fmax(fabs(s.theta[0]), fabs(lo)), 1e-300);
+      bool ok_all = true;
+      maxres = 0.0;
+      for (int i = 0; i < b; ++i) {
+        double ri = sqrt(fmax(s.red1[i], 0.0));
+        if (tid == 0) s.res[i] = ri;   // only thread 0 writes; reads below use ri
+        if (i < k) {
+          double tol = (i < r ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) * scale;
+          bool ok = (ri <= tol) || (s.theta[i] + ri < 0.0) || (fabs(s.theta[i]) + ri <= 1e-10 * scale);
+          if (!ok) { ok_all = false; maxres = fmax(maxres, ri / scale); }
+        }
+        if (!isfinite(s.theta[i]) || !isfinite(ri)) ok_all = true;  // give up on non-finite
+      }
+      __syncthreads();
+      if (ok_all) { converged = 1; break; }
+      // stagnation at the rounding floor
+      if (pass >= 2 && maxres > 0.5 * prev_maxres && maxres < 1e-10) { converged = 2; break; }
+      prev_maxres = maxres;
+      mfail = 0;
+    }
+  }
+  for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) s.lamN[i] = (i < r && i < b) ? fmax(s.theta[i], 0.0) : 0.0;
+  __syncthreads();
+
+  // ---------------- dual step: y+ = u - alpha proj_box(u/alpha) ----------------
+  const double* yk = ctl.ypar ? d.ybuf1 : d.ybuf0;
+  double* yn = ctl.ypar ? d.ybuf0 : d.ybuf1;
+  const int rN = (r < b) ? r : b;
+  double ed2 = 0.0, fin = 1.0;
+  {
+    const int G = d.group;
+    const int lane = tid & 31, sub = lane % G;
+    const int gid = tid / G, ng = blockDim.x / G;
+    const int a0 = d.asplit[x.c], a1 = d.asplit[x.c + 1];
+    for (int i0 = a0; i0 < a1; i0 += ng) {
+      const int i = i0 + gid;
+      double s2 = 0.0, sd = 0.0;
+      if (i < a1) {
+        for (int e = d.aptr[i] + sub; e < d.aptr[i + 1]; e += G) {
+          const int p = d.ai[e], q = d.aj[e];
+          const double* Vp = d.V + (size_t)p * ld; const double* Vq = d.V + (size_t)q * ld;
+          const double* Fp = d.F + (size_t)p * ld; const double* Fq = d.F + (size_t)q * ld;
+          double xn = 0.0, xo = 0.0;
+          for (int l = 0; l < rN; ++l) xn = fma(Vp[l] * s.lamN[l], Vq[l], xn);
+          for (int l = 0; l < rF; ++l) xo = fma(Fp[l] * s.lamF[l], Fq[l], xo);
+          const double g = d.ag[e];
+          s2 = fma(g, 2.0 * xn - xo, s2);
+          sd = fma(g, xn - xo, sd);
+        }
+      }
+      for (int o = G >> 1; o > 0; o >>= 1) {
+        s2 += __shfl_down_sync(0xffffffffu, s2, o, G);
+        sd += __shfl_down_sync(0xffffffffu, sd, o, G);
+      }
+      if (i < a1 && sub == 0) {
+        const double u = yk[i] + alpha * s2;
+        const double pr = (i < d.m) ? d.bv[i] : fmin(u / alpha, d.hv[i - d.m]);
+        const double ynew = u - alpha * pr;
+        const double dyi = ynew - yk[i];
+        yn[i] = ynew;
+        d.dy[i] = dyi;
+        const double t = dyi / alpha - sd;
+        ed2 = fma(t, t, ed2);
+        if (!isfinite(ynew)) fin = 0.0;
+      }
+    }
+  }
+  // block reduce ed2 (sum), fin (min -> use max of negatives)
+  {
+    double v = warp_sum(ed2);
+    double f = fin;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f = fmin(f, __shfl_xor_sync(0xffffffffu, f, o));
+    if ((tid & 31) == 0) { s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = f; }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, ff = 1.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; ff = fmin(ff, s.scr[32 + w]); }
+      double* slot = red_slot(d, x, x.c);
+      slot[0] = a;
+      slot[1] = -ff;   // max of -fin
+    }
+    __syncthreads();
+  }
+  cluster_reduce(d, x, 1, 1, s.red1);
+  const double ed2_tot = s.red1[0];
+  double fin_tot = -s.red1[1];
+  for (int i = 0; i < b; ++i) if (!isfinite(s.theta[i])) fin_tot = 0.0;
+
+  // ---------------- adjoint gather: Z_{k+1} = C + M^T y+, support correction ----------------
+  double corr = 0.0;
+  {
+    const int e0 = d.zptr[x.r0], e1 = d.zptr[x.r1];
+    for (int e = e0 + tid; e < e1; e += blockDim.x) {
+      double z = d.cval[e], a = 0.0;
+      for (int t = d.tptr[e]; t < d.tptr[e + 1]; ++t) {
+        const int row = d.trow[t];
+        const double cf = d.tcoef[t];
+        z = fma(yn[row], cf, z);
+        a = fma(d.dy[row], cf, a);
+      }
+      d.zval[e] = z;
+      const int i = d.zrow[e], j = d.zcol[e];
+      if (j >= i) {
+        const double* Vi = d.V + (size_t)i * ld; const double* Vj = d.V + (size_t)j * ld;
+        const double* Fi = d.F + (size_t)i * ld; const double* Fj = d.F + (size_t)j * ld;
+        double xn = 0.0, xo = 0.0;
+        for (int l = 0; l < rN; ++l) xn = fma(Vi[l] * s.lamN[l], Vj[l], xn);
+        for (int l = 0; l < rF; ++l) xo = fma(Fi[l] * s.lamF[l], Fj[l], xo);
+        const double v = (xn - xo) / alpha;
+        const double w = (i == j) ? 1.0 : 2.0;
+        corr = fma(w * a, a - 2.0 * v, corr);
+      }
+    }
+  }
+  __syncthreads();
+  double gmax = 0.0;
+  for (int rho = x.r0 + tid; rho < x.r1; rho += blockDim.x) {
+    double sacc = 0.0;
+    for (int e = d.zptr[rho]; e < d.zptr[rho + 1]; ++e) sacc += fabs(d.zval[e]);
+    gmax = fmax(gmax, sacc);
+  }
+  {
+    double v = warp_sum(corr);
+    double g = gmax;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if ((tid & 31) == 0) { s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = g; }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, gg = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; gg = fmax(gg, s.scr[32 + w]); }
+      double* slot = red_slot(d, x, x.c);
+      slot[0] = a;
+      slot[1] = gg;
+    }
+    __syncthreads();
+  }
+  cluster_reduce(d, x, 1, 1, s.red1);
+
+  // ---------------- epilogue: state for the next iteration + scalars ----------------
+  if (x.c == 0) {
+    for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
+      st->theta[i] = (i < b) ? s.theta[i] : 0.0;
+      st->res[i] = (i < b) ? s.res[i] : 0.0;
+      st->lamN[i] = s.lamN[i];
+    }
+    if (tid == 0) {
+      st->b = b;
+      st->rF = rN;
+      st->theta_valid = theta_valid ? 1 : 0;
+      st->iav = iav;
+      st->ed2 = ed2_tot;
+      st->corr = s.red1[0];
+      st->lo = -alpha * s.red1[1];
+      st->finite = fin_tot;
+      double* o = d.out;
+      o[O_LAM] = s.theta[k - 1];
+      o[O_FIN] = fin_tot;
+      o[O_PASSES] = passes;
+      o[O_MATVECS] = matvecs;
+      o[O_EIGCONV] = converged;
+      o[O_EIGRES] = maxres;
+      o[O_ED2] = ed2_tot;
+      o[O_CORR] = s.red1[0];
+      o[O_BLK] = b;
+    }
+  }
+}
+
+}  // namespace pdsdp

@@ -1,0 +1,706 @@
+// Host runtime + C ABI of the B200 LR-PD-SDP hot path (see include/pdsdp_b200.h).
+//
+// Responsibilities:
+//   * one-time re-indexing of the reference's packed problem layout
+//     (problem.py:119-137) into dense (i, j) coordinates: the symmetric Z
+//     pattern, per-slot adjoint contributor lists, constraint rows with
+//     gather coefficients, the touched-position space of the operator norm;
+//   * one device arena per instance, descriptors, host-mapped outputs;
+//   * launching the cluster iteration kernel and the whole-GPU residual kernel.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pdsdp_b200.h"
+#include "common.cuh"
+#include "iterate.cuh"
+#include "opnorm.cuh"
+#include "residual.cuh"
+
+using namespace pdsdp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(PDSDP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0, cap = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T) + 16;
+    return p;
+  }
+};
+
+struct Instance {
+  int n = 0, m = 0, p = 0, mp = 0, ld = 0;
+  long long nz = 0;
+  int group = 1;
+  int ntile = 0;
+  // host copies of the re-indexed problem
+  std::vector<int> zptr, zcol, zrow, tptr, trow, aptr, ai, aj;
+  std::vector<double> cval, tcoef, ag, bv, hv;
+  // operator-norm T-space
+  std::vector<long long> tpos;
+  std::vector<int> o_seg_lo, o_seg_hi, o_row_seg, o_mcol, o_tptr, o_trow;
+  std::vector<double> o_mval, o_tval;
+  // device
+  void* dmem = nullptr;
+  size_t dbytes = 0;
+  Inst desc{};
+  OpnormDev od{};
+  double* d_packed = nullptr;   // scratch packed vector (op-level maps)
+  long long P = 0;
+};
+
+}  // namespace
+
+struct pdsdp_batch {
+  std::vector<Instance*> inst;
+  int C = 1, lds = 4;
+  size_t smem = 0;
+  cudaStream_t stream = nullptr;
+  Inst* d_insts = nullptr;
+  Ctl* h_ctl = nullptr;
+  Ctl* d_ctl = nullptr;
+  int* h_active = nullptr;
+  int* d_active = nullptr;
+  double* h_out = nullptr;   // mapped pinned, count * OUT_LEN
+  double* d_out = nullptr;
+  double* d_objpart = nullptr;
+  unsigned* d_objcnt = nullptr;
+  double* d_objres = nullptr;
+  int max_tiles = 1;
+};
+
+namespace {
+
+inline long long packed_len(long long n) { return n * (n + 1) / 2; }
+
+int build_instance(const pdsdp_problem& pr, Instance& I) {
+  const int n = pr.n, m = pr.m, p = pr.p;
+  if (n < 1) return fail(PDSDP_EINVAL, "matrix dimension must be positive");
+  if (m < 0 || p < 0) return fail(PDSDP_EINVAL, "negative constraint count");
+  if (!pr.C_packed) return fail(PDSDP_EINVAL, "C_packed is NULL");
+  const int mp = m + p;
+  const long long P = packed_len(n);
+  I.n = n; I.m = m; I.p = p; I.mp = mp; I.P = P;
+  const int bcap = std::min(n, PDSDP_BMAX);
+  I.ld = (bcap + 1) & ~1;
+  std::vector<long long> rstart(n + 1);
+  for (long long i = 0; i <= n; ++i) rstart[i] = i * n - i * (i - 1) / 2;
+  auto coords = [&](long long pos, int& i, int& j) {
+    int ii = (int)(std::upper_bound(rstart.begin(), rstart.begin() + n, pos) - rstart.begin()) - 1;
+    i = ii;
+    j = (int)(pos - rstart[ii] + ii);
+  };
+  const long long nnz = mp ? pr.row_ptr[mp] : 0;
+  if (mp && (!pr.row_ptr || (nnz && (!pr.row_idx || !pr.row_val))))
+    return fail(PDSDP_EINVAL, "constraint arrays are NULL");
+  for (int r = 0; r < mp; ++r) {
+    if (pr.row_ptr[r + 1] < pr.row_ptr[r]) return fail(PDSDP_EINVAL, "row_ptr not monotone");
+    for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) {
+      if (pr.row_idx[e] < 0 || pr.row_idx[e] >= P) return fail(PDSDP_EINVAL, "constraint row index out of range");
+      if (e > pr.row_ptr[r] && pr.row_idx[e] <= pr.row_idx[e - 1])
+        return fail(PDSDP_EINVAL, "indices must be strictly increasing");
+    }
+  }
+  // ---- support = nonzeros of C  U  positions of all constraint entries ----
+  std::vector<int> sid(P, -1);
+  std::vector<long long> spos;
+  {
+    std::vector<unsigned char> mark(P, 0);
+    for (long long q = 0; q < P; ++q) if (pr.C_packed[q] != 0.0) mark[q] = 1;
+    for (long long e = 0; e < nnz; ++e) mark[pr.row_idx[e]] = 1;
+    for (long long q = 0; q < P; ++q) if (mark[q]) { sid[q] = (int)spos.size(); spos.push_back(q); }
+  }
+  const long long U = (long long)spos.size();
+  // contributors per support entry
+  std::vector<int> ccount(U + 1, 0);
+  for (long long e = 0; e < nnz; ++e) ccount[sid[pr.row_idx[e]] + 1]++;
+  for (long long u = 0; u < U; ++u) ccount[u + 1] += ccount[u];
+  std::vector<int> crow(nnz);
+  std::vector<double> ccoef(nnz);
+  {
+    std::vector<int> fillp(ccount.begin(), ccount.end() - 1);
+    for (int r = 0; r < mp; ++r)
+      for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) {
+        int i, j;
+        coords(pr.row_idx[e], i, j);
+        const int u = sid[pr.row_idx[e]];
+        crow[fillp[u]] = r;
+        ccoef[fillp[u]] = (i == j) ? pr.row_val[e] : pr.row_val[e] / std::sqrt(2.0);
+        fillp[u]++;
+      }
+  }
+  // ---- symmetric CSR in dense coordinates ----
+  std::vector<int> si(U), sj(U);
+  std::vector<long long> rowcnt(n + 1, 0);
+  for (long long u = 0; u < U; ++u) {
+    int i, j;
+    coords(spos[u], i, j);
+    si[u] = i; sj[u] = j;
+    rowcnt[i + 1]++;
+    if (i != j) rowcnt[j + 1]++;
+  }
+  for (int i = 0; i < n; ++i) rowcnt[i + 1] += rowcnt[i];
+  const long long nz = rowcnt[n];
+  if (nz >= (1ll << 31) || nnz >= (1ll << 31)) return fail(PDSDP_EINVAL, "problem too large for int32 indexing");
+  I.nz = nz;
+  I.zptr.assign(rowcnt.begin(), rowcnt.end());
+  I.zcol.resize(nz); I.zrow.resize(nz); I.cval.resize(nz);
+  std::vector<long long> slot_u(nz);
+  {
+    std::vector<long long> fillp(rowcnt.begin(), rowcnt.end() - 1);
+    for (long long u = 0; u < U; ++u) {
+      const int i = si[u], j = sj[u];
+      const double c = (i == j) ? pr.C_packed[spos[u]] : pr.C_packed[spos[u]] / std::sqrt(2.0);
+      long long s = fillp[i]++;
+      I.zcol[s] = j; I.zrow[s] = i; I.cval[s] = c; slot_u[s] = u;
+      if (i != j) {
+        s = fillp[j]++;
+        I.zcol[s] = i; I.zrow[s] = j; I.cval[s] = c; slot_u[s] = u;
+      }
+    }
+  }
+  I.tptr.assign(nz + 1, 0);
+  for (long long s = 0; s < nz; ++s) I.tptr[s + 1] = I.tptr[s] + (ccount[slot_u[s] + 1] - ccount[slot_u[s]]);
+  if ((long long)I.tptr[nz] >= (1ll << 31)) return fail(PDSDP_EINVAL, "too many adjoint contributors");
+  I.trow.resize(I.tptr[nz]); I.tcoef.resize(I.tptr[nz]);
+  for (long long s = 0; s < nz; ++s) {
+    const long long u = slot_u[s];
+    int o = I.tptr[s];
+    for (int c = ccount[u]; c < ccount[u + 1]; ++c, ++o) { I.trow[o] = crow[c]; I.tcoef[o] = ccoef[c]; }
+  }
+  // ---- constraint rows in dense coordinates ----
+  I.aptr.resize(mp + 1);
+  I.ai.resize(nnz); I.aj.resize(nnz); I.ag.resize(nnz);
+  int maxrow = 0;
+  for (int r = 0; r <= mp; ++r) I.aptr[r] = mp ? (int)pr.row_ptr[r] : 0;
+  for (long long e = 0; e < nnz; ++e) {
+    int i, j;
+    coords(pr.row_idx[e], i, j);
+    I.ai[e] = i; I.aj[e] = j;
+    I.ag[e] = (i == j) ? pr.row_val[e] : pr.row_val[e] * std::sqrt(2.0);
+  }
+  for (int r = 0; r < mp; ++r) maxrow = std::max(maxrow, I.aptr[r + 1] - I.aptr[r]);
+  I.group = 1;
+  while (I.group < maxrow && I.group < 32) I.group <<= 1;
+  I.bv.assign(pr.b, pr.b + m);
+  I.hv.assign(pr.h, pr.h + p);
+  // ---- operator-norm T-space ----
+  {
+    std::vector<int> tid_of(P, -1);
+    for (long long e = 0; e < nnz; ++e) {
+      const long long q = pr.row_idx[e];
+      if (tid_of[q] < 0) { tid_of[q] = 0; }
+    }
+    I.tpos.clear();
+    for (long long q = 0; q < P; ++q) if (tid_of[q] == 0) { tid_of[q] = (int)I.tpos.size(); I.tpos.push_back(q); }
+    const int nT = (int)I.tpos.size();
+    I.o_mcol.resize(nnz); I.o_mval.resize(nnz);
+    for (long long e = 0; e < nnz; ++e) { I.o_mcol[e] = tid_of[pr.row_idx[e]]; I.o_mval[e] = pr.row_val[e]; }
+    I.o_row_seg.assign(mp + 1, 0);
+    I.o_seg_lo.clear(); I.o_seg_hi.clear();
+    for (int r = 0; r < mp; ++r) {
+      long long a = pr.row_ptr[r], bnd = pr.row_ptr[r + 1];
+      if (a == bnd) { I.o_seg_lo.push_back((int)a); I.o_seg_hi.push_back((int)a); }
+      for (long long s = a; s < bnd; s += SEG_LEN) {
+        I.o_seg_lo.push_back((int)s);
+        I.o_seg_hi.push_back((int)std::min(bnd, s + SEG_LEN));
+      }
+      I.o_row_seg[r + 1] = (int)I.o_seg_lo.size();
+    }
+    I.o_tptr.assign(nT + 1, 0);
+    for (long long e = 0; e < nnz; ++e) I.o_tptr[tid_of[pr.row_idx[e]] + 1]++;
+    for (int t = 0; t < nT; ++t) I.o_tptr[t + 1] += I.o_tptr[t];
+    I.o_trow.resize(nnz); I.o_tval.resize(nnz);
+    std::vector<int> fillp(I.o_tptr.begin(), I.o_tptr.end() - 1);
+    for (int r = 0; r < mp; ++r)
+      for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) {
+        const int t = tid_of[pr.row_idx[e]];
+        I.o_trow[fillp[t]] = r; I.o_tval[fillp[t]] = pr.row_val[e]; fillp[t]++;
+      }
+  }
+  const int nt = (n + RES_TILE - 1) / RES_TILE;
+  I.ntile = nt * (nt + 1) / 2;
+  return PDSDP_OK;
+}
+
+template <class T>
+int upload(Arena& a, T*& dst, const std::vector<T>& src, size_t min_count = 1) {
+  dst = a.take<T>(std::max(src.size(), min_count));
+  if (!src.empty()) CK(cudaMemcpy(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return PDSDP_OK;
+}
+
+int alloc_instance(Instance& I, int C, double* out_dev) {
+  const size_t nld = (size_t)I.n * I.ld;
+  const int nseg = (int)I.o_seg_lo.size();
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 16) + 255) & ~size_t(255); };
+  add((I.n + 1) * 4); add(I.nz * 4); add(I.nz * 4); add(I.nz * 8); add((I.nz + 1) * 4);
+  add(I.trow.size() * 4 + 4); add(I.tcoef.size() * 8 + 8); add(I.nz * 8);
+  add((I.mp + 1) * 4); add(I.ai.size() * 4 + 4); add(I.aj.size() * 4 + 4); add(I.ag.size() * 8 + 8);
+  add((C + 1) * 4); add(I.bv.size() * 8 + 8); add(I.hv.size() * 8 + 8);
+  for (int k = 0; k < 6; ++k) add(nld * 8);
+  add(I.mp * 8 + 8); add(I.mp * 8 + 8); add(I.mp * 8 + 8);
+  add((size_t)2 * C * PDSDP_RED_MAX * 8);
+  add((size_t)I.ntile * 8 + 8); add(64); add(sizeof(State));
+  // opnorm
+  add(nseg * 4 + 4); add(nseg * 4 + 4); add((I.mp + 1) * 4); add(I.o_mcol.size() * 4 + 4);
+  add(I.o_mval.size() * 8 + 8); add(I.o_tptr.size() * 4 + 4); add(I.o_trow.size() * 4 + 4);
+  add(I.o_tval.size() * 8 + 8); add(I.tpos.size() * 8 + 8); add(I.mp * 8 + 8); add(nseg * 8 + 8);
+  add(NORM_BLOCKS * 8); add(64); add(4096 * 8);
+  add((size_t)I.P * 8);
+  bytes += 4096;
+  CK(cudaMalloc(&I.dmem, bytes));
+  I.dbytes = bytes;
+  CK(cudaMemset(I.dmem, 0, bytes));
+  Arena a{(char*)I.dmem, 0, bytes};
+  Inst& d = I.desc;
+  d.n = I.n; d.m = I.m; d.p = I.p; d.mp = I.mp; d.ld = I.ld; d.C = C;
+  d.nz = (int)I.nz; d.group = I.group;
+  int rc;
+  int* zptr; int* zcol; int* zrow; double* cval; int* tptr; int* trow; double* tcoef;
+  if ((rc = upload(a, zptr, I.zptr))) return rc;
+  if ((rc = upload(a, zcol, I.zcol))) return rc;
+  if ((rc = upload(a, zrow, I.zrow))) return rc;
+  if ((rc = upload(a, cval, I.cval))) return rc;
+  if ((rc = upload(a, tptr, I.tptr))) return rc;
+  if ((rc = upload(a, trow, I.trow))) return rc;
+  if ((rc = upload(a, tcoef, I.tcoef))) return rc;
+  d.zptr = zptr; d.zcol = zcol; d.zrow = zrow; d.cval = cval; d.tptr = tptr; d.trow = trow; d.tcoef = tcoef;
+  d.zval = a.take<double>(I.nz + 1);
+  int *aptr, *ai, *aj; double* ag;
+  if ((rc = upload(a, aptr, I.aptr))) return rc;
+  if ((rc = upload(a, ai, I.ai))) return rc;
+  if ((rc = upload(a, aj, I.aj))) return rc;
+  if ((rc = upload(a, ag, I.ag))) return rc;
+  d.aptr = aptr; d.ai = ai; d.aj = aj; d.ag = ag;
+  // constraint-row split across the C CTAs, balanced by entries
+  std::vector<int> split(C + 1, I.mp);
+  {
+    const long long tot = I.aptr[I.mp] + I.mp;
+    int r = 0;
+    split[0] = 0;
+    for (int c = 1; c < C; ++c) {
+      const long long target = tot * c / C;
+      while (r < I.mp && (long long)I.aptr[r] + r < target) ++r;
+      split[c] = r;
+    }
+    split[C] = I.mp;
+  }
+  int* asplit;
+  if ((rc = upload(a, asplit, split))) return rc;
+  d.asplit = asplit;
+  double *bv, *hv;
+  if ((rc = upload(a, bv, I.bv))) return rc;
+  if ((rc = upload(a, hv, I.hv))) return rc;
+  d.bv = bv; d.hv = hv;
+  d.V = a.take<double>(nld); d.AV = a.take<double>(nld); d.Y0 = a.take<double>(nld);
+  d.Y1 = a.take<double>(nld); d.Y2 = a.take<double>(nld); d.F = a.take<double>(nld);
+  d.ybuf0 = a.take<double>(I.mp + 1); d.ybuf1 = a.take<double>(I.mp + 1); d.dy = a.take<double>(I.mp + 1);
+  d.red = a.take<double>((size_t)2 * C * PDSDP_RED_MAX);
+  d.rpart = a.take<double>(I.ntile + 1);
+  d.rcount = a.take<unsigned>(16);
+  d.st = a.take<State>(1);
+  d.out = out_dev;
+  d.alpha = 1.0;
+  // opnorm
+  OpnormDev& o = I.od;
+  o.mp = I.mp; o.nT = (int)I.tpos.size(); o.nseg = nseg;
+  int *slo, *shi, *rseg, *mcol, *otp, *otr; double *mval, *otv;
+  if ((rc = upload(a, slo, I.o_seg_lo))) return rc;
+  if ((rc = upload(a, shi, I.o_seg_hi))) return rc;
+  if ((rc = upload(a, rseg, I.o_row_seg))) return rc;
+  if ((rc = upload(a, mcol, I.o_mcol))) return rc;
+  if ((rc = upload(a, mval, I.o_mval))) return rc;
+  if ((rc = upload(a, otp, I.o_tptr))) return rc;
+  if ((rc = upload(a, otr, I.o_trow))) return rc;
+  if ((rc = upload(a, otv, I.o_tval))) return rc;
+  o.seg_lo = slo; o.seg_hi = shi; o.row_seg = rseg; o.mcol = mcol; o.mval = mval;
+  o.tptr = otp; o.trow = otr; o.tval = otv;
+  o.x = a.take<double>(I.tpos.size() + 1);
+  o.y = a.take<double>(I.mp + 1);
+  o.seg_part = a.take<double>(nseg + 1);
+  o.norm_part = a.take<double>(NORM_BLOCKS);
+  o.scal = a.take<double>(8);
+  o.s_hist = a.take<double>(4096);
+  I.d_packed = a.take<double>((size_t)I.P);
+  if (a.off > bytes) return fail(PDSDP_ENOMEM, "arena overflow");
+  return PDSDP_OK;
+}
+
+int check_inst(pdsdp_batch* b, int inst) {
+  if (!b) return fail(PDSDP_EINVAL, "batch is NULL");
+  if (inst < 0 || inst >= (int)b->inst.size()) return fail(PDSDP_EINVAL, "instance index out of range");
+  return PDSDP_OK;
+}
+
+int launch_iterate(pdsdp_batch* b, int nact) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nact * b->C);
+  cfg.blockDim = dim3(PDSDP_NTHR);
+  cfg.dynamicSmemBytes = b->smem;
+  cfg.stream = b->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = b->C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, lrpdhg_iterate_kernel, (const Inst*)b->d_insts, (const Ctl*)b->d_ctl,
+                        (const int*)b->d_active, b->lds));
+  return PDSDP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pdsdp_last_error(void) { return g_err.c_str(); }
+
+const char* pdsdp_strerror(int code) {
+  switch (code) {
+    case PDSDP_OK: return "ok";
+    case PDSDP_EINVAL: return "invalid argument";
+    case PDSDP_ECUDA: return "CUDA error";
+    case PDSDP_ENOMEM: return "out of memory";
+    case PDSDP_ERANK: return "target rank exceeds the eigen block limit";
+    default: return "unknown error";
+  }
+}
+
+int pdsdp_version(void) { return 1; }
+
+int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** out) {
+  if (!out || !problems || count < 1) return fail(PDSDP_EINVAL, "bad batch arguments");
+  *out = nullptr;
+  int dev;
+  CK(cudaGetDevice(&dev));
+  pdsdp_batch* b = new pdsdp_batch();
+  int maxn = 0;
+  for (int k = 0; k < count; ++k) maxn = std::max(maxn, (int)problems[k].n);
+  int C = 1;
+  while (C < 16 && C * 128 < maxn) C <<= 1;
+  b->C = C;
+  int lds = std::min(maxn, PDSDP_BMAX);
+  b->lds = lds < 4 ? 4 : lds;
+  b->smem = (size_t)(5 * b->lds * b->lds + PDSDP_NTHR + 10 * PDSDP_BMAX) * sizeof(double) +
+            (size_t)(3 * PDSDP_BMAX + 8) * sizeof(int) + 64;
+  CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  CK(cudaHostAlloc((void**)&b->h_out, (size_t)count * PDSDP_OUT_LEN * sizeof(double), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&b->d_out, b->h_out, 0));
+  memset(b->h_out, 0, (size_t)count * PDSDP_OUT_LEN * sizeof(double));
+  CK(cudaHostAlloc((void**)&b->h_ctl, (size_t)count * sizeof(Ctl), 0));
+  CK(cudaHostAlloc((void**)&b->h_active, (size_t)count * sizeof(int), 0));
+  CK(cudaMalloc(&b->d_ctl, (size_t)count * sizeof(Ctl)));
+  CK(cudaMalloc(&b->d_active, (size_t)count * sizeof(int)));
+  CK(cudaMalloc(&b->d_insts, (size_t)count * sizeof(Inst)));
+  CK(cudaMalloc(&b->d_objpart, (size_t)count * 256 * sizeof(double)));
+  CK(cudaMalloc(&b->d_objcnt, (size_t)count * sizeof(unsigned)));
+  CK(cudaMemset(b->d_objcnt, 0, (size_t)count * sizeof(unsigned)));
+  CK(cudaMalloc(&b->d_objres, (size_t)count * sizeof(double)));
+  std::vector<Inst> descs(count);
+  for (int k = 0; k < count; ++k) {
+    Instance* I = new Instance();
+    b->inst.push_back(I);
+    int rc = build_instance(problems[k], *I);
+    if (rc) { pdsdp_batch_destroy(b); return rc; }
+    rc = alloc_instance(*I, C, b->d_out + (size_t)k * PDSDP_OUT_LEN);
+    if (rc) { std::string e = g_err; pdsdp_batch_destroy(b); g_err = e; return rc; }
+    descs[k] = I->desc;
+    b->max_tiles = std::max(b->max_tiles, I->ntile);
+  }
+  CK(cudaMemcpy(b->d_insts, descs.data(), count * sizeof(Inst), cudaMemcpyHostToDevice));
+  if (C > 8) CK(cudaFuncSetAttribute(lrpdhg_iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(lrpdhg_iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
+  const size_t rsm = (size_t)2 * RES_TILE * (RES_KMAX + 1) * sizeof(double);
+  CK(cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+  for (int k = 0; k < count; ++k) {
+    int rc = pdsdp_reset(b, k, 0.0);
+    if (rc) { std::string e = g_err; pdsdp_batch_destroy(b); g_err = e; return rc; }
+  }
+  *out = b;
+  return PDSDP_OK;
+}
+
+int pdsdp_batch_destroy(pdsdp_batch* b) {
+  if (!b) return PDSDP_OK;
+  if (b->stream) cudaStreamSynchronize(b->stream);
+  for (Instance* I : b->inst) {
+    if (I->dmem) cudaFree(I->dmem);
+    delete I;
+  }
+  if (b->h_out) cudaFreeHost(b->h_out);
+  if (b->h_ctl) cudaFreeHost(b->h_ctl);
+  if (b->h_active) cudaFreeHost(b->h_active);
+  if (b->d_ctl) cudaFree(b->d_ctl);
+  if (b->d_active) cudaFree(b->d_active);
+  if (b->d_insts) cudaFree(b->d_insts);
+  if (b->d_objpart) cudaFree(b->d_objpart);
+  if (b->d_objcnt) cudaFree(b->d_objcnt);
+  if (b->d_objres) cudaFree(b->d_objres);
+  if (b->stream) cudaStreamDestroy(b->stream);
+  delete b;
+  return PDSDP_OK;
+}
+
+int pdsdp_batch_info(const pdsdp_batch* b, int inst, int64_t* info) {
+  if (!b || !info || inst < 0 || inst >= (int)b->inst.size()) return fail(PDSDP_EINVAL, "bad info arguments");
+  const Instance* I = b->inst[inst];
+  info[0] = I->n; info[1] = I->nz; info[2] = (int64_t)I->tpos.size(); info[3] = b->C;
+  info[4] = I->ld; info[5] = I->group; info[6] = (int64_t)b->smem; info[7] = (int64_t)I->dbytes;
+  return PDSDP_OK;
+}
+
+void* pdsdp_batch_stream(pdsdp_batch* b) { return b ? (void*)b->stream : nullptr; }
+
+int pdsdp_opnorm_positions(pdsdp_batch* b, int inst, int64_t* pos_out, int64_t* count) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  const Instance* I = b->inst[inst];
+  if (count) *count = (int64_t)I->tpos.size();
+  if (pos_out) for (size_t t = 0; t < I->tpos.size(); ++t) pos_out[t] = I->tpos[t];
+  return PDSDP_OK;
+}
+
+static int opnorm_step(pdsdp_batch* b, Instance* I, double* hist, int idx) {
+  OpnormDev& o = I->od;
+  cudaStream_t s = b->stream;
+  // y = M x ; s = |y|
+  seg_dot_kernel<<<o.nseg, 256, 0, s>>>(o);
+  seg_final_kernel<<<std::max(1, std::min(1024, (o.mp + 255) / 256)), 256, 0, s>>>(o);
+  sumsq_kernel<<<NORM_BLOCKS, 256, 0, s>>>(o.y, o.mp, o.norm_part);
+  norm_final_kernel<<<1, 32, 0, s>>>(o.norm_part, NORM_BLOCKS, o.scal, hist, idx);
+  // x = M^T y / |M^T y|
+  adjT_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, s>>>(o);
+  sumsq_kernel<<<NORM_BLOCKS, 256, 0, s>>>(o.x, o.nT, o.norm_part);
+  norm_final_kernel<<<1, 32, 0, s>>>(o.norm_part, NORM_BLOCKS, o.scal + 1, nullptr, 0);
+  inv_scale_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, s>>>(o.x, o.nT, o.scal + 1);
+  CK(cudaGetLastError());
+  return PDSDP_OK;
+}
+
+int pdsdp_opnorm_run(pdsdp_batch* b, int inst, const double* x0, int iters, double* s_out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (iters < 1 || iters > 4096 || !s_out) return fail(PDSDP_EINVAL, "iters must lie in [1, 4096]");
+  Instance* I = b->inst[inst];
+  if (I->od.nT == 0 || I->o_mval.empty()) return fail(PDSDP_EINVAL, "all constraint rows are zero; operator norm is 0");
+  if (x0) CK(cudaMemcpyAsync(I->od.x, x0, I->tpos.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  for (int it = 0; it < iters; ++it)
+    if ((rc = opnorm_step(b, I, I->od.s_hist, it))) return rc;
+  CK(cudaMemcpyAsync(s_out, I->od.s_hist, iters * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
+int pdsdp_set_alpha(pdsdp_batch* b, int inst, double alpha) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(PDSDP_EINVAL, "alpha must be positive");
+  Instance* I = b->inst[inst];
+  I->desc.alpha = alpha;
+  CK(cudaMemcpyAsync(&b->d_insts[inst].alpha, &I->desc.alpha, sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
+__global__ void init_finalize_kernel(const Inst* insts, int inst, double seed) {
+  State* st = insts[inst].st;
+  const double g = st->lo;
+  st->lo = -insts[inst].alpha * g;
+  st->seed = seed;
+  st->b = 0; st->rF = 0; st->theta_valid = 0; st->iav = 1; st->rF_used = 0; st->r_cur = 0;
+}
+
+int pdsdp_reset(pdsdp_batch* b, int inst, double seed) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  Instance* I = b->inst[inst];
+  CK(cudaMemsetAsync(I->desc.st, 0, sizeof(State), b->stream));
+  CK(cudaMemsetAsync(I->desc.V, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
+  CK(cudaMemsetAsync(I->desc.F, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
+  init_kernel<<<148, 256, 0, b->stream>>>(b->d_insts, inst, seed);
+  init_finalize_kernel<<<1, 1, 0, b->stream>>>(b->d_insts, inst, seed);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
+int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank, const int32_t* ypar,
+                  const int32_t* flags, int32_t maxpass, double* out) {
+  if (!b || nact < 1 || nact > (int)b->inst.size() || !insts || !rank || !ypar || !out)
+    return fail(PDSDP_EINVAL, "bad iterate arguments");
+  const int N = (int)b->inst.size();
+  for (int a = 0; a < nact; ++a) {
+    const int k = insts[a];
+    if (k < 0 || k >= N) return fail(PDSDP_EINVAL, "instance index out of range");
+    const Instance* I = b->inst[k];
+    if (rank[a] < 1 || rank[a] > I->n)
+      return fail(PDSDP_EINVAL, "rank r=" + std::to_string(rank[a]) + " outside [1, " + std::to_string(I->n) + "]");
+    const int kk = std::min(rank[a] + 1, I->n);
+    if (kk > PDSDP_BMAX) return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + " needs an eigen block above 64");
+    b->h_ctl[k].r = rank[a];
+    b->h_ctl[k].ypar = ypar[a] & 1;
+    b->h_ctl[k].flags = flags ? flags[a] : 0;
+    b->h_ctl[k].maxpass = maxpass;
+    b->h_active[a] = k;
+  }
+  CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, N * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(b->d_active, b->h_active, nact * sizeof(int), cudaMemcpyHostToDevice, b->stream));
+  int rc = launch_iterate(b, nact);
+  if (rc) return rc;
+  int maxr = 1;
+  for (int a = 0; a < nact; ++a) maxr = std::max(maxr, (int)rank[a]);
+  const int kp = std::min(RES_KMAX, (2 * std::min(maxr, PDSDP_BMAX) + 3) & ~3);
+  const size_t rsm = (size_t)2 * RES_TILE * (kp + 1) * sizeof(double);
+  residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_active);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(b->stream));
+  for (int a = 0; a < nact; ++a)
+    memcpy(out + (size_t)a * PDSDP_OUT_LEN, b->h_out + (size_t)insts[a] * PDSDP_OUT_LEN, PDSDP_OUT_LEN * sizeof(double));
+  return PDSDP_OK;
+}
+
+int pdsdp_objective(pdsdp_batch* b, int inst, int which, double* out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (!out) return fail(PDSDP_EINVAL, "out is NULL");
+  b->h_active[0] = inst;
+  CK(cudaMemcpyAsync(b->d_active, b->h_active, sizeof(int), cudaMemcpyHostToDevice, b->stream));
+  objective_kernel<<<dim3(148, 1), 256, 0, b->stream>>>(b->d_insts, b->d_active, which ? 1 : 0, b->d_objpart,
+                                                       b->d_objcnt, b->d_objres);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, b->d_objres, sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
+int pdsdp_download_x(pdsdp_batch* b, int inst, int which, double* packed_out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (!packed_out) return fail(PDSDP_EINVAL, "out is NULL");
+  Instance* I = b->inst[inst];
+  const long long P = I->P;
+  const int grid = (int)std::min<long long>(148 * 8, (P + 255) / 256);
+  pack_kernel<<<std::max(grid, 1), 256, 0, b->stream>>>(b->d_insts, inst, which ? 1 : 0, I->d_packed);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(packed_out, I->d_packed, P * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
+int pdsdp_download_y(pdsdp_batch* b, int inst, int ypar, double* y_out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  Instance* I = b->inst[inst];
+  if (I->mp == 0) return PDSDP_OK;
+  if (!y_out) return fail(PDSDP_EINVAL, "out is NULL");
+  CK(cudaMemcpyAsync(y_out, (ypar & 1) ? I->desc.ybuf1 : I->desc.ybuf0, I->mp * sizeof(double),
+                     cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
+__global__ void gather_T_kernel(const double* __restrict__ packed, const long long* __restrict__ tpos, int nT,
+                                double* __restrict__ x) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nT; t += gridDim.x * blockDim.x) x[t] = packed[tpos[t]];
+}
+__global__ void scatter_T_kernel(const double* __restrict__ x, const long long* __restrict__ tpos, int nT,
+                                 double* __restrict__ packed) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nT; t += gridDim.x * blockDim.x) packed[tpos[t]] = x[t];
+}
+
+int pdsdp_apply_M(pdsdp_batch* b, int inst, const double* X_packed, double* out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  Instance* I = b->inst[inst];
+  if (I->mp == 0) return PDSDP_OK;
+  if (!X_packed || !out) return fail(PDSDP_EINVAL, "NULL argument");
+  OpnormDev& o = I->od;
+  long long* dpos = nullptr;
+  CK(cudaMalloc(&dpos, std::max<size_t>(1, I->tpos.size()) * sizeof(long long)));
+  CK(cudaMemcpyAsync(dpos, I->tpos.data(), I->tpos.size() * sizeof(long long), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(I->d_packed, X_packed, I->P * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  if (o.nT) gather_T_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, b->stream>>>(I->d_packed, dpos, o.nT, o.x);
+  seg_dot_kernel<<<o.nseg, 256, 0, b->stream>>>(o);
+  seg_final_kernel<<<std::max(1, std::min(1024, (o.mp + 255) / 256)), 256, 0, b->stream>>>(o);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, o.y, I->mp * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  cudaFree(dpos);
+  return PDSDP_OK;
+}
+
+int pdsdp_apply_M_adjoint(pdsdp_batch* b, int inst, const double* y, double* out_packed) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  Instance* I = b->inst[inst];
+  if (!out_packed || (I->mp && !y)) return fail(PDSDP_EINVAL, "NULL argument");
+  OpnormDev& o = I->od;
+  long long* dpos = nullptr;
+  CK(cudaMalloc(&dpos, std::max<size_t>(1, I->tpos.size()) * sizeof(long long)));
+  CK(cudaMemcpyAsync(dpos, I->tpos.data(), I->tpos.size() * sizeof(long long), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemsetAsync(I->d_packed, 0, I->P * sizeof(double), b->stream));
+  if (I->mp) CK(cudaMemcpyAsync(o.y, y, I->mp * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  if (o.nT) {
+    adjT_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, b->stream>>>(o);
+    scatter_T_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, b->stream>>>(o.x, dpos, o.nT, I->d_packed);
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_packed, I->d_packed, I->P * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  cudaFree(dpos);
+  return PDSDP_OK;
+}
+
+int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_packed_out, double* lambda_out) {
+  if (n < 1 || !S_packed || !P_packed_out) return fail(PDSDP_EINVAL, "bad aproj arguments");
+  if (r < 1 || r > n) return fail(PDSDP_EINVAL, "rank r=" + std::to_string(r) + " outside [1, " + std::to_string(n) + "]");
+  const long long P = packed_len(n);
+  std::vector<double> C(P);
+  for (long long q = 0; q < P; ++q) C[q] = -S_packed[q];
+  pdsdp_problem pr{};
+  pr.n = n; pr.m = 0; pr.p = 0; pr.C_packed = C.data();
+  int64_t rp0 = 0;
+  pr.row_ptr = &rp0;
+  pdsdp_batch* b = nullptr;
+  int rc = pdsdp_batch_create(1, &pr, &b);
+  if (rc) return rc;
+  int32_t inst = 0, rr = r, yp = 0, fl = 1;
+  double out[PDSDP_OUT_LEN];
+  rc = pdsdp_set_alpha(b, 0, 1.0);
+  if (!rc) rc = pdsdp_reset(b, 0, 0.0);
+  if (!rc) rc = pdsdp_iterate(b, 1, &inst, &rr, &yp, &fl, 200, out);
+  if (!rc) rc = pdsdp_download_x(b, 0, 0, P_packed_out);
+  if (!rc && lambda_out) *lambda_out = out[PDSDP_OUT_LAMBDA];
+  std::string e = g_err;
+  pdsdp_batch_destroy(b);
+  g_err = e;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+"""Drop-in ``solve_lr_pd_sdp`` running the per-iteration hot path on a B200.
+
+Host side of the boundary.  The control flow is the reference's Algorithm 2
+driver (``pkg/src/pdsdp/lowrank.py:102-208``) statement for statement —
+relative residual scale, checkpoints, rank certificate on lambda_{r+1}, stall
+window, rank doubling, time limit, objectives — while every per-iteration
+computation (``approximate_primal_step``, ``dual_step``, ``residuals``,
+``_finite``) is one call into the sm_100a library, which returns scalars
+only.  Iterates stay on the device; X and y are downloaded at checkpoints and
+at the end (the reference copies them there too, ``lowrank.py:163-169``).
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+import time
+
+import numpy as np
+
+from .config import (
+    DEFAULT_EPS_LAMBDA_PER_N,
+    Checkpoint,
+    ProgressCallback,
+    ProgressInfo,
+    RankController,
+    SolveResult,
+    SolveStatus,
+    SolverConfig,
+    rank_certificate_satisfied,
+    stall_detected,
+    update_rank,
+)
+from .device import (
+    OUT_EIGCONV, OUT_EPS_D, OUT_EPS_P, OUT_FINITE, OUT_LAMBDA, OUT_MATVECS, OUT_PASSES,
+    DeviceBatch,
+)
+from .layout import SymMatrix, approx_error_bound
+from .model import SdpProblem
+
+logger = logging.getLogger(__name__)
+
+# problem.py:21-26
+_NORM_MIN_ITER = 200
+_NORM_MAX_ITER = 10_000
+_NORM_REL_TOL = 1e-10
+_NORM_SAFETY = 1.0 + 1e-7
+_NORM_CHUNK = 256
+
+
+def _device_batch(prob: SdpProblem) -> DeviceBatch:
+    cache = prob._device_cache
+    if "batch" not in cache:
+        cache["batch"] = DeviceBatch([prob])
+    return cache["batch"]
+
+
+def operator_norm_on_device(batch: DeviceBatch, inst: int, seed: int = 0) -> float:
+    """Seeded power iteration on M^T M (reference ``problem.py:157-185``).
+
+    The start vectors come from the reference's own RNG stream on the host;
+    each product runs on the device; the stopping rule is evaluated on the
+    host over the device's per-iteration ||M x|| values, iteration by
+    iteration, so the accepted estimate is the one the reference accepts."""
+    prob = batch.problems[inst]
+    P = prob.packed_len
+    pos = batch.opnorm_positions(inst)
+    if pos.size == 0:
+        raise ValueError("all constraint rows are zero; operator norm is 0")
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(P)
+    x /= np.linalg.norm(x)
+    start = x[pos]
+    sigma = 0.0
+    it = 0
+    while it < _NORM_MAX_ITER:
+        chunk = min(_NORM_CHUNK, _NORM_MAX_ITER - it)
+        s_vals = batch.opnorm_run(inst, start, chunk)
+        start = None
+        advanced = chunk
+        for j in range(chunk):
+            s = float(s_vals[j])
+            itj = it + j
+            if s == 0.0:
+                x = rng.standard_normal(P)
+                x /= np.linalg.norm(x)
+                start = x[pos]
+                advanced = j + 1
+                break
+            if itj + 1 >= _NORM_MIN_ITER and abs(s - sigma) <= _NORM_REL_TOL * s:
+                return s * _NORM_SAFETY
+            sigma = s
+        it += advanced
+    return sigma * _NORM_SAFETY
+
+
+def estimate_operator_norm(prob: SdpProblem, seed: int = 0) -> float:
+    """Drop-in for ``problem.estimate_operator_norm`` (device products)."""
+    return operator_norm_on_device(_device_batch(prob), 0, seed)
+
+
+def step_size(prob: SdpProblem, config: SolverConfig) -> float:
+    """reference ``pdhg.py:211-214``"""
+    if config.alpha_override is not None:
+        return config.alpha_override
+    return config.alpha_safety / estimate_operator_norm(prob, config.seed)
+
+
+class _DeviceIterate:
+    """Device-resident (X_k, y_k) of one instance: which buffers hold what."""
+
+    def __init__(self, batch: DeviceBatch, inst: int):
+        self.batch, self.inst = batch, inst
+        self.ypar = 0          # y_k is ybuf[ypar]
+        self.which = 0         # X_k is the newest factor (0) or the previous one (1)
+        self.k = 0
+
+    def X(self) -> SymMatrix:
+        n = self.batch.problems[self.inst].n
+        if self.k == 0:
+            return SymMatrix.zero(n)
+        return SymMatrix(n, self.batch.download_x(self.inst, self.which))
+
+    def y(self) -> np.ndarray:
+        return self.batch.download_y(self.inst, self.ypar)
+
+    def objective(self) -> float:
+        if self.k == 0:
+            return 0.0
+        return self.batch.objective(self.inst, self.which)
+
+
+def solve_lr_pd_sdp(
+    prob: SdpProblem,
+    config: SolverConfig | None = None,
+    callback: ProgressCallback | None = None,
+    *,
+    stats: dict | None = None,
+) -> SolveResult:
+    """Rank-adaptive primal-dual iteration from a zero start
+    (reference ``lowrank.py:102-208``); per-iteration work on the B200."""
+    config = config or SolverConfig()
+    config.validate()
+    t0 = time.perf_counter()
+    n = prob.n
+    batch = _device_batch(prob)
+    alpha = step_size(prob, config)
+    eps_lambda = (config.eps_lambda if config.eps_lambda is not None
+                  else DEFAULT_EPS_LAMBDA_PER_N * n)
+    controller = RankController(r=min(max(config.initial_rank, 1), n), ell=config.window_ell)
+    batch.set_alpha(0, alpha)
+    batch.reset(0, 0.0)
+    it = _DeviceIterate(batch, 0)
+    rank_path = [(0, controller.r)]
+    status = None
+    res = (math.nan, math.nan, math.nan)
+    scale = 1.0
+    eig_passes = eig_matvecs = eig_unconverged = 0
+    for k in range(1, config.max_iter + 1):
+        out = batch.iterate([0], [controller.r], [it.ypar])[0]
+        eig_passes += int(out[OUT_PASSES])
+        eig_matvecs += int(out[OUT_MATVECS])
+        if out[OUT_EIGCONV] == 0:
+            eig_unconverged += 1
+            logger.info("eigensolver hit its pass limit at k=%d (r=%d)", k, controller.r)
+        if out[OUT_FINITE] != 1.0:
+            status = SolveStatus.DIVERGED
+            it.which = 1
+            break
+        # state.advance (pdhg.py:113-118)
+        it.k = k
+        it.ypar ^= 1
+        it.which = 0
+        lambda_r = float(out[OUT_LAMBDA])
+        controller.last_lambda_r = lambda_r
+        ep, ed = float(out[OUT_EPS_P]), float(out[OUT_EPS_D])
+        res = (ep, ed, ep + ed)
+        controller.history.append(res[2])
+        if k == 1 and config.relative_residuals:
+            scale = 1.0 + res[2]
+        if callback is not None and k % config.progress_every == 0:
+            callback(ProgressInfo(k, *res, controller.r, it.objective()))
+        if res[2] <= config.eps_tol * scale:
+            Xc = it.X()
+            controller.checkpoints.append(
+                Checkpoint(controller.r, Xc, it.y(), prob.C.inner(Xc)))
+            if rank_certificate_satisfied(n, controller.r, lambda_r, eps_lambda):
+                status = SolveStatus.OPTIMAL
+                break
+            logger.debug("converged at rank %d but certificate %.3e > %.3e; doubling",
+                         controller.r, approx_error_bound(n, controller.r, lambda_r), eps_lambda)
+            update_rank(controller, n)
+            rank_path.append((k, controller.r))
+        elif controller.r < n and stall_detected(controller.history, controller.ell):
+            logger.debug("stalled at rank %d after %d iterations; doubling", controller.r, k)
+            update_rank(controller, n)
+            rank_path.append((k, controller.r))
+        if time.perf_counter() - t0 > config.time_limit_s:
+            status = SolveStatus.TIME_LIMIT
+            break
+    if status is None:
+        status = SolveStatus.MAX_ITERATIONS
+    X = it.X()
+    y = it.y()
+    pobj = prob.C.inner(X)
+    dobj = -float(prob.b @ y[: prob.m] + prob.h @ y[prob.m:])
+    if stats is not None:
+        stats.update(eig_passes=eig_passes, eig_matvecs=eig_matvecs,
+                     eig_unconverged=eig_unconverged, alpha=alpha)
+    return SolveResult(
+        status=status, X=X, y=y, primal_objective=pobj, dual_objective=dobj,
+        final_residuals=res, iterations=it.k, rank_path=rank_path,
+        checkpoints=controller.checkpoints, wall_time_s=time.perf_counter() - t0,
+        residual_scale=scale, objective_sign=prob.objective_sign,
+    )
