@@ -163,6 +163,12 @@ __device__ void scale_T(const Sm& s, int rF, int b) {
   __syncthreads();
 }
 
+// dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
+inline size_t iterate_smem_bytes(int lds) {
+  return (size_t)(5 * lds * lds + PDSDP_NTHR + 11 * PDSDP_BMAX) * sizeof(double) +
+         (size_t)(3 * PDSDP_BMAX + 8) * sizeof(int) + 64;
+}
+
 __device__ int choose_block(int k, int n) {
   int g = k / 4;
   if (g < 4) g = 4;

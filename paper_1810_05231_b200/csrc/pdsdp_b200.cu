@@ -407,8 +407,7 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
   b->C = C;
   int lds = std::min(maxn, PDSDP_BMAX);
   b->lds = lds < 4 ? 4 : lds;
-  b->smem = (size_t)(5 * b->lds * b->lds + PDSDP_NTHR + 10 * PDSDP_BMAX) * sizeof(double) +
-            (size_t)(3 * PDSDP_BMAX + 8) * sizeof(int) + 64;
+  b->smem = iterate_smem_bytes(b->lds);
   CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
   CK(cudaHostAlloc((void**)&b->h_out, (size_t)count * PDSDP_OUT_LEN * sizeof(double), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&b->d_out, b->h_out, 0));
