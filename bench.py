@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py — PDHG iterations/s and time-to-1e-4 residual on BASELINE.json
+configs[1]: n=2000 Max-Cut SDP (G(2000, 0.01), +-1 weights, seed 0), FP64.
+
+A step is one complete LR-PD-SDP solve to the reference's relative 1e-4 rule
+(lowrank.py:153-161).  `value` = PDHG iterations / device time of the solve
+loop with the problem already resident in HBM (CUDA events on the library's
+stream, L2 flushed between steps).  `e2e` = the same metric through the
+public drop-in API `solve_lr_pd_sdp(prob, config)` from host data: problem
+upload and re-indexing, operator-norm estimate, the loop, the final X / y
+download (host wall clock around synchronised calls).
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy/scipy oracle port, oracle/lrpdhg_oracle.py; the reference itself is pure
+Python and cannot travel to the GPU box) on this host's cores, each step a
+bounded sample of iterations of the same workload.
+
+Multi-GPU (torchrun, one process per GPU): every rank solves its own seeded
+instance of the workload (seed = rank; instances are independent, no
+data-path collective, "scaling": "weak"); per-instance results are gathered
+with NCCL all_gather and the time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PDHG iterations/s and time-to-1e-4 residual, n=2000 Max-Cut SDP, FP64"
+WORKLOADS = {
+    "cfg1": (0, "maxcut_n100_p0.1_unit_r5"),
+    "cfg2": (1, "maxcut_n2000_p0.01_pm1_r10"),
+    "cfg4": (3, "sensor_n1002_d2_r0.1"),
+    "cfg5": (4, "maxcut_n1000_p0.02_pm1_r1"),
+}
+FP64_DMMA_TFLOPS = 37.1   # measured on this pool's B200 (profiles/r01_fp64_cluster_probe.txt)
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def oracle_sample(prob, cfg, iters: int, alpha: float | None = None):
+    """Time `iters` iterations of the CPU oracle (reference algorithm) after
+    the first; returns (iterations/s, per-iteration timestamps)."""
+    from oracle import lrpdhg_oracle as orc
+    from paper_1810_05231_b200.config import SolverConfig
+    stamps = []
+    c = SolverConfig(**{**cfg.__dict__, "progress_every": 1, "max_iter": iters + 1,
+                        "time_limit_s": 1e9})
+    orc.solve_lr(prob, c, progress=lambda info: stamps.append(time.perf_counter()),
+                 alpha=alpha, stop_after=iters + 1)
+    rate = (len(stamps) - 1) / (stamps[-1] - stamps[0]) if len(stamps) > 1 else float("nan")
+    return rate, stamps
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU implementation."""
+    if rank != 0:
+        return 0
+    from paper_1810_05231_b200 import workloads
+    idx, wname = WORKLOADS[args.workload]
+    prob, cfg = workloads.config(idx, seed=0)
+    per_step = args.ref_iters_per_step
+    total = (args.warmup + args.steps) * per_step
+    _, stamps = oracle_sample(prob, cfg, total)
+    # step boundaries over the per-iteration timestamps
+    b0 = args.warmup * per_step
+    t_timed = stamps[min(len(stamps) - 1, b0 + args.steps * per_step)] - stamps[b0]
+    its = args.steps * per_step
+    value = its / t_timed
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_timed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE recipe)",
+        "config": {"workload": wname, "steps_are": f"{per_step} PDHG iterations of one continuing solve",
+                   "threads": cores},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores, "kind": "port",
+                         "sample": f"{its} timed LR-PDHG iterations (after {b0 + 1} warm-up) of "
+                                   f"{wname} with numpy/scipy (OpenBLAS, ARPACK) on all host threads"},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def flush_l2(torch, stream):
+    buf = getattr(flush_l2, "buf", None)
+    if buf is None:
+        buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+        flush_l2.buf = buf
+    with torch.cuda.stream(stream):
+        buf.fill_(1.0)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1810_05231_b200 import SolverConfig, solve_lr_pd_sdp, workloads
+    from paper_1810_05231_b200.device import DeviceBatch
+    from paper_1810_05231_b200.layout import packed_length
+    from paper_1810_05231_b200.solver import operator_norm_on_device, run_lr_loop
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    idx, wname = WORKLOADS[args.workload]
+    prob, cfg = workloads.config(idx, seed=rank)
+    batch = DeviceBatch([prob])
+    alpha = cfg.alpha_safety / operator_norm_on_device(batch, 0, cfg.seed)
+    stream = torch.cuda.ExternalStream(batch.stream_handle())
+
+    def one_solve():
+        return run_lr_loop(batch, 0, prob, cfg, alpha)
+
+    for _ in range(args.warmup):
+        o = one_solve()
+    # ---- timed region: device-resident solves ----
+    batch.set_timing(True)
+    times, iters, outcomes = [], [], []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush_l2(torch, stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            o = one_solve()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            iters.append(o.it.k)
+            outcomes.append(o)
+    ktimes = batch.kernel_times()
+    batch.set_timing(False)
+    t_loop = sum(times)
+    it_tot = sum(iters)
+    # max over ranks, iterations summed
+    t_all, it_all = t_loop, it_tot
+    gathered = None
+    o = outcomes[-1]
+    final = torch.tensor([float(o.it.k), o.res[0], o.res[1], o.res[2], float(o.controller.r),
+                          1.0 if o.status.value == "optimal" else 0.0], dtype=torch.float64,
+                         device="cuda")
+    if world > 1:
+        tt = torch.tensor([t_loop, float(it_tot)], dtype=torch.float64, device="cuda")
+        lst = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(lst, tt)
+        t_all = max(float(x[0]) for x in lst)
+        it_all = sum(float(x[1]) for x in lst)
+        glist = [torch.zeros_like(final) for _ in range(world)]
+        dist.all_gather(glist, final)          # per-instance results over NCCL
+        gathered = [g.tolist() for g in glist]
+    value = it_all / t_all * (args.steps and 1)
+    # ---- e2e: public API from host data ----
+    e2e_times, e2e_iters = [], []
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        p2, c2 = workloads.config(idx, seed=rank)
+        indptr, ridx, rval = p2.stacked_arrays()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        res = solve_lr_pd_sdp(p2, c2)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t)
+        e2e_iters.append(res.iterations)
+        b2 = p2._device_cache["batch"]
+        nT = b2.info(0)["t_space"]
+        h2d = (p2.C.data.nbytes + indptr.nbytes + ridx.nbytes + rval.nbytes + p2.b.nbytes +
+               p2.h.nbytes + 8 * nT + res.iterations * 16 * 2)
+        d2h = (8 * packed_length(p2.n) * (1 + len(res.checkpoints)) + res.y.nbytes *
+               (1 + len(res.checkpoints)) + res.iterations * 16 * 8)
+        b2.close()
+        p2._device_cache.clear()
+    e2e_rate = sum(e2e_iters) / sum(e2e_times)
+    if world > 1:
+        tt = torch.tensor([sum(e2e_times), float(sum(e2e_iters))], dtype=torch.float64, device="cuda")
+        lst = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(lst, tt)
+        e2e_rate = sum(float(x[1]) for x in lst) / max(float(x[0]) for x in lst)
+    # ---- roofline of the dominant kernel ----
+    n = prob.n
+    r = o.controller.r
+    it_ms = ktimes["iterate_ms"] / max(1, ktimes["iterate_launches"])
+    rs_ms = ktimes["residual_ms"] / max(1, ktimes["residual_launches"])
+    if rs_ms >= it_ms:
+        flops = float(n) * (n + 1) * (2 * r)   # n(n+1)/2 entries x 2K flops, K = r + r_prev
+        achieved = flops / (rs_ms * 1e-3) / 1e12
+        roof = {"kernel": "residual_kernel (DMMA m8n8k4.f64)", "bound": "tensor", "achieved": achieved,
+                "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_TFLOPS,
+                "traffic": None, "peak_source": "measured DMMA f64 (profiles/r01_fp64_cluster_probe.txt)"}
+    else:
+        nz = batch.info(0)["z_slots"]
+        mv = sum(x.eig_matvecs for x in outcomes) / max(1, it_tot)
+        b = min(n, max(r + 1 + max(4, (r + 1) // 4), 4))
+        bytes_per_mv = 8.0 * n * b * 2 + 12.0 * nz + 8.0 * n * r
+        algo = mv * bytes_per_mv
+        achieved = algo / (it_ms * 1e-3) / 1e9
+        peak = 6551.7
+        try:
+            peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except (OSError, ValueError, KeyError):
+            pass
+        roof = {"kernel": "lrpdhg_iterate_kernel (cluster eigensolver + dual step)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roof.update({"iterate_kernel_us": 1e3 * it_ms, "residual_kernel_us": 1e3 * rs_ms,
+                 "loop_us_per_iteration": 1e6 * t_loop / max(1, it_tot)})
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, stamps = oracle_sample(prob, cfg, args.cpu_iters, alpha=alpha)
+        cpu = {"value": rate, "unit": "iterations/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{args.cpu_iters} LR-PDHG iterations of {wname} (after 1 warm-up iteration) "
+                         f"with the numpy/scipy oracle port on all host threads"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE recipe; each rank its own instance, seed = rank)",
+            "config": {"workload": wname, "step": "one full LR-PD-SDP solve to eps_tol=1e-4 (relative)",
+                       "iterations_per_solve": iters, "time_to_tol_s": times,
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "parallelism": f"replicas x{world}", "final_rank": r,
+                       "eig_matvecs_per_iter": sum(x.eig_matvecs for x in outcomes) / max(1, it_tot),
+                       "eig_passes_per_iter": sum(x.eig_passes for x in outcomes) / max(1, it_tot),
+                       "status": o.status.value},
+            "e2e": {"value": e2e_rate, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "time_to_tol_s": e2e_times},
+            "gpu_launches": int(2 * it_tot + 2 * args.steps),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        if gathered is not None:
+            line["per_instance"] = gathered
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--cpu-iters", type=int, default=25)
+    ap.add_argument("--ref-iters-per-step", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    rank, world, local_rank = env_rank()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -107,6 +107,17 @@ int pdsdp_apply_M(pdsdp_batch* b, int inst, const double* X_packed, double* out)
 int pdsdp_apply_M_adjoint(pdsdp_batch* b, int inst, const double* y, double* out_packed);
 int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_packed_out, double* lambda_out);
 
+/* Per-kernel CUDA-event timing of pdsdp_iterate (for the roofline report):
+ * out[0] iterate-kernel ms total, out[1] launches, out[2] residual-kernel ms
+ * total, out[3] launches.  enable != 0 switches recording on and clears. */
+int pdsdp_set_timing(pdsdp_batch* b, int enable);
+int pdsdp_kernel_times(pdsdp_batch* b, double* out /* [4] */);
+
+/* Eigensolver diagnostics of the last iteration of one instance:
+ * out[0..256) per pass (m, worst rel residual, slow column, theta, t, lo, cut, ||X+||),
+ * out[256..320) Ritz values, out[320..384) Ritz residual norms. */
+int pdsdp_debug(pdsdp_batch* b, int inst, double* out /* [384] */);
+
 const char* pdsdp_strerror(int code);
 const char* pdsdp_last_error(void);
 int pdsdp_version(void);

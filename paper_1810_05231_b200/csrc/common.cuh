@@ -35,11 +35,13 @@ struct State {
   double res[PDSDP_BMAX];
   double lamF[PDSDP_BMAX];   // eigenvalues of X_k   (clipped)
   double lamN[PDSDP_BMAX];   // eigenvalues of X_k+1 (clipped)
-  double lo;        // lower bound of spec(S) for the Chebyshev interval
+  double lo_par[2]; // lower bound of spec(S) for Z in zbuf[par] (Chebyshev interval)
   double ed2;       // sum (dy/alpha - M dX)^2
   double corr;      // sparse-support correction of the primal residual
   double finite;    // 1 when y+ and theta are finite
   double seed;
+  double mhint;     // total filter degree used by the previous iteration
+  double dbg[32][8];  // per pass: m, worst rel residual, slow column, theta, t, lo, cut, xnorm
 };
 
 // Per-instance descriptor (device resident).  Sizes and pointers only.
@@ -55,7 +57,8 @@ struct Inst {
   const int* tptr;     // [nz+1] contributors of M^T y to the slot
   const int* trow;     // constraint row of each contributor
   const double* tcoef; // scatter coefficient (packed value / s, s = 1 or sqrt 2)
-  double* zval;        // [nz] current Z values
+  double* zbuf0;       // [nz] Z = C + M^T y for y in ybuf0
+  double* zbuf1;       // [nz] ... for y in ybuf1
   const int* aptr;     // [mp+1] constraint rows in dense coordinates
   const int* ai;
   const int* aj;

@@ -23,9 +23,28 @@ namespace cg = cooperative_groups;
 namespace pdsdp {
 
 // tolerances of the eigensolver (relative to the spectral scale)
-#define PDSDP_TOL_KEEP 1e-13
+#define PDSDP_TOL_KEEP 1e-12   // ARPACK's tol in the reference (symmat.py:33), relative to the spectral scale
+#define PDSDP_TOL_X 1e-12      // admissible per-iteration error of X+ (relative to ||X+||_F)
 #define PDSDP_TOL_CERT 1e-8
 #define PDSDP_MMAX 24
+
+// Is Ritz pair i accurate enough?  i < r: kept in X+ (clipped at 0);
+// i == r: the certificate eigenvalue lambda_{r+1} (only its value matters).
+__device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, int r, int b,
+                                       double scale, double xnorm, bool need_cert) {
+  const double th = theta[i];
+  if (!(ri == ri) || !(th == th)) return true;          // non-finite: give up, reported as such
+  if (th + ri < 0.0) return true;                       // certainly clipped / certificate passes
+  if (i < r) {
+    if (ri <= PDSDP_TOL_KEEP * scale) return true;
+    // remaining effect on X+: |dtheta| <= ri plus rotation ~ 2 theta ri / gap (Davis-Kahan)
+    const double thr = (r < b) ? theta[r] : -1.0e308;
+    const double gap = th - thr;
+    const double impact = ri + 2.0 * fmax(th, 0.0) * fmin(1.0, ri / fmax(gap, 1e-300));
+    return impact <= PDSDP_TOL_X * xnorm;
+  }
+  return !need_cert || ri <= PDSDP_TOL_CERT * scale;
+}
 
 struct Sm {
   double *A, *Q, *L, *M, *T;   // lds x lds each
@@ -119,7 +138,8 @@ __device__ void colres_partial(const double* __restrict__ P, const double* __res
 
 // out = ca * (S Yin) + cb * Yin + cd * Yprev  on own rows, where
 // S Yin = F (LT) - alpha Z Yin  and LT = diag(lamF) F^T Yin (in smem).
-__device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ Yin,
+__device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
+                           const double* __restrict__ Yin,
                            const double* __restrict__ Yprev, double* __restrict__ out, int b, int rF,
                            double ca, double cb, double cd) {
   const int ld = d.ld;
@@ -132,7 +152,7 @@ __device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const doubl
     for (int l = 0; l < rF; ++l) w = fma(Fr[l], s.T[l * b + j], w);
     double z = 0.0;
     const int e1 = d.zptr[rho + 1];
-    for (int e = d.zptr[rho]; e < e1; ++e) z = fma(d.zval[e], Yin[(size_t)d.zcol[e] * ld + j], z);
+    for (int e = d.zptr[rho]; e < e1; ++e) z = fma(zv[e], Yin[(size_t)d.zcol[e] * ld + j], z);
     w = fma(-alpha, z, w);
     double o = ca * w;
     if (cb != 0.0) o = fma(cb, Yin[(size_t)rho * ld + j], o);
@@ -212,10 +232,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   double* buf[5] = {d.V, d.AV, d.Y0, d.Y1, d.Y2};
 
   // ---------------- prologue: F <- V[:, :rF] (X_k), block setup ----------------
+  // flags: bit0 cold start; bit1 the certificate eigenvalue lambda_{r+1} must be
+  // accurate (checkpoint iterations); bit2 re-run of the last iteration from
+  // the same (X_k, y_k) (F, lamF, Z_k kept) -- used when a checkpoint turns up
+  // in an iteration that ran without bit1.
   const int r = ctl.r;
   const int k = (r + 1 < n) ? r + 1 : n;
-  const bool cold = (ctl.flags & 1) || st->b == 0;
-  const int rF = cold ? 0 : st->rF;
+  const bool need_cert = (ctl.flags & 2) != 0;
+  const bool rerun = (ctl.flags & 4) != 0;
+  const bool cold = !rerun && ((ctl.flags & 1) || st->b == 0);
+  const int rF = cold ? 0 : (rerun ? st->rF_used : st->rF);
   const int b_old = cold ? 0 : st->b;
   int b = choose_block(k, n);
   if (b < b_old) b = b_old;
@@ -225,15 +251,17 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
     double th = (!cold && i < b_old) ? st->theta[i] : 0.0;
     s.theta[i] = th;
-    s.lamF[i] = (i < rF) ? fmax(th, 0.0) : 0.0;
+    s.lamF[i] = rerun ? st->lamF[i] : ((i < rF) ? fmax(th, 0.0) : 0.0);
     s.res[i] = (!cold && i < b_old) ? st->res[i] : 1.0e300;
   }
-  const double lo = st->lo;
+  const double lo = st->lo_par[ctl.ypar & 1];
   const double alpha = d.alpha;
+  const double* zv = (ctl.ypar & 1) ? d.zbuf1 : d.zbuf0;     // Z_k  = C + M^T y_k
+  double* zvn = (ctl.ypar & 1) ? d.zbuf0 : d.zbuf1;          // Z_k+1
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
     const int rho = x.r0 + it / b, j = it % b;
     double* Vr = d.V + (size_t)rho * ld;
-    if (j < rF) d.F[(size_t)rho * ld + j] = Vr[j];
+    if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = Vr[j];
     if (j >= b_old) Vr[j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
   }
   __syncthreads();
@@ -245,7 +273,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   int passes = 0, matvecs = 0, converged = 0;
   double prev_maxres = 1.0e300, maxres = 1.0e300;
   const int maxpass = ctl.maxpass > 0 ? ctl.maxpass : 60;
-  int mfail = 0;
+  int force_m = -1, msucc = 0, fails = 0;
+  const int hint = (int)st->mhint;
   for (int pass = 0; pass < maxpass; ++pass) {
     // ---- filter parameters (identical in every thread) ----
     int m = 0;
@@ -260,24 +289,34 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       if (top - fc <= fe) top = fc + 1.0001 * fe;
       sig1 = fe / (top - fc);
       // slowest still-needed column and required reduction
+      double xnorm = 0.0;
+      for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
+      xnorm = sqrt(xnorm);
       double rho_need = 1.0, tmin = 1.0e300;
+      int islow = -1;
       for (int i = 0; i < k; ++i) {
-        double tol = (i < r ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) * scale;
         double ri = s.res[i];
-        bool ok = (ri <= tol) || (s.theta[i] + ri < 0.0) || (fabs(s.theta[i]) + ri <= 1e-10 * scale);
-        if (!ok) {
+        if (!col_ok(i, ri, s.theta, r, b, scale, xnorm, need_cert)) {
+          double tol = (i < r) ? fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm) : PDSDP_TOL_CERT * scale;
           rho_need = fmax(rho_need, ri / tol);
           double t = (s.theta[i] - fc) / fe;
-          tmin = fmin(tmin, t);
+          if (t < tmin) { tmin = t; islow = i; }
         }
       }
-      if (rho_need <= 1.0) { m = 0; }
-      else {
+      if (force_m >= 0) {
+        m = force_m;                      // retry after a breakdown
+      } else if (pass == 0 && !rerun && hint > 0) {
+        // new PDHG iteration: the stored residuals belong to the previous S;
+        // reuse the filter degree the previous iteration needed
+        m = hint < 2 ? 2 : (hint > PDSDP_MMAX ? PDSDP_MMAX : hint);
+      } else if (rho_need <= 1.0) {
+        m = 0;
+      } else {
         double at = (tmin > 1.0 + 1e-6) ? acosh(tmin) : 0.0;
         m = (at > 0.0) ? (int)ceil(acosh(rho_need) / at) + 1 : 8;
         double t1 = (top - fc) / fe;
         double spread = acosh(fmax(t1, 1.0 + 1e-6)) - ((tmin > 1.0 + 1e-6) ? acosh(tmin) : 0.0);
-        double eps_rel = fmin(fmax(maxres / scale, 1e-16), 1.0);
+        double eps_rel = fmin(fmax(maxres, 1e-16), 1.0);
         if (spread > 1e-3) {
           int mcap = (int)floor(log(1e4 / eps_rel) / spread);
           if (mcap < 2) mcap = 2;
@@ -285,9 +324,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         }
         if (m < 2) m = 2;
         if (m > PDSDP_MMAX) m = PDSDP_MMAX;
-        if (mfail) m = max(1, m >> mfail);
+      }
+      if (x.c == 0 && tid == 0 && pass < 32) {
+        double* g = st->dbg[pass];
+        g[0] = m; g[1] = maxres; g[2] = islow; g[3] = islow >= 0 ? s.theta[islow] : 0.0;
+        g[4] = tmin; g[5] = lo; g[6] = cut; g[7] = xnorm;
       }
     }
+    force_m = -1;
     // ---- Chebyshev filter  Y_m = p_m(S) V ----
     int iy = 0;                       // buffer index holding Y_j (0 == V)
     int iyp = -1;                     // buffer holding Y_{j-1}
@@ -308,7 +352,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             gram_partial(d.F, rF, d.V, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
             cluster_reduce(d, x, rF * b, 0, s.T);
             scale_T(s, rF, b);
-            apply_rows(d, x, s, d.V, nullptr, buf[io], b, rF, ca, cb, 0.0);
+            apply_rows(d, x, s, zv, d.V, nullptr, buf[io], b, rF, ca, cb, 0.0);
             ++matvecs;
           }
         } else {
@@ -317,7 +361,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           gram_partial(d.F, rF, buf[iy], b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
           cluster_reduce(d, x, rF * b, 0, s.T);
           scale_T(s, rF, b);
-          apply_rows(d, x, s, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], b, rF, ca, cb, cd);
+          apply_rows(d, x, s, zv, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], b, rF, ca, cb, cd);
           ++matvecs;
           sg = sn;
         }
@@ -347,15 +391,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
     }
     scale_T(s, rF, b);
-    apply_rows(d, x, s, buf[iy], nullptr, buf[iw], b, rF, 1.0, 0.0, 0.0);
+    apply_rows(d, x, s, zv, buf[iy], nullptr, buf[iw], b, rF, 1.0, 0.0, 0.0);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
     bool okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
     if (!okc) {
-      // breakdown: filtered block lost rank; retry from V with a lower degree
-      mfail += 1;
-      theta_valid = theta_valid && (mfail < 6);
-      if (mfail >= 8) break;
+      // breakdown: the filtered block lost rank; retry from V with half the degree
+      if (++fails >= 8 || m == 0) break;
+      force_m = m / 2;
       __syncthreads();
       continue;
     }
@@ -387,7 +430,12 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe
     okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
-    if (!okc) { mfail += 1; if (mfail >= 8) break; continue; }
+    if (!okc) {
+      if (++fails >= 8 || m == 0) break;
+      force_m = m / 2;
+      continue;
+    }
+    msucc += m;
     tri_inv_lower(s.A, s.L, b, lds);            // L = L2^-1
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
@@ -431,24 +479,21 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     ++passes;
     {
       double scale = fmax(fmax(fabs(s.theta[0]), fabs(lo)), 1e-300);
+      double xnorm = 0.0;
+      for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
+      xnorm = sqrt(xnorm);
       bool ok_all = true;
       maxres = 0.0;
       for (int i = 0; i < b; ++i) {
         double ri = sqrt(fmax(s.red1[i], 0.0));
-        if (tid == 0) s.res[i] = ri;   // only thread 0 writes; reads below use ri
-        if (i < k) {
-          double tol = (i < r ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) * scale;
-          bool ok = (ri <= tol) || (s.theta[i] + ri < 0.0) || (fabs(s.theta[i]) + ri <= 1e-10 * scale);
-          if (!ok) { ok_all = false; maxres = fmax(maxres, ri / scale); }
-        }
-        if (!isfinite(s.theta[i]) || !isfinite(ri)) ok_all = true;  // give up on non-finite
+        if (tid == 0) s.res[i] = ri;
+        if (i < k && !col_ok(i, ri, s.theta, r, b, scale, xnorm, need_cert)) { ok_all = false; maxres = fmax(maxres, ri / scale); }
       }
       __syncthreads();
       if (ok_all) { converged = 1; break; }
       // stagnation at the rounding floor
       if (pass >= 2 && maxres > 0.5 * prev_maxres && maxres < 1e-10) { converged = 2; break; }
       prev_maxres = maxres;
-      mfail = 0;
     }
   }
   for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) s.lamN[i] = (i < r && i < b) ? fmax(s.theta[i], 0.0) : 0.0;
@@ -531,7 +576,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         z = fma(yn[row], cf, z);
         a = fma(d.dy[row], cf, a);
       }
-      d.zval[e] = z;
+      zvn[e] = z;
       const int i = d.zrow[e], j = d.zcol[e];
       if (j >= i) {
         const double* Vi = d.V + (size_t)i * ld; const double* Vj = d.V + (size_t)j * ld;
@@ -549,7 +594,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   double gmax = 0.0;
   for (int rho = x.r0 + tid; rho < x.r1; rho += blockDim.x) {
     double sacc = 0.0;
-    for (int e = d.zptr[rho]; e < d.zptr[rho + 1]; ++e) sacc += fabs(d.zval[e]);
+    for (int e = d.zptr[rho]; e < d.zptr[rho + 1]; ++e) sacc += fabs(zvn[e]);
     gmax = fmax(gmax, sacc);
   }
   {
@@ -581,10 +626,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       st->b = b;
       st->rF = rN;
       st->theta_valid = theta_valid ? 1 : 0;
+      if (!rerun && msucc > 0) st->mhint = msucc;
       st->iav = iav;
       st->ed2 = ed2_tot;
       st->corr = s.red1[0];
-      st->lo = -alpha * s.red1[1];
+      st->lo_par[(ctl.ypar & 1) ^ 1] = -alpha * s.red1[1];
       st->finite = fin_tot;
       double* o = d.out;
       o[O_LAM] = s.theta[k - 1];

@@ -90,6 +90,9 @@ struct pdsdp_batch {
   unsigned* d_objcnt = nullptr;
   double* d_objres = nullptr;
   int max_tiles = 1;
+  int timing = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0;
 };
 
 namespace {
@@ -259,7 +262,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 16) + 255) & ~size_t(255); };
   add((I.n + 1) * 4); add(I.nz * 4); add(I.nz * 4); add(I.nz * 8); add((I.nz + 1) * 4);
-  add(I.trow.size() * 4 + 4); add(I.tcoef.size() * 8 + 8); add(I.nz * 8);
+  add(I.trow.size() * 4 + 4); add(I.tcoef.size() * 8 + 8); add(I.nz * 8); add(I.nz * 8);
   add((I.mp + 1) * 4); add(I.ai.size() * 4 + 4); add(I.aj.size() * 4 + 4); add(I.ag.size() * 8 + 8);
   add((C + 1) * 4); add(I.bv.size() * 8 + 8); add(I.hv.size() * 8 + 8);
   for (int k = 0; k < 6; ++k) add(nld * 8);
@@ -290,7 +293,8 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   if ((rc = upload(a, trow, I.trow))) return rc;
   if ((rc = upload(a, tcoef, I.tcoef))) return rc;
   d.zptr = zptr; d.zcol = zcol; d.zrow = zrow; d.cval = cval; d.tptr = tptr; d.trow = trow; d.tcoef = tcoef;
-  d.zval = a.take<double>(I.nz + 1);
+  d.zbuf0 = a.take<double>(I.nz + 1);
+  d.zbuf1 = a.take<double>(I.nz + 1);
   int *aptr, *ai, *aj; double* ag;
   if ((rc = upload(a, aptr, I.aptr))) return rc;
   if ((rc = upload(a, ai, I.ai))) return rc;
@@ -461,6 +465,7 @@ int pdsdp_batch_destroy(pdsdp_batch* b) {
   if (b->d_objpart) cudaFree(b->d_objpart);
   if (b->d_objcnt) cudaFree(b->d_objcnt);
   if (b->d_objres) cudaFree(b->d_objres);
+  for (int k = 0; k < 3; ++k) if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   if (b->stream) cudaStreamDestroy(b->stream);
   delete b;
   return PDSDP_OK;
@@ -529,8 +534,9 @@ int pdsdp_set_alpha(pdsdp_batch* b, int inst, double alpha) {
 
 __global__ void init_finalize_kernel(const Inst* insts, int inst, double seed) {
   State* st = insts[inst].st;
-  const double g = st->lo;
-  st->lo = -insts[inst].alpha * g;
+  const double g = st->lo_par[0];
+  st->lo_par[0] = -insts[inst].alpha * g;
+  st->lo_par[1] = st->lo_par[0];
   st->seed = seed;
   st->b = 0; st->rF = 0; st->theta_valid = 0; st->iav = 1; st->rF_used = 0; st->r_cur = 0;
 }
@@ -570,17 +576,53 @@ int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t*
   }
   CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, N * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
   CK(cudaMemcpyAsync(b->d_active, b->h_active, nact * sizeof(int), cudaMemcpyHostToDevice, b->stream));
+  if (b->timing) CK(cudaEventRecord(b->ev[0], b->stream));
   int rc = launch_iterate(b, nact);
   if (rc) return rc;
+  if (b->timing) CK(cudaEventRecord(b->ev[1], b->stream));
   int maxr = 1;
   for (int a = 0; a < nact; ++a) maxr = std::max(maxr, (int)rank[a]);
   const int kp = std::min(RES_KMAX, (2 * std::min(maxr, PDSDP_BMAX) + 3) & ~3);
   const size_t rsm = (size_t)2 * RES_TILE * (kp + 1) * sizeof(double);
   residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_active);
   CK(cudaGetLastError());
+  if (b->timing) CK(cudaEventRecord(b->ev[2], b->stream));
   CK(cudaStreamSynchronize(b->stream));
+  if (b->timing) {
+    float a = 0.f, c = 0.f;
+    CK(cudaEventElapsedTime(&a, b->ev[0], b->ev[1]));
+    CK(cudaEventElapsedTime(&c, b->ev[1], b->ev[2]));
+    b->t_iter += a; b->n_iter += 1; b->t_res += c; b->n_res += 1;
+  }
   for (int a = 0; a < nact; ++a)
     memcpy(out + (size_t)a * PDSDP_OUT_LEN, b->h_out + (size_t)insts[a] * PDSDP_OUT_LEN, PDSDP_OUT_LEN * sizeof(double));
+  return PDSDP_OK;
+}
+
+int pdsdp_set_timing(pdsdp_batch* b, int enable) {
+  if (!b) return fail(PDSDP_EINVAL, "batch is NULL");
+  for (int k = 0; k < 3; ++k)
+    if (!b->ev[k]) CK(cudaEventCreate(&b->ev[k]));
+  b->timing = enable ? 1 : 0;
+  b->t_iter = b->n_iter = b->t_res = b->n_res = 0.0;
+  return PDSDP_OK;
+}
+
+int pdsdp_debug(pdsdp_batch* b, int inst, double* out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (!out) return fail(PDSDP_EINVAL, "out is NULL");
+  State h;
+  CK(cudaMemcpy(&h, b->inst[inst]->desc.st, sizeof(State), cudaMemcpyDeviceToHost));
+  memcpy(out, h.dbg, sizeof(h.dbg));
+  memcpy(out + 256, h.theta, sizeof(h.theta));
+  memcpy(out + 320, h.res, sizeof(h.res));
+  return PDSDP_OK;
+}
+
+int pdsdp_kernel_times(pdsdp_batch* b, double* out) {
+  if (!b || !out) return fail(PDSDP_EINVAL, "bad arguments");
+  out[0] = b->t_iter; out[1] = b->n_iter; out[2] = b->t_res; out[3] = b->n_res;
   return PDSDP_OK;
 }
 
@@ -689,7 +731,7 @@ int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_pack
   pdsdp_batch* b = nullptr;
   int rc = pdsdp_batch_create(1, &pr, &b);
   if (rc) return rc;
-  int32_t inst = 0, rr = r, yp = 0, fl = 1;
+  int32_t inst = 0, rr = r, yp = 0, fl = 1 | 2;
   double out[PDSDP_OUT_LEN];
   rc = pdsdp_set_alpha(b, 0, 1.0);
   if (!rc) rc = pdsdp_reset(b, 0, 0.0);

@@ -205,7 +205,7 @@ __global__ void pack_kernel(const Inst* __restrict__ insts, int inst, int which,
 // reset: y = 0, Z = C, state cleared; gersh(C) via max over rows
 __global__ void init_kernel(const Inst* __restrict__ insts, int inst, double seed) {
   const Inst d = insts[inst];
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d.nz; e += gridDim.x * blockDim.x) d.zval[e] = d.cval[e];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d.nz; e += gridDim.x * blockDim.x) { d.zbuf0[e] = d.cval[e]; d.zbuf1[e] = d.cval[e]; }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.mp; i += gridDim.x * blockDim.x) {
     d.ybuf0[i] = 0.0; d.ybuf1[i] = 0.0; d.dy[i] = 0.0;
   }
@@ -218,7 +218,7 @@ __global__ void init_kernel(const Inst* __restrict__ insts, int inst, double see
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
   if ((threadIdx.x & 31) == 0 && g > 0.0)
-    atomicMax((unsigned long long*)&d.st->lo, (unsigned long long)__double_as_longlong(g));  // non-negative doubles order as integers
+    atomicMax((unsigned long long*)&d.st->lo_par[0], (unsigned long long)__double_as_longlong(g));  // non-negative doubles order as integers
 }
 
 }  // namespace pdsdp

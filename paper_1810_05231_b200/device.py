@@ -31,7 +31,8 @@ EXPORTED = (
     "pdsdp_opnorm_positions", "pdsdp_opnorm_run", "pdsdp_set_alpha", "pdsdp_reset",
     "pdsdp_iterate", "pdsdp_objective", "pdsdp_download_x", "pdsdp_download_y",
     "pdsdp_apply_M", "pdsdp_apply_M_adjoint", "pdsdp_aproj_psd", "pdsdp_strerror",
-    "pdsdp_last_error", "pdsdp_version",
+    "pdsdp_last_error", "pdsdp_version", "pdsdp_set_timing", "pdsdp_kernel_times",
+    "pdsdp_debug",
 )
 
 
@@ -78,6 +79,9 @@ def load_library(path: str = LIB_PATH):
             "pdsdp_strerror": (ct.c_char_p, [ct.c_int]),
             "pdsdp_last_error": (ct.c_char_p, []),
             "pdsdp_version": (ct.c_int, []),
+            "pdsdp_set_timing": (ct.c_int, [P, ct.c_int]),
+            "pdsdp_kernel_times": (ct.c_int, [P, P]),
+            "pdsdp_debug": (ct.c_int, [P, ct.c_int, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -147,6 +151,20 @@ class DeviceBatch:
 
     def stream_handle(self) -> int:
         return self.lib.pdsdp_batch_stream(self.h) or 0
+
+    def set_timing(self, enable: bool):
+        _check(self.lib.pdsdp_set_timing(self.h, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        out = np.zeros(4)
+        _check(self.lib.pdsdp_kernel_times(self.h, _ptr(out)))
+        return {"iterate_ms": out[0], "iterate_launches": int(out[1]),
+                "residual_ms": out[2], "residual_launches": int(out[3])}
+
+    def debug(self, inst: int = 0) -> dict:
+        out = np.zeros(384)
+        _check(self.lib.pdsdp_debug(self.h, inst, _ptr(out)))
+        return {"passes": out[:256].reshape(32, 8), "theta": out[256:320], "res": out[320:384]}
 
     # ---- operator norm (problem.py:157-185) ----
     def opnorm_positions(self, inst: int) -> np.ndarray:

@@ -46,6 +46,7 @@ _NORM_MAX_ITER = 10_000
 _NORM_REL_TOL = 1e-10
 _NORM_SAFETY = 1.0 + 1e-7
 _NORM_CHUNK = 256
+FLAG_COLD, FLAG_CERT, FLAG_RERUN = 1, 2, 4
 
 
 def _device_batch(prob: SdpProblem) -> DeviceBatch:
@@ -130,45 +131,53 @@ class _DeviceIterate:
         return self.batch.objective(self.inst, self.which)
 
 
-def solve_lr_pd_sdp(
-    prob: SdpProblem,
-    config: SolverConfig | None = None,
-    callback: ProgressCallback | None = None,
-    *,
-    stats: dict | None = None,
-) -> SolveResult:
-    """Rank-adaptive primal-dual iteration from a zero start
-    (reference ``lowrank.py:102-208``); per-iteration work on the B200."""
-    config = config or SolverConfig()
-    config.validate()
-    t0 = time.perf_counter()
+class LoopOutcome:
+    """What the host loop leaves behind (iterates stay on the device)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverConfig,
+                alpha: float, callback: ProgressCallback | None = None,
+                t0: float | None = None) -> LoopOutcome:
+    """The ``for k`` loop of reference ``lowrank.py:125-190`` on a resident
+    instance: one device call per iteration, scalars back, host decisions."""
+    t0 = time.perf_counter() if t0 is None else t0
     n = prob.n
-    batch = _device_batch(prob)
-    alpha = step_size(prob, config)
     eps_lambda = (config.eps_lambda if config.eps_lambda is not None
                   else DEFAULT_EPS_LAMBDA_PER_N * n)
     controller = RankController(r=min(max(config.initial_rank, 1), n), ell=config.window_ell)
-    batch.set_alpha(0, alpha)
-    batch.reset(0, 0.0)
-    it = _DeviceIterate(batch, 0)
+    batch.set_alpha(inst, alpha)
+    batch.reset(inst, 0.0)
+    it = _DeviceIterate(batch, inst)
     rank_path = [(0, controller.r)]
     status = None
     res = (math.nan, math.nan, math.nan)
     scale = 1.0
     eig_passes = eig_matvecs = eig_unconverged = 0
     for k in range(1, config.max_iter + 1):
-        out = batch.iterate([0], [controller.r], [it.ypar])[0]
+        out = batch.iterate([inst], [controller.r], [it.ypar])[0]
         eig_passes += int(out[OUT_PASSES])
         eig_matvecs += int(out[OUT_MATVECS])
+        if out[OUT_FINITE] == 1.0:
+            ec = float(out[OUT_EPS_P]) + float(out[OUT_EPS_D])
+            sc = (1.0 + ec) if (k == 1 and config.relative_residuals) else scale
+            if ec <= config.eps_tol * sc:
+                # checkpoint iteration: the certificate needs lambda_{r+1} to the
+                # reference's accuracy; re-run this iteration from the same
+                # (X_k, y_k) with the certificate eigenpair converged too
+                out = batch.iterate([inst], [controller.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
+                eig_passes += int(out[OUT_PASSES])
+                eig_matvecs += int(out[OUT_MATVECS])
         if out[OUT_EIGCONV] == 0:
             eig_unconverged += 1
             logger.info("eigensolver hit its pass limit at k=%d (r=%d)", k, controller.r)
-        if out[OUT_FINITE] != 1.0:
+        if out[OUT_FINITE] != 1.0:                       # _finite, lowrank.py:145-147
             status = SolveStatus.DIVERGED
             it.which = 1
             break
-        # state.advance (pdhg.py:113-118)
-        it.k = k
+        it.k = k                                         # state.advance, pdhg.py:113-118
         it.ypar ^= 1
         it.which = 0
         lambda_r = float(out[OUT_LAMBDA])
@@ -200,16 +209,36 @@ def solve_lr_pd_sdp(
             break
     if status is None:
         status = SolveStatus.MAX_ITERATIONS
-    X = it.X()
-    y = it.y()
-    pobj = prob.C.inner(X)
+    return LoopOutcome(status=status, it=it, res=res, rank_path=rank_path, controller=controller,
+                       scale=scale, eig_passes=eig_passes, eig_matvecs=eig_matvecs,
+                       eig_unconverged=eig_unconverged)
+
+
+def solve_lr_pd_sdp(
+    prob: SdpProblem,
+    config: SolverConfig | None = None,
+    callback: ProgressCallback | None = None,
+    *,
+    stats: dict | None = None,
+) -> SolveResult:
+    """Rank-adaptive primal-dual iteration from a zero start
+    (reference ``lowrank.py:102-208``); per-iteration work on the B200."""
+    config = config or SolverConfig()
+    config.validate()
+    t0 = time.perf_counter()
+    batch = _device_batch(prob)
+    alpha = step_size(prob, config)
+    o = run_lr_loop(batch, 0, prob, config, alpha, callback, t0)
+    X = o.it.X()
+    y = o.it.y()
+    pobj = prob.C.inner(X)                               # lowrank.py:191-194
     dobj = -float(prob.b @ y[: prob.m] + prob.h @ y[prob.m:])
     if stats is not None:
-        stats.update(eig_passes=eig_passes, eig_matvecs=eig_matvecs,
-                     eig_unconverged=eig_unconverged, alpha=alpha)
+        stats.update(eig_passes=o.eig_passes, eig_matvecs=o.eig_matvecs,
+                     eig_unconverged=o.eig_unconverged, alpha=alpha)
     return SolveResult(
-        status=status, X=X, y=y, primal_objective=pobj, dual_objective=dobj,
-        final_residuals=res, iterations=it.k, rank_path=rank_path,
-        checkpoints=controller.checkpoints, wall_time_s=time.perf_counter() - t0,
-        residual_scale=scale, objective_sign=prob.objective_sign,
+        status=o.status, X=X, y=y, primal_objective=pobj, dual_objective=dobj,
+        final_residuals=o.res, iterations=o.it.k, rank_path=o.rank_path,
+        checkpoints=o.controller.checkpoints, wall_time_s=time.perf_counter() - t0,
+        residual_scale=o.scale, objective_sign=prob.objective_sign,
     )

@@ -1,0 +1,220 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+own outputs (golden fixtures from tests/golden/make_golden.py) and the CPU
+oracle on the same seeded inputs.
+
+Tolerances are the north star's (BASELINE.json): iterates within 1e-8
+relative Frobenius at a fixed iteration count, objectives within 1e-5
+relative, the same 1e-4 stopping rule met at the same iteration.  Integer /
+index outputs (iteration counts, rank paths, statuses) must match exactly.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, problem_from_golden
+from oracle import lrpdhg_oracle as orc
+import paper_1810_05231_b200 as pk
+from paper_1810_05231_b200 import workloads
+from paper_1810_05231_b200.config import SolverConfig
+
+pytestmark = pytest.mark.gpu
+
+ITER_TOL = 1e-8      # relative Frobenius, fixed K
+OBJ_TOL = 1e-5       # relative objective
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+def with_iters(cfg, K, **kw):
+    return SolverConfig(**{**cfg.__dict__, "max_iter": K, **kw})
+
+
+# ---------------------------------------------------------------- op level
+
+@pytest.mark.parametrize("ci", range(5))
+def test_linear_maps_and_opnorm(ci):
+    d = load_golden("ops_small.npz")
+    pre = f"c{ci}_"
+    prob = problem_from_golden(d, pre)
+    n = prob.n
+    mx = pk.apply_M(prob, pk.SymMatrix(n, d[pre + "X"]))
+    np.testing.assert_allclose(mx, d[pre + "MX"], rtol=0, atol=1e-12)
+    mty = pk.apply_M_adjoint(prob, d[pre + "y"]).data
+    np.testing.assert_allclose(mty, d[pre + "MTy"], rtol=0, atol=1e-12)
+    assert pk.estimate_operator_norm(prob, 0) == pytest.approx(float(d[pre + "opnorm"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("ci", range(5))
+def test_aproj_psd_matches_reference(ci):
+    d = load_golden("ops_small.npz")
+    pre = f"c{ci}_"
+    n = int(d[pre + "n"])
+    S = pk.SymMatrix(n, d[pre + "S"])
+    for r in (1, 3, n // 2, n):
+        P, lam = pk.aproj_psd(S, r)
+        ref = d[pre + f"aproj{r}"]
+        assert rel(P.data, ref) <= ITER_TOL
+        assert lam == pytest.approx(float(d[pre + f"aproj{r}_lam"]), rel=1e-9, abs=1e-11)
+
+
+def test_aproj_known_answer_and_errors():
+    # reference test_symmat.py:197-201 (pins lambda_{r+1})
+    P, lam = pk.aproj_psd(pk.SymMatrix.from_dense(np.diag([5.0, 3.0, -1.0])), 1)
+    np.testing.assert_allclose(P.to_dense(), np.diag([5.0, 0.0, 0.0]), atol=1e-12)
+    assert lam == pytest.approx(3.0)
+    with pytest.raises(ValueError, match="outside"):
+        pk.aproj_psd(pk.SymMatrix.from_dense(np.eye(3)), 0)
+    with pytest.raises(ValueError, match="outside"):
+        pk.aproj_psd(pk.SymMatrix.from_dense(np.eye(3)), 4)
+
+
+def test_aproj_random_vs_oracle(rng):
+    for n, r in ((33, 4), (80, 7), (150, 12), (300, 20)):
+        R = rng.standard_normal((n, n))
+        S = orc.pack(0.5 * (R + R.T))
+        P, lam = pk.aproj_psd(pk.SymMatrix(n, S), r)
+        Pr, lr = orc.aproj_psd(S, n, r)
+        assert rel(P.data, Pr) <= ITER_TOL
+        assert lam == pytest.approx(lr, rel=1e-8)
+
+
+# ---------------------------------------------------------------- full solves
+
+@pytest.mark.parametrize("ci", range(5))
+def test_small_lr_solves_match_reference(ci):
+    d = load_golden("lr_small.npz")
+    pre = f"c{ci}_"
+    prob = problem_from_golden(d, pre)
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=400, initial_rank=int(d[pre + "r0"]),
+                       window_ell=50, time_limit_s=1e9)
+    res = pk.solve_lr_pd_sdp(prob, cfg)
+    assert res.status.value == str(d[pre + "status"])
+    assert res.iterations == int(d[pre + "iters"])
+    assert [tuple(x) for x in res.rank_path] == [tuple(x) for x in d[pre + "rank_path"].tolist()]
+    assert rel(res.X.data, d[pre + "X"]) <= ITER_TOL
+    assert rel(res.y, d[pre + "y"]) <= ITER_TOL
+    assert res.primal_objective == pytest.approx(float(d[pre + "pobj"]), rel=OBJ_TOL)
+    assert res.dual_objective == pytest.approx(float(d[pre + "dobj"]), rel=OBJ_TOL)
+    assert res.residual_scale == pytest.approx(float(d[pre + "scale"]), rel=1e-10)
+
+
+def test_config1_end_to_end_matches_reference():
+    d = load_golden("cfg1.npz")
+    prob, cfg = workloads.config(0)
+    for K in (1, 10, 100):
+        res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, K))
+        assert res.iterations == K
+        assert rel(res.X.data, d[f"X{K}"]) <= ITER_TOL
+        assert rel(res.y, d[f"y{K}"]) <= ITER_TOL
+        np.testing.assert_allclose(res.final_residuals, d[f"res{K}"], rtol=1e-8)
+    hist = []
+    res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, cfg.max_iter, progress_every=1),
+                             callback=lambda info: hist.append(tuple(info)))
+    assert res.status.value == str(d["status"]) == "optimal"
+    assert res.iterations == int(d["iters"]) == 1718
+    assert [tuple(x) for x in res.rank_path] == [tuple(x) for x in d["rank_path"].tolist()]
+    assert rel(res.X.data, d["X_final"]) <= ITER_TOL
+    assert res.primal_objective == pytest.approx(float(d["pobj"]), rel=OBJ_TOL)
+    assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
+    assert len(res.checkpoints) == len(d["checkpoints"])
+    for c, (rk, obj) in zip(res.checkpoints, d["checkpoints"]):
+        assert c.rank == int(rk) and c.objective == pytest.approx(obj, rel=OBJ_TOL)
+    h = np.array(hist)
+    np.testing.assert_allclose(h[:, 1:4], d["history"][:, 1:4], rtol=1e-6)
+    np.testing.assert_allclose(h[:, 5], d["history"][:, 5], rtol=1e-8)
+
+
+@pytest.mark.parametrize("idx,fname", [(4, "cfg5_sketch.npz"), (3, "cfg4_sketch.npz"),
+                                       (1, "cfg2_sketch.npz"), (2, "cfg3_sketch.npz")])
+def test_large_configs_fixed_K_sketches(idx, fname):
+    """Configs 2-5 at the reference's full sizes, fixed K: y, diag(X), the
+    sketch X z for a seeded z, ||X||_F, tr(CX) and the residuals."""
+    d = load_golden(fname)
+    prob, cfg = workloads.config(idx)
+    z = np.random.default_rng(777).standard_normal(prob.n)
+    # the power iteration stops on |s - sigma| <= 1e-10 s (problem.py:181), so
+    # estimates agree to that order, not to rounding
+    assert pk.estimate_operator_norm(prob, cfg.seed) == pytest.approx(float(d["opnorm"]), rel=1e-9)
+    for K in d["Ks"].tolist():
+        res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, int(K)))
+        Xd = res.X.to_dense()
+        assert rel(res.y, d[f"y{K}"]) <= ITER_TOL
+        assert rel(Xd @ z, d[f"Xz{K}"]) <= ITER_TOL
+        assert rel(np.diag(Xd), d[f"diag{K}"]) <= ITER_TOL
+        assert np.linalg.norm(Xd) == pytest.approx(float(d[f"fro{K}"]), rel=ITER_TOL)
+        assert res.primal_objective == pytest.approx(float(d[f"pobj{K}"]), rel=OBJ_TOL, abs=1e-9)
+        np.testing.assert_allclose(res.final_residuals, d[f"res{K}"], rtol=1e-7)
+
+
+def test_oracle_parity_with_inequalities(rng):
+    """Seeded random problems with inequality rows (exercises min(u/alpha, h)),
+    against the oracle at fixed K."""
+    for n, m, p, r0 in ((20, 10, 12, 1), (50, 20, 30, 3)):
+        R = rng.standard_normal((n, n))
+        C = pk.SymMatrix.from_dense(R @ R.T / n)
+        rows = []
+        for _ in range(m + p):
+            ents = [(int(i), int(j), float(rng.standard_normal()))
+                    for i, j in {tuple(sorted(rng.integers(0, n, 2))) for _ in range(4)}]
+            rows.append(pk.SparseRow.from_matrix_entries(n, ents))
+        prob = pk.SdpProblem(n=n, C=C, A=rows[:m], b=np.abs(rng.standard_normal(m)) + 0.5,
+                             G=rows[m:], h=np.abs(rng.standard_normal(p)) + 0.2)
+        cfg = SolverConfig(eps_tol=1e-6, max_iter=150, initial_rank=r0, window_ell=40)
+        res = pk.solve_lr_pd_sdp(prob, cfg)
+        ref = orc.solve_lr(prob, cfg)
+        assert res.iterations == ref.iterations
+        assert res.rank_path == ref.rank_path
+        assert rel(res.X.data, ref.X) <= ITER_TOL
+        assert rel(res.y, ref.y) <= ITER_TOL
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_oversized_steps_follow_reference():
+    # reference test_pdhg.py:296-305 (alpha = 2/||M||) plus overflow regimes:
+    # status and iteration count must match the oracle exactly.
+    for n, a, K in ((2, None, 3000), (2, 1e100, 50), (40, 1e200, 50)):
+        prob = pk.SdpProblem(n=n, C=pk.SymMatrix.from_dense(np.eye(n)),
+                             A=[pk.SparseRow.from_matrix_entries(n, [(i, i, 1.0) for i in range(n)])],
+                             b=np.array([1.0]))
+        alpha = 2.0 / orc.op_norm(orc.stacked_csr(prob)) if a is None else a
+        cfg = SolverConfig(alpha_override=alpha, max_iter=K, initial_rank=1)
+        res = pk.solve_lr_pd_sdp(prob, cfg)
+        ref = orc.solve_lr(prob, cfg)
+        assert res.status.value == ref.status
+        assert res.iterations == ref.iterations
+        if np.all(np.isfinite(ref.y)):
+            assert rel(res.y, ref.y) <= ITER_TOL
+
+
+def test_full_rank_and_tiny_problems():
+    # r = n (no truncation, certificate vacuous) and n = 1
+    prob = workloads.maxcut_problem(12, 0.5, 3, signed=True)
+    cfg = SolverConfig(eps_tol=1e-5, max_iter=300, initial_rank=12)
+    res = pk.solve_lr_pd_sdp(prob, cfg)
+    ref = orc.solve_lr(prob, cfg)
+    assert res.status.value == ref.status and res.iterations == ref.iterations
+    assert rel(res.X.data, ref.X) <= ITER_TOL
+    one = pk.SdpProblem(n=1, C=pk.SymMatrix(1, np.array([2.0])),
+                        A=[pk.SparseRow(np.array([0]), np.array([1.0]))], b=np.array([3.0]))
+    res = pk.solve_lr_pd_sdp(one, SolverConfig(max_iter=100))
+    ref = orc.solve_lr(one, SolverConfig(max_iter=100))
+    assert res.iterations == ref.iterations and res.status.value == ref.status
+    assert res.primal_objective == pytest.approx(ref.primal_objective, rel=OBJ_TOL)
+
+
+def test_rank_above_block_limit_fails_loudly():
+    prob = workloads.maxcut_problem(200, 0.1, 0, signed=False)
+    with pytest.raises(ValueError, match="eigen block"):
+        pk.solve_lr_pd_sdp(prob, SolverConfig(initial_rank=80, max_iter=2))
+
+
+def test_time_limit_and_max_iter_status():
+    prob, cfg = workloads.config(0)
+    res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, 7))
+    assert res.status.value == "max_iterations" and res.iterations == 7
+    res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, 100000, time_limit_s=1e-9))
+    assert res.status.value == "time_limit" and res.iterations == 1
