@@ -136,20 +136,24 @@ __device__ void colres_partial(const double* __restrict__ P, const double* __res
   __syncthreads();
 }
 
-// out = ca * (S Yin) + cb * Yin + cd * Yprev  on own rows, where
-// S Yin = F (LT) - alpha Z Yin  and LT = diag(lamF) F^T Yin (in smem).
+// Columns [c0, c0+bc) of  out = ca * (S_d Yin) + cb * Yin + cd * Yprev  on own rows:
+//   S_d Yin = F T_F + Vl T_V - alpha Z Yin
+// with T (smem, (rF + nlock) x bc, flat) already scaled: T_F = diag(lamF) F^T Yin
+// and T_V = -diag(theta) Vl^T Yin (deflation of locked Ritz pairs, nlock may be 0).
 __device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
-                           const double* __restrict__ Yin,
-                           const double* __restrict__ Yprev, double* __restrict__ out, int b, int rF,
+                           const double* __restrict__ Yin, const double* __restrict__ Yprev,
+                           double* __restrict__ out, int c0, int bc, int rF, int nlock,
                            double ca, double cb, double cd) {
   const int ld = d.ld;
   const int nl = x.r1 - x.r0;
   const double alpha = d.alpha;
-  for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
-    const int rho = x.r0 + it / b, j = it % b;
+  for (int it = threadIdx.x; it < nl * bc; it += blockDim.x) {
+    const int rho = x.r0 + it / bc, jj = it % bc, j = c0 + jj;
     double w = 0.0;
     const double* Fr = d.F + (size_t)rho * ld;
-    for (int l = 0; l < rF; ++l) w = fma(Fr[l], s.T[l * b + j], w);
+    for (int l = 0; l < rF; ++l) if (s.lamF[l] != 0.0) w = fma(Fr[l], s.T[l * bc + jj], w);
+    const double* Vr = d.V + (size_t)rho * ld;
+    for (int l = 0; l < nlock; ++l) w = fma(Vr[l], s.T[(rF + l) * bc + jj], w);
     double z = 0.0;
     const int e1 = d.zptr[rho + 1];
     for (int e = d.zptr[rho]; e < e1; ++e) z = fma(zv[e], Yin[(size_t)d.zcol[e] * ld + j], z);
@@ -175,12 +179,27 @@ __device__ void rotate_rows(const Inst& d, const Cta& x, const double* __restric
   }
 }
 
-// T (smem, rF x b) <- lamF .* T  (in place): LT used by apply_rows
-__device__ void scale_T(const Sm& s, int rF, int b) {
-  for (int e = threadIdx.x; e < rF * b; e += blockDim.x) {
-    s.T[e] *= s.lamF[e / b];
+// T (smem, (rF + nlock) x bc) <- [diag(lamF); -diag(theta)] .* T  (in place)
+__device__ void scale_T(const Sm& s, int rF, int nlock, int bc) {
+  for (int e = threadIdx.x; e < (rF + nlock) * bc; e += blockDim.x) {
+    const int l = e / bc;
+    const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
+    s.T[e] = (c == 0.0) ? 0.0 : s.T[e] * c;
   }
   __syncthreads();
+}
+
+// One operator product on columns [c0, c0+bc): reduction of [F | Vl]^T Yin
+// (one cluster barrier, which also publishes Yin to every CTA), then rows.
+__device__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* zv, const double* Yin,
+                              const double* Yprev, double* out, int c0, int bc, int rF, int nlock,
+                              double ca, double cb, double cd) {
+  double* slot = red_slot(d, x, x.c);
+  gram_partial(d.F, rF, Yin + c0, bc, d.ld, x.r0, x.r1, slot, s.scr);
+  gram_partial(d.V, nlock, Yin + c0, bc, d.ld, x.r0, x.r1, slot + rF * bc, s.scr);
+  cluster_reduce(d, x, (rF + nlock) * bc, 0, s.T);
+  scale_T(s, rF, nlock, bc);
+  apply_rows(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
 }
 
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
@@ -251,7 +270,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
     double th = (!cold && i < b_old) ? st->theta[i] : 0.0;
     s.theta[i] = th;
-    s.lamF[i] = rerun ? st->lamF[i] : ((i < rF) ? fmax(th, 0.0) : 0.0);
+    s.lamF[i] = rerun ? st->lamF[i] : ((i < rF && th > 0.0) ? th : 0.0);
     s.res[i] = (!cold && i < b_old) ? st->res[i] : 1.0e300;
   }
   const double lo = st->lo_par[ctl.ypar & 1];
@@ -276,63 +295,83 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   int force_m = -1, msucc = 0, fails = 0;
   const int hint = (int)st->mhint;
   for (int pass = 0; pass < maxpass; ++pass) {
-    // ---- filter parameters (identical in every thread) ----
-    int m = 0;
+    // ---- pass plan (identical in every thread): degree m, active columns
+    //      [c0, c0+bc) to filter, nlock locked (deflated) leading pairs ----
+    int m = 0, c0 = 0, bc = b, nlock = 0;
     double fe = 1.0, fc = 0.0, sig1 = 1.0;
     if (theta_valid && b < n) {
-      double cut = s.theta[b - 1], top = s.theta[0];
-      double scale = fmax(fmax(fabs(top), fabs(lo)), 1e-300);
-      double lo_ = fmin(lo, cut);
-      fe = 0.5 * (cut - lo_);
-      fc = 0.5 * (cut + lo_);
-      if (fe < 1e-14 * scale) fe = 1e-14 * scale;
-      if (top - fc <= fe) top = fc + 1.0001 * fe;
-      sig1 = fe / (top - fc);
-      // slowest still-needed column and required reduction
+      const double scale = fmax(fmax(fabs(s.theta[0]), fabs(lo)), 1e-300);
       double xnorm = 0.0;
       for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
       xnorm = sqrt(xnorm);
-      double rho_need = 1.0, tmin = 1.0e300;
-      int islow = -1;
+      int last_bad = -1;             // last kept column still needing work
+      bool cert_bad = false;
+      double rho_k = 1.0;            // reduction still needed on the kept columns
       for (int i = 0; i < k; ++i) {
-        double ri = s.res[i];
-        if (!col_ok(i, ri, s.theta, r, b, scale, xnorm, need_cert)) {
-          double tol = (i < r) ? fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm) : PDSDP_TOL_CERT * scale;
-          rho_need = fmax(rho_need, ri / tol);
-          double t = (s.theta[i] - fc) / fe;
-          if (t < tmin) { tmin = t; islow = i; }
+        const double ri = s.res[i];
+        if (col_ok(i, ri, s.theta, r, b, scale, xnorm, need_cert)) continue;
+        if (i < r) {
+          last_bad = i;
+          rho_k = fmax(rho_k, ri / fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
+        } else {
+          cert_bad = true;
         }
       }
-      if (force_m >= 0) {
-        m = force_m;                      // retry after a breakdown
-      } else if (pass == 0 && !rerun && hint > 0) {
-        // new PDHG iteration: the stored residuals belong to the previous S;
-        // reuse the filter degree the previous iteration needed
-        m = hint < 2 ? 2 : (hint > PDSDP_MMAX ? PDSDP_MMAX : hint);
-      } else if (rho_need <= 1.0) {
-        m = 0;
-      } else {
-        double at = (tmin > 1.0 + 1e-6) ? acosh(tmin) : 0.0;
-        m = (at > 0.0) ? (int)ceil(acosh(rho_need) / at) + 1 : 8;
-        double t1 = (top - fc) / fe;
-        double spread = acosh(fmax(t1, 1.0 + 1e-6)) - ((tmin > 1.0 + 1e-6) ? acosh(tmin) : 0.0);
-        double eps_rel = fmin(fmax(maxres, 1e-16), 1.0);
-        if (spread > 1e-3) {
-          int mcap = (int)floor(log(1e4 / eps_rel) / spread);
-          if (mcap < 2) mcap = 2;
-          if (m > mcap) m = mcap;
-        }
-        if (m < 2) m = 2;
-        if (m > PDSDP_MMAX) m = PDSDP_MMAX;
+      // Chebyshev degree that reduces a column at t by rho against [lo, cut],
+      // capped so the amplification spread over the active columns stays
+      // below ~1e4/eps (beyond that CholQR of the filtered block breaks down)
+      auto plan = [&](int a0, int a1, double top, double cut, double slow, double rho, int& mm,
+                      double& e_, double& c_, double& s_) {
+        const double lo_ = fmin(lo, cut);
+        e_ = 0.5 * (cut - lo_);
+        c_ = 0.5 * (cut + lo_);
+        if (e_ < 1e-14 * scale) e_ = 1e-14 * scale;
+        if (top - c_ <= e_) top = c_ + 1.0001 * e_;
+        s_ = e_ / (top - c_);
+        const double ts = (slow - c_) / e_;
+        const double at = (ts > 1.0 + 1e-6) ? acosh(ts) : 0.0;
+        mm = (at > 0.0) ? (int)ceil(acosh(fmax(rho, 1.0)) / at) + 1 : 8;
+        const double tb = (s.theta[a1 - 1] - c_) / e_;
+        const double spread = acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? acosh(tb) : 0.0);
+        const double eps_rel = fmin(fmax(maxres, 1e-16), 1.0);
+        int mcap = PDSDP_MMAX;
+        if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(1e4 / eps_rel) / spread));
+        if (mcap < 2) mcap = 2;
+        return mcap;
+      };
+      int mcap = PDSDP_MMAX;
+      if (last_bad >= 0 || (pass == 0 && !rerun)) {
+        // kept columns: filter [0, a1) against the next Ritz value as the cut
+        int a1 = (last_bad >= 0) ? last_bad + 1 : r;
+        if (a1 > b - 1) a1 = b - 1;
+        if (a1 < 1) a1 = 1;
+        const double slow = s.theta[(last_bad >= 0) ? last_bad : a1 - 1];
+        double e1, c1, s1; int m1;
+        int cap1 = plan(0, a1, s.theta[0], s.theta[a1], slow, rho_k, m1, e1, c1, s1);
+        // all columns (guards filtered too) when that does not risk collapse
+        double e2, c2, s2; int m2;
+        int cap2 = plan(0, b, s.theta[0], s.theta[b - 1], slow, rho_k, m2, e2, c2, s2);
+        if (m2 <= cap2 && a1 < b) { m = m2; mcap = cap2; c0 = 0; bc = b; fe = e2; fc = c2; sig1 = s2; }
+        else { m = m1; mcap = cap1; c0 = 0; bc = a1; fe = e1; fc = c1; sig1 = s1; }
+      } else if (cert_bad) {
+        // kept pairs converged: lock them and filter the tail for lambda_{r+1}
+        nlock = r; c0 = r; bc = b - r;
+        const double rr = s.res[r] / fmax(PDSDP_TOL_CERT * scale, 1e-300);
+        mcap = plan(r, b, s.theta[r], s.theta[b - 1], s.theta[r], rr, m, fe, fc, sig1);
       }
+      if (force_m >= 0) m = force_m;                        // retry after a breakdown
+      else if (pass == 0 && !rerun && hint > 0) m = hint;   // new PDHG iteration: reuse last degree
+      if (m > mcap) m = mcap;
+      if (m > PDSDP_MMAX) m = PDSDP_MMAX;
+      if (last_bad < 0 && !cert_bad && !(pass == 0 && !rerun)) m = 0;
       if (x.c == 0 && tid == 0 && pass < 32) {
         double* g = st->dbg[pass];
-        g[0] = m; g[1] = maxres; g[2] = islow; g[3] = islow >= 0 ? s.theta[islow] : 0.0;
-        g[4] = tmin; g[5] = lo; g[6] = cut; g[7] = xnorm;
+        g[0] = m; g[1] = maxres; g[2] = last_bad; g[3] = c0; g[4] = bc; g[5] = lo; g[6] = fc - fe;
+        g[7] = xnorm;
       }
     }
     force_m = -1;
-    // ---- Chebyshev filter  Y_m = p_m(S) V ----
+    // ---- Chebyshev filter on the active columns:  Y_m = p_m(S_d) V ----
     int iy = 0;                       // buffer index holding Y_j (0 == V)
     int iyp = -1;                     // buffer holding Y_{j-1}
     int fre[3], nf = 0;
@@ -344,29 +383,33 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         if (j == 1) {
           const double ca = sig1 / fe, cb = -fc * sig1 / fe;
           if (av_valid) {
-            for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
-              const size_t o = (size_t)(x.r0 + it / b) * ld + it % b;
+            for (int it = tid; it < (x.r1 - x.r0) * bc; it += blockDim.x) {
+              const size_t o = (size_t)(x.r0 + it / bc) * ld + c0 + it % bc;
               buf[io][o] = fma(ca, buf[iav][o], cb * d.V[o]);
             }
           } else {
-            gram_partial(d.F, rF, d.V, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
-            cluster_reduce(d, x, rF * b, 0, s.T);
-            scale_T(s, rF, b);
-            apply_rows(d, x, s, zv, d.V, nullptr, buf[io], b, rF, ca, cb, 0.0);
+            operator_step(d, x, s, zv, d.V, nullptr, buf[io], c0, bc, rF, nlock, ca, cb, 0.0);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          gram_partial(d.F, rF, buf[iy], b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
-          cluster_reduce(d, x, rF * b, 0, s.T);
-          scale_T(s, rF, b);
-          apply_rows(d, x, s, zv, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], b, rF, ca, cb, cd);
+          operator_step(d, x, s, zv, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], c0, bc, rF, nlock, ca, cb, cd);
           ++matvecs;
           sg = sn;
         }
         iyp = iy;
         iy = io;
+        __syncthreads();
+      }
+      // passive columns ride along unfiltered
+      if (bc < b) {
+        for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
+          const int jj = it % b;
+          if (jj >= c0 && jj < c0 + bc) continue;
+          const size_t o = (size_t)(x.r0 + it / b) * ld + jj;
+          buf[iy][o] = d.V[o];
+        }
         __syncthreads();
       }
     }
@@ -390,8 +433,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       x.par ^= 1;
       __syncthreads();
     }
-    scale_T(s, rF, b);
-    apply_rows(d, x, s, zv, buf[iy], nullptr, buf[iw], b, rF, 1.0, 0.0, 0.0);
+    scale_T(s, rF, 0, b);
+    apply_rows(d, x, s, zv, buf[iy], nullptr, buf[iw], 0, b, rF, 0, 1.0, 0.0, 0.0);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
     bool okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
@@ -435,7 +478,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       force_m = m / 2;
       continue;
     }
-    msucc += m;
+    if (nlock == 0) msucc += m;
     tri_inv_lower(s.A, s.L, b, lds);            // L = L2^-1
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
@@ -496,7 +539,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       prev_maxres = maxres;
     }
   }
-  for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) s.lamN[i] = (i < r && i < b) ? fmax(s.theta[i], 0.0) : 0.0;
+  for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) s.lamN[i] = (i < r && i < b && s.theta[i] > 0.0) ? s.theta[i] : 0.0;
   __syncthreads();
 
   // ---------------- dual step: y+ = u - alpha proj_box(u/alpha) ----------------
@@ -518,8 +561,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const double* Vp = d.V + (size_t)p * ld; const double* Vq = d.V + (size_t)q * ld;
           const double* Fp = d.F + (size_t)p * ld; const double* Fq = d.F + (size_t)q * ld;
           double xn = 0.0, xo = 0.0;
-          for (int l = 0; l < rN; ++l) xn = fma(Vp[l] * s.lamN[l], Vq[l], xn);
-          for (int l = 0; l < rF; ++l) xo = fma(Fp[l] * s.lamF[l], Fq[l], xo);
+          for (int l = 0; l < rN; ++l) if (s.lamN[l] != 0.0) xn = fma(Vp[l] * s.lamN[l], Vq[l], xn);
+          for (int l = 0; l < rF; ++l) if (s.lamF[l] != 0.0) xo = fma(Fp[l] * s.lamF[l], Fq[l], xo);
           const double g = d.ag[e];
           s2 = fma(g, 2.0 * xn - xo, s2);
           sd = fma(g, xn - xo, sd);
@@ -562,7 +605,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   cluster_reduce(d, x, 1, 1, s.red1);
   const double ed2_tot = s.red1[0];
   double fin_tot = -s.red1[1];
-  for (int i = 0; i < b; ++i) if (!isfinite(s.theta[i])) fin_tot = 0.0;
+  for (int i = 0; i < rN; ++i) if (s.theta[i] > 0.0 && !isfinite(s.theta[i])) fin_tot = 0.0;
 
   // ---------------- adjoint gather: Z_{k+1} = C + M^T y+, support correction ----------------
   double corr = 0.0;
@@ -582,8 +625,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         const double* Vi = d.V + (size_t)i * ld; const double* Vj = d.V + (size_t)j * ld;
         const double* Fi = d.F + (size_t)i * ld; const double* Fj = d.F + (size_t)j * ld;
         double xn = 0.0, xo = 0.0;
-        for (int l = 0; l < rN; ++l) xn = fma(Vi[l] * s.lamN[l], Vj[l], xn);
-        for (int l = 0; l < rF; ++l) xo = fma(Fi[l] * s.lamF[l], Fj[l], xo);
+        for (int l = 0; l < rN; ++l) if (s.lamN[l] != 0.0) xn = fma(Vi[l] * s.lamN[l], Vj[l], xn);
+        for (int l = 0; l < rF; ++l) if (s.lamF[l] != 0.0) xo = fma(Fi[l] * s.lamF[l], Fj[l], xo);
         const double v = (xn - xo) / alpha;
         const double w = (i == j) ? 1.0 : 2.0;
         corr = fma(w * a, a - 2.0 * v, corr);

@@ -55,12 +55,16 @@ residual_kernel(const Inst* __restrict__ insts, const int* __restrict__ active) 
     const int gi = I * RES_TILE + row, gj = J * RES_TILE + row;
     double a = 0.0, bb = 0.0;
     if (l < rN) {
-      if (gi < n) a = d.V[(size_t)gi * ld + l] * (st->lamN[l] * ia);
-      if (gj < n) bb = d.V[(size_t)gj * ld + l];
+      if (st->lamN[l] != 0.0) {
+        if (gi < n) a = d.V[(size_t)gi * ld + l] * (st->lamN[l] * ia);
+        if (gj < n) bb = d.V[(size_t)gj * ld + l];
+      }
     } else if (l < K) {
       const int q = l - rN;
-      if (gi < n) a = -d.F[(size_t)gi * ld + q] * (st->lamF[q] * ia);
-      if (gj < n) bb = d.F[(size_t)gj * ld + q];
+      if (st->lamF[q] != 0.0) {
+        if (gi < n) a = -d.F[(size_t)gi * ld + q] * (st->lamF[q] * ia);
+        if (gj < n) bb = d.F[(size_t)gj * ld + q];
+      }
     }
     GI[row * lda + l] = a;
     GJ[row * lda + l] = bb;
@@ -148,7 +152,7 @@ __global__ void objective_kernel(const Inst* __restrict__ insts, const int* __re
     const double* Ui = U + (size_t)d.zrow[e] * ld;
     const double* Uj = U + (size_t)d.zcol[e] * ld;
     double xv = 0.0;
-    for (int l = 0; l < r; ++l) xv = fma(Ui[l] * lam[l], Uj[l], xv);
+    for (int l = 0; l < r; ++l) if (lam[l] != 0.0) xv = fma(Ui[l] * lam[l], Uj[l], xv);
     s = fma(c, xv, s);
   }
   s = warp_sum(s);
@@ -197,7 +201,7 @@ __global__ void pack_kernel(const Inst* __restrict__ insts, int inst, int which,
     const double* Ui = U + (size_t)i * ld;
     const double* Uj = U + (size_t)j * ld;
     double xv = 0.0;
-    for (int l = 0; l < r; ++l) xv = fma(Ui[l] * lam[l], Uj[l], xv);
+    for (int l = 0; l < r; ++l) if (lam[l] != 0.0) xv = fma(Ui[l] * lam[l], Uj[l], xv);
     out[pos] = (i == j) ? xv : xv * 1.4142135623730951;
   }
 }

@@ -23,9 +23,11 @@ ITER_TOL = 1e-8      # relative Frobenius, fixed K
 OBJ_TOL = 1e-5       # relative objective
 
 
-def rel(a, b):
+def rel(a, b, floor=1e-12):
+    """Relative error; references that are zero up to rounding (e.g. X+ = 0
+    when S is negative semidefinite) are compared absolutely against `floor`."""
     nb = np.linalg.norm(b)
-    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(nb, floor)
 
 
 def with_iters(cfg, K, **kw):

@@ -21,7 +21,8 @@ for k in range(1, K + 1):
         d = b.debug(0)
         npass = int(o[4])
         print(f"k={k} eps=({o[0]:.4e},{o[1]:.4e}) lam={o[2]:.4e} passes={npass} matvecs={int(o[5])} conv={int(o[6])} blk={int(o[11])}")
-        for p in range(min(npass, 32)):
+        for p in range(32):
+            if not d["passes"][p].any(): break
             print("    pass", p, d["passes"][p])
         bb = int(o[11])
         print("    theta", d["theta"][:bb]); print("    res", d["res"][:bb])
