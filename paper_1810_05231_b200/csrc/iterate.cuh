@@ -31,7 +31,7 @@ namespace pdsdp {
 // Is Ritz pair i accurate enough?  i < r: kept in X+ (clipped at 0);
 // i == r: the certificate eigenvalue lambda_{r+1} (only its value matters).
 __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, int r, int b,
-                                       double scale, double xnorm, bool need_cert) {
+                                       double scale, double xnorm, double cert_tol) {
   const double th = theta[i];
   if (!(ri == ri) || !(th == th)) return true;          // non-finite: give up, reported as such
   if (th + ri < 0.0) return true;                       // certainly clipped / certificate passes
@@ -43,7 +43,7 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
     const double impact = ri + 2.0 * fmax(th, 0.0) * fmin(1.0, ri / fmax(gap, 1e-300));
     return impact <= PDSDP_TOL_X * xnorm;
   }
-  return !need_cert || ri <= PDSDP_TOL_CERT * scale;
+  return cert_tol <= 0.0 || ri <= cert_tol * scale;
 }
 
 struct Sm {
@@ -202,6 +202,66 @@ __device__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* 
   apply_rows(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
 }
 
+// Convergence state of the Ritz block (identical in every thread).
+struct Assess {
+  int last_bad;     // last kept column (< r) still needing work, -1 if none
+  bool cert_bad;    // lambda_{r+1} requested and not yet accurate
+  bool tail_bad;    // lambda_{r+1} not clearly separated from the kept pairs
+  double rho_k;     // residual reduction still needed on the kept columns
+  double maxres;    // worst relative residual among columns needing work
+};
+
+__device__ Assess assess(const double* theta, const double* res, int r, int b, int k, double scale,
+                         double xnorm, double cert_tol) {
+  Assess a{-1, false, false, 1.0, 0.0};
+  for (int i = 0; i < k; ++i) {
+    const double ri = res[i];
+    if (col_ok(i, ri, theta, r, b, scale, xnorm, cert_tol)) continue;
+    a.maxres = fmax(a.maxres, ri / scale);
+    if (i < r) {
+      a.last_bad = i;
+      a.rho_k = fmax(a.rho_k, ri / fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
+    } else {
+      a.cert_bad = true;
+    }
+  }
+  // The kept set must be the true top r: the first excluded Ritz pair has to
+  // be either clearly below the last kept one or itself converged.
+  if (r < b && r < k + 1 && r >= 1) {
+    const double lo_k = theta[r - 1] - 2.0 * res[r - 1];
+    const double hi_t = theta[r] + 2.0 * res[r];
+    if (!(hi_t < lo_k) && res[r] > PDSDP_TOL_CERT * scale && !(theta[r] + res[r] < 0.0)) {
+      a.tail_bad = true;
+      a.maxres = fmax(a.maxres, res[r] / scale);
+    }
+  }
+  return a;
+}
+
+// Chebyshev filter for columns [a0, a1): damp [lo, cut], scale at `top`;
+// degree to reduce a column at `slow` by `rho`, and a cap keeping the
+// amplification spread across the active columns below ~1e4/eps_rel
+// (beyond that the filtered block loses rank and CholQR breaks down).
+__device__ int cheb_plan(const double* theta, int a1, double lo, double top, double cut, double slow,
+                         double rho, double scale, double eps_rel, int& mm, double& e_, double& c_,
+                         double& s_) {
+  const double lo_ = fmin(lo, cut);
+  e_ = 0.5 * (cut - lo_);
+  c_ = 0.5 * (cut + lo_);
+  if (e_ < 1e-14 * scale) e_ = 1e-14 * scale;
+  if (top - c_ <= e_) top = c_ + 1.0001 * e_;
+  s_ = e_ / (top - c_);
+  const double ts = (slow - c_) / e_;
+  const double at = (ts > 1.0 + 1e-6) ? acosh(ts) : 0.0;
+  mm = (at > 0.0) ? (int)ceil(acosh(fmax(rho, 1.0)) / at) + 1 : 8;
+  const double tb = (theta[a1 - 1] - c_) / e_;
+  const double spread = acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? acosh(tb) : 0.0);
+  int mcap = PDSDP_MMAX;
+  if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(1e4 / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
+  if (mcap < 2) mcap = 2;
+  return mcap;
+}
+
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
 inline size_t iterate_smem_bytes(int lds) {
   return (size_t)(5 * lds * lds + PDSDP_NTHR + 11 * PDSDP_BMAX) * sizeof(double) +
@@ -258,6 +318,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   const int r = ctl.r;
   const int k = (r + 1 < n) ? r + 1 : n;
   const bool need_cert = (ctl.flags & 2) != 0;
+  // bit3: certificate eigenpair to the kept-pair tolerance (op-level aproj_psd)
+  const double cert_tol = need_cert ? ((ctl.flags & 8) ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) : 0.0;
   const bool rerun = (ctl.flags & 4) != 0;
   const bool cold = !rerun && ((ctl.flags & 1) || st->b == 0);
   const int rF = cold ? 0 : (rerun ? st->rF_used : st->rF);
@@ -304,66 +366,35 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       double xnorm = 0.0;
       for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
       xnorm = sqrt(xnorm);
-      int last_bad = -1;             // last kept column still needing work
-      bool cert_bad = false;
-      double rho_k = 1.0;            // reduction still needed on the kept columns
-      for (int i = 0; i < k; ++i) {
-        const double ri = s.res[i];
-        if (col_ok(i, ri, s.theta, r, b, scale, xnorm, need_cert)) continue;
-        if (i < r) {
-          last_bad = i;
-          rho_k = fmax(rho_k, ri / fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
-        } else {
-          cert_bad = true;
-        }
-      }
-      // Chebyshev degree that reduces a column at t by rho against [lo, cut],
-      // capped so the amplification spread over the active columns stays
-      // below ~1e4/eps (beyond that CholQR of the filtered block breaks down)
-      auto plan = [&](int a0, int a1, double top, double cut, double slow, double rho, int& mm,
-                      double& e_, double& c_, double& s_) {
-        const double lo_ = fmin(lo, cut);
-        e_ = 0.5 * (cut - lo_);
-        c_ = 0.5 * (cut + lo_);
-        if (e_ < 1e-14 * scale) e_ = 1e-14 * scale;
-        if (top - c_ <= e_) top = c_ + 1.0001 * e_;
-        s_ = e_ / (top - c_);
-        const double ts = (slow - c_) / e_;
-        const double at = (ts > 1.0 + 1e-6) ? acosh(ts) : 0.0;
-        mm = (at > 0.0) ? (int)ceil(acosh(fmax(rho, 1.0)) / at) + 1 : 8;
-        const double tb = (s.theta[a1 - 1] - c_) / e_;
-        const double spread = acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? acosh(tb) : 0.0);
-        const double eps_rel = fmin(fmax(maxres, 1e-16), 1.0);
-        int mcap = PDSDP_MMAX;
-        if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(1e4 / eps_rel) / spread));
-        if (mcap < 2) mcap = 2;
-        return mcap;
-      };
+      const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
+      const bool stale = (pass == 0 && !rerun);   // residuals belong to the previous S
+      const double eps_rel = fmax(as.maxres, stale ? 1e-3 : 0.0);
       int mcap = PDSDP_MMAX;
-      if (last_bad >= 0 || (pass == 0 && !rerun)) {
-        // kept columns: filter [0, a1) against the next Ritz value as the cut
-        int a1 = (last_bad >= 0) ? last_bad + 1 : r;
+      if (as.last_bad >= 0 || stale) {
+        // kept columns; guards filtered too unless that would collapse the block
+        int a1 = (as.last_bad >= 0) ? as.last_bad + 1 : r;
         if (a1 > b - 1) a1 = b - 1;
         if (a1 < 1) a1 = 1;
-        const double slow = s.theta[(last_bad >= 0) ? last_bad : a1 - 1];
-        double e1, c1, s1; int m1;
-        int cap1 = plan(0, a1, s.theta[0], s.theta[a1], slow, rho_k, m1, e1, c1, s1);
-        // all columns (guards filtered too) when that does not risk collapse
-        double e2, c2, s2; int m2;
-        int cap2 = plan(0, b, s.theta[0], s.theta[b - 1], slow, rho_k, m2, e2, c2, s2);
-        if (m2 <= cap2 && a1 < b) { m = m2; mcap = cap2; c0 = 0; bc = b; fe = e2; fc = c2; sig1 = s2; }
-        else { m = m1; mcap = cap1; c0 = 0; bc = a1; fe = e1; fc = c1; sig1 = s1; }
-      } else if (cert_bad) {
-        // kept pairs converged: lock them and filter the tail for lambda_{r+1}
+        const double slow = s.theta[(as.last_bad >= 0) ? as.last_bad : a1 - 1];
+        double e1, c1, s1, e2, c2, s2;
+        int m1, m2;
+        const int cap1 = cheb_plan(s.theta, a1, lo, s.theta[0], s.theta[a1], slow, as.rho_k, scale, eps_rel, m1, e1, c1, s1);
+        const int cap2 = cheb_plan(s.theta, b, lo, s.theta[0], s.theta[b - 1], slow, as.rho_k, scale, eps_rel, m2, e2, c2, s2);
+        int want2 = stale ? (hint > 0 ? hint : 4) : m2;
+        int want1 = stale ? (hint > 0 ? hint : 4) : m1;
+        if (cap2 >= min(want2, 6)) { m = min(want2, cap2); mcap = cap2; c0 = 0; bc = b; fe = e2; fc = c2; sig1 = s2; }
+        else { m = min(want1, cap1); mcap = cap1; c0 = 0; bc = a1; fe = e1; fc = c1; sig1 = s1; }
+      } else if (as.cert_bad || as.tail_bad) {
+        // kept pairs converged: lock (deflate) them and filter the tail
         nlock = r; c0 = r; bc = b - r;
-        const double rr = s.res[r] / fmax(PDSDP_TOL_CERT * scale, 1e-300);
-        mcap = plan(r, b, s.theta[r], s.theta[b - 1], s.theta[r], rr, m, fe, fc, sig1);
+        const double rr = s.res[r] / fmax(fmax(cert_tol, PDSDP_TOL_CERT * 1e-4) * scale, 1e-300);
+        mcap = cheb_plan(s.theta, b, lo, s.theta[r], s.theta[b - 1], s.theta[r], rr, scale, eps_rel, m, fe, fc, sig1);
+        if (m > mcap) m = mcap;
       }
       if (force_m >= 0) m = force_m;                        // retry after a breakdown
-      else if (pass == 0 && !rerun && hint > 0) m = hint;   // new PDHG iteration: reuse last degree
       if (m > mcap) m = mcap;
       if (m > PDSDP_MMAX) m = PDSDP_MMAX;
-      if (last_bad < 0 && !cert_bad && !(pass == 0 && !rerun)) m = 0;
+      const int last_bad = as.last_bad;
       if (x.c == 0 && tid == 0 && pass < 32) {
         double* g = st->dbg[pass];
         g[0] = m; g[1] = maxres; g[2] = last_bad; g[3] = c0; g[4] = bc; g[5] = lo; g[6] = fc - fe;
@@ -525,15 +556,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       double xnorm = 0.0;
       for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
       xnorm = sqrt(xnorm);
-      bool ok_all = true;
-      maxres = 0.0;
-      for (int i = 0; i < b; ++i) {
-        double ri = sqrt(fmax(s.red1[i], 0.0));
-        if (tid == 0) s.res[i] = ri;
-        if (i < k && !col_ok(i, ri, s.theta, r, b, scale, xnorm, need_cert)) { ok_all = false; maxres = fmax(maxres, ri / scale); }
-      }
+      for (int i = tid; i < b; i += blockDim.x) s.res[i] = sqrt(fmax(s.red1[i], 0.0));
       __syncthreads();
-      if (ok_all) { converged = 1; break; }
+      const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
+      maxres = as.maxres;
+      if (as.last_bad < 0 && !as.cert_bad && !as.tail_bad) { converged = 1; break; }
       // stagnation at the rounding floor
       if (pass >= 2 && maxres > 0.5 * prev_maxres && maxres < 1e-10) { converged = 2; break; }
       prev_maxres = maxres;

@@ -731,7 +731,7 @@ int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_pack
   pdsdp_batch* b = nullptr;
   int rc = pdsdp_batch_create(1, &pr, &b);
   if (rc) return rc;
-  int32_t inst = 0, rr = r, yp = 0, fl = 1 | 2;
+  int32_t inst = 0, rr = r, yp = 0, fl = 1 | 2 | 8;
   double out[PDSDP_OUT_LEN];
   rc = pdsdp_set_alpha(b, 0, 1.0);
   if (!rc) rc = pdsdp_reset(b, 0, 0.0);

@@ -144,8 +144,8 @@ def test_large_configs_fixed_K_sketches(idx, fname):
         res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, int(K)))
         Xd = res.X.to_dense()
         assert rel(res.y, d[f"y{K}"]) <= ITER_TOL
-        assert rel(Xd @ z, d[f"Xz{K}"]) <= ITER_TOL
-        assert rel(np.diag(Xd), d[f"diag{K}"]) <= ITER_TOL
+        assert rel(Xd @ z, d[f"Xz{K}"], floor=1e-4) <= ITER_TOL
+        assert rel(np.diag(Xd), d[f"diag{K}"], floor=1e-4) <= ITER_TOL
         assert np.linalg.norm(Xd) == pytest.approx(float(d[f"fro{K}"]), rel=ITER_TOL)
         assert res.primal_objective == pytest.approx(float(d[f"pobj{K}"]), rel=OBJ_TOL, abs=1e-9)
         np.testing.assert_allclose(res.final_residuals, d[f"res{K}"], rtol=1e-7)
@@ -189,7 +189,8 @@ def test_oversized_steps_follow_reference():
         assert res.status.value == ref.status
         assert res.iterations == ref.iterations
         if np.all(np.isfinite(ref.y)):
-            assert rel(res.y, ref.y) <= ITER_TOL
+            scale = max(np.abs(ref.y).max(), 1e-300)
+            assert np.abs(res.y - ref.y).max() <= ITER_TOL * scale
 
 
 def test_full_rank_and_tiny_problems():
