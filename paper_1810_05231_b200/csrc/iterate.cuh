@@ -26,6 +26,7 @@ namespace pdsdp {
 #define PDSDP_TOL_KEEP 1e-12   // ARPACK's tol in the reference (symmat.py:33), relative to the spectral scale
 #define PDSDP_TOL_X 1e-12      // admissible per-iteration error of X+ (relative to ||X+||_F)
 #define PDSDP_TOL_CERT 1e-8
+#define PDSDP_TOL_CLIP 1e-6
 #define PDSDP_MMAX 24
 
 // Is Ritz pair i accurate enough?  i < r: kept in X+ (clipped at 0);
@@ -34,7 +35,10 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
                                        double scale, double xnorm, double cert_tol) {
   const double th = theta[i];
   if (!(ri == ri) || !(th == th)) return true;          // non-finite: give up, reported as such
-  if (th + ri < 0.0) return true;                       // certainly clipped / certificate passes
+  // clipped / certificate passes -- only trusted once the pair is nearly
+  // invariant (a Ritz value of an unconverged block can sit far below the
+  // eigenvalue it will converge to)
+  if (th + ri < 0.0 && ri <= PDSDP_TOL_CLIP * scale) return true;
   if (i < r) {
     if (ri <= PDSDP_TOL_KEEP * scale) return true;
     // remaining effect on X+: |dtheta| <= ri plus rotation ~ 2 theta ri / gap (Davis-Kahan)
@@ -230,7 +234,8 @@ __device__ Assess assess(const double* theta, const double* res, int r, int b, i
   if (r < b && r < k + 1 && r >= 1) {
     const double lo_k = theta[r - 1] - 2.0 * res[r - 1];
     const double hi_t = theta[r] + 2.0 * res[r];
-    if (!(hi_t < lo_k) && res[r] > PDSDP_TOL_CERT * scale && !(theta[r] + res[r] < 0.0)) {
+    if (!(hi_t < lo_k) && res[r] > PDSDP_TOL_CERT * scale &&
+        !(theta[r] + res[r] < 0.0 && res[r] <= PDSDP_TOL_CLIP * scale)) {
       a.tail_bad = true;
       a.maxres = fmax(a.maxres, res[r] / scale);
     }
@@ -370,7 +375,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const bool stale = (pass == 0 && !rerun);   // residuals belong to the previous S
       const double eps_rel = fmax(as.maxres, stale ? 1e-3 : 0.0);
       int mcap = PDSDP_MMAX;
-      if (as.last_bad >= 0 || stale) {
+      if (as.last_bad >= 0 || stale || (!as.cert_bad && !as.tail_bad)) {
         // kept columns; guards filtered too unless that would collapse the block
         int a1 = (as.last_bad >= 0) ? as.last_bad + 1 : r;
         if (a1 > b - 1) a1 = b - 1;
@@ -380,8 +385,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         int m1, m2;
         const int cap1 = cheb_plan(s.theta, a1, lo, s.theta[0], s.theta[a1], slow, as.rho_k, scale, eps_rel, m1, e1, c1, s1);
         const int cap2 = cheb_plan(s.theta, b, lo, s.theta[0], s.theta[b - 1], slow, as.rho_k, scale, eps_rel, m2, e2, c2, s2);
-        int want2 = stale ? (hint > 0 ? hint : 4) : m2;
-        int want1 = stale ? (hint > 0 ? hint : 4) : m1;
+        int want2 = stale ? (hint > 0 ? hint : 4) : max(m2, 2);
+        int want1 = stale ? (hint > 0 ? hint : 4) : max(m1, 2);
         if (cap2 >= min(want2, 6)) { m = min(want2, cap2); mcap = cap2; c0 = 0; bc = b; fe = e2; fc = c2; sig1 = s2; }
         else { m = min(want1, cap1); mcap = cap1; c0 = 0; bc = a1; fe = e1; fc = c1; sig1 = s1; }
       } else if (as.cert_bad || as.tail_bad) {
@@ -560,7 +565,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
       const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
       maxres = as.maxres;
-      if (as.last_bad < 0 && !as.cert_bad && !as.tail_bad) { converged = 1; break; }
+      // a block that was not filtered in this pass (cold RR) is not trusted
+      if (as.last_bad < 0 && !as.cert_bad && !as.tail_bad && (m > 0 || b >= n)) { converged = 1; break; }
       // stagnation at the rounding floor
       if (pass >= 2 && maxres > 0.5 * prev_maxres && maxres < 1e-10) { converged = 2; break; }
       prev_maxres = maxres;
