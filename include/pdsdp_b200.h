@@ -115,8 +115,10 @@ int pdsdp_kernel_times(pdsdp_batch* b, double* out /* [4] */);
 
 /* Eigensolver diagnostics of the last iteration of one instance:
  * out[0..256) per pass (m, worst rel residual, slow column, theta, t, lo, cut, ||X+||),
- * out[256..320) Ritz values, out[320..384) Ritz residual norms. */
-int pdsdp_debug(pdsdp_batch* b, int inst, double* out /* [384] */);
+ * out[256..320) Ritz values, out[320..384) Ritz residual norms,
+ * out[384..400) SM cycles per kernel phase (CTA 0), out[400..4504) the last
+ * projected Rayleigh-Ritz matrix when flag bit 4 was set (b x b, b at 4496). */
+int pdsdp_debug(pdsdp_batch* b, int inst, double* out /* [4504] */);
 
 const char* pdsdp_strerror(int code);
 const char* pdsdp_last_error(void);

@@ -42,7 +42,24 @@ struct State {
   double seed;
   double mhint;     // total filter degree used by the previous iteration
   double dbg[32][8];  // per pass: m, worst rel residual, slow column, theta, t, lo, cut, xnorm
+  double prof[16];    // SM cycles of CTA 0 per phase in the last launch
+  double hdump[PDSDP_BMAX * PDSDP_BMAX + 8];  // diagnostic: last projected matrix H' (flag bit4)
 };
+
+// thread-0 phase timer (clock64 deltas; diagnostic only)
+struct Prof {
+  long long last;
+  long long acc[16];
+  int cur;
+};
+__device__ __forceinline__ void prof_mark(Prof& p, int phase) {
+  if (threadIdx.x == 0) {
+    const long long now = clock64();
+    p.acc[p.cur] += now - p.last;
+    p.last = now;
+    p.cur = phase;
+  }
+}
 
 // Per-instance descriptor (device resident).  Sizes and pointers only.
 struct Inst {

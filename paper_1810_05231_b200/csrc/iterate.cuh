@@ -52,6 +52,12 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
 
 struct Sm {
   double *A, *Q, *L, *M, *T;   // lds x lds each
+  double *gsc;                 // PDSDP_GRAM_SCR
+  double* ys;                  // staged operand block (n x ycw)
+  int ycw;                     // staged column chunk width (even; 0 = gather path)
+  const int* zc;               // staged Z columns of own rows
+  const double* zvs;           // staged Z values of own rows
+  int zoff, zstaged;
   double *scr;                 // NTHR
   double *theta, *res, *lamF, *lamN, *dsc, *cs, *red1;  // BMAX each (red1: 2*BMAX)
   int *perm, *pq, *flag;
@@ -66,44 +72,62 @@ __device__ __forceinline__ double* red_slot(const Inst& d, const Cta& x, int cc)
   return d.red + ((size_t)x.par * x.C + cc) * PDSDP_RED_MAX;
 }
 
+// Sum of element i over the C partials of the current reduction slot; the C
+// loads are issued together (one L2 round trip) and added in rank order.
+__device__ __forceinline__ double cluster_sum(const Inst& d, const Cta& x, int i, bool is_max) {
+  double v[16];
+#pragma unroll
+  for (int cc = 0; cc < 16; ++cc) v[cc] = (cc < x.C) ? __ldcg(red_slot(d, x, cc) + i) : 0.0;
+  double s = is_max ? -1.0e308 : 0.0;
+#pragma unroll
+  for (int cc = 0; cc < 16; ++cc)
+    if (cc < x.C) s = is_max ? fmax(s, v[cc]) : s + v[cc];
+  return s;
+}
+
 // Finish a cluster reduction whose per-CTA partial (q_sum sums followed by
 // q_max maxima) is already in red_slot(x, x.c).  Result -> dst (smem).
 __device__ void cluster_reduce(const Inst& d, Cta& x, int q_sum, int q_max, double* dst) {
   cg::this_cluster().sync();
   const int q = q_sum + q_max;
-  for (int i = threadIdx.x; i < q; i += blockDim.x) {
-    double s = (i < q_sum) ? 0.0 : -1.0e308;
-    for (int cc = 0; cc < x.C; ++cc) {
-      double v = red_slot(d, x, cc)[i];
-      s = (i < q_sum) ? s + v : fmax(s, v);
-    }
-    dst[i] = s;
-  }
+  for (int i = threadIdx.x; i < q; i += blockDim.x) dst[i] = cluster_sum(d, x, i, i >= q_sum);
   x.par ^= 1;
   __syncthreads();
 }
 
-// partial[o] = sum over own rows of A[rho, i] * B[rho, j], o = off + i*nb + j.
+// partial[o] = sum over own rows of A[rho, i] * B[rho, j], o = i*nb + j.
 // Written to the global reduction slot (deterministic, one finisher per o).
+// Each thread owns one output and one contiguous row chunk; rows are read
+// four at a time so that eight independent loads are in flight.
 __device__ void gram_partial(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
                              int ld, int r0, int r1, double* gout, double* scr) {
   const int q = na * nb;
   const int tid = threadIdx.x, nt = blockDim.x;
   if (q == 0) return;
-  if (q >= nt / 2) {
-    for (int o = tid; o < q; o += nt) {
-      const int i = o / nb, j = o % nb;
-      double s = 0.0;
-      for (int rho = r0; rho < r1; ++rho) s = fma(A[(size_t)rho * ld + i], B[(size_t)rho * ld + j], s);
-      gout[o] = s;
+  auto dot = [&](int i, int j, int ra, int rb) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int rho = ra;
+    for (; rho + 4 <= rb; rho += 4) {
+      const double a0 = A[(size_t)rho * ld + i], a1 = A[(size_t)(rho + 1) * ld + i];
+      const double a2 = A[(size_t)(rho + 2) * ld + i], a3 = A[(size_t)(rho + 3) * ld + i];
+      const double b0 = B[(size_t)rho * ld + j], b1 = B[(size_t)(rho + 1) * ld + j];
+      const double b2 = B[(size_t)(rho + 2) * ld + j], b3 = B[(size_t)(rho + 3) * ld + j];
+      s0 = fma(a0, b0, s0); s1 = fma(a1, b1, s1); s2 = fma(a2, b2, s2); s3 = fma(a3, b3, s3);
     }
+    for (; rho < rb; ++rho) s0 = fma(A[(size_t)rho * ld + i], B[(size_t)rho * ld + j], s0);
+    return (s0 + s1) + (s2 + s3);
+  };
+  if (q >= nt / 2) {
+    for (int o = tid; o < q; o += nt) gout[o] = dot(o / nb, o % nb, r0, r1);
   } else {
     const int S = nt / q;
     const int o = tid % q, sl = tid / q;
     double s = 0.0;
     if (sl < S) {
-      const int i = o / nb, j = o % nb;
-      for (int rho = r0 + sl; rho < r1; rho += S) s = fma(A[(size_t)rho * ld + i], B[(size_t)rho * ld + j], s);
+      const int len = (r1 - r0 + S - 1) / S;
+      const int ra = r0 + sl * len;
+      const int rb = min(r1, ra + len);
+      if (ra < rb) s = dot(o / nb, o % nb, ra, rb);
     }
     scr[tid] = s;
     __syncthreads();
@@ -116,6 +140,72 @@ __device__ void gram_partial(const double* __restrict__ A, int na, const double*
   }
 }
 
+#define PDSDP_GRAM_SCR 4096     // doubles of smem for the cross-warp Gram reduction
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// gout[i*nb + j] = sum over own rows rho of A[rho, i] * B[rho, j]  (i < na, j < nb)
+// on FP64 tensor cores: warps take (tile group, row chunk) work items, each
+// accumulating up to four 8x8 DMMA tiles over its rows (k = 4 rows per
+// mma.m8n8k4); chunks are then added in a fixed order through shared memory.
+__device__ void gram_mma(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
+                         int ld, int r0, int r1, double* gout, double* wsm) {
+  const int q = na * nb;
+  if (q == 0) return;
+  const int mt = (na + 7) >> 3, ntl = (nb + 7) >> 3, tiles = mt * ntl;
+  const int NG = (tiles + 3) >> 2;
+  const int nw = blockDim.x >> 5;
+  // partial tiles live in wsm (PDSDP_GRAM_SCR doubles = 16 work items of 4 tiles)
+  const int chunks = max(1, min(nw, PDSDP_GRAM_SCR / 256) / NG);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int nrows = r1 - r0;
+  const int clen = (((nrows + chunks - 1) / chunks) + 3) & ~3;
+  for (int wk = warp; wk < NG * chunks; wk += nw) {
+    const int grp = wk % NG, ch = wk / NG;
+    const int ra = r0 + ch * clen, rb = min(r1, ra + clen);
+    double acc[4][2];
+    int ti[4], tj[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      acc[t][0] = 0.0; acc[t][1] = 0.0;
+      const int tt = grp * 4 + t;
+      ti[t] = (tt < tiles) ? (tt / ntl) * 8 + g : 1 << 30;
+      tj[t] = (tt < tiles) ? (tt % ntl) * 8 + g : 1 << 30;
+    }
+    for (int rho0 = ra; rho0 < rb; rho0 += 4) {
+      const int rho = rho0 + tq;
+      const bool rv = rho < rb;
+      double av[4], bv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        av[t] = (rv && ti[t] < na) ? A[(size_t)rho * ld + ti[t]] : 0.0;
+        bv[t] = (rv && tj[t] < nb) ? B[(size_t)rho * ld + tj[t]] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) dmma884(acc[t][0], acc[t][1], av[t], bv[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      double* w = wsm + ((size_t)(ch * NG + grp) * 4 + t) * 64 + g * 8 + 2 * tq;
+      w[0] = acc[t][0];
+      w[1] = acc[t][1];
+    }
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < q; o += blockDim.x) {
+    const int i = o / nb, j = o % nb;
+    const int t = (i >> 3) * ntl + (j >> 3);
+    const int grp = t >> 2, slot = t & 3, el = (i & 7) * 8 + (j & 7);
+    double sum = 0.0;
+    for (int ch = 0; ch < chunks; ++ch) sum += wsm[((size_t)(ch * NG + grp) * 4 + slot) * 64 + el];
+    gout[o] = sum;
+  }
+  __syncthreads();
+}
+
 // column sums of squares of (P[:, j] - th[j] * Q[:, j]) over own rows
 __device__ void colres_partial(const double* __restrict__ P, const double* __restrict__ Qm,
                                const double* th, int b, int ld, int r0, int r1, double* gout, double* scr) {
@@ -125,10 +215,21 @@ __device__ void colres_partial(const double* __restrict__ P, const double* __res
   double s = 0.0;
   if (sl < S) {
     const double t = th[j];
-    for (int rho = r0 + sl; rho < r1; rho += S) {
-      double v = P[(size_t)rho * ld + j] - t * Qm[(size_t)rho * ld + j];
+    const int len = (r1 - r0 + S - 1) / S;
+    const int ra = r0 + sl * len, rb = min(r1, ra + len);
+    double s1 = 0.0;
+    int rho = ra;
+    for (; rho + 2 <= rb; rho += 2) {
+      const double v0 = P[(size_t)rho * ld + j] - t * Qm[(size_t)rho * ld + j];
+      const double v1 = P[(size_t)(rho + 1) * ld + j] - t * Qm[(size_t)(rho + 1) * ld + j];
+      s = fma(v0, v0, s);
+      s1 = fma(v1, v1, s1);
+    }
+    for (; rho < rb; ++rho) {
+      const double v = P[(size_t)rho * ld + j] - t * Qm[(size_t)rho * ld + j];
       s = fma(v, v, s);
     }
+    s += s1;
   }
   scr[tid] = s;
   __syncthreads();
@@ -151,21 +252,113 @@ __device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const doubl
   const int ld = d.ld;
   const int nl = x.r1 - x.r0;
   const double alpha = d.alpha;
+  // Z rows of this CTA: staged in shared memory when they fit, so the gather
+  // addresses come from smem and only the Y loads go to L2
+  const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
+  const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
+  const int zoff = s.zstaged ? s.zoff : 0;
+  // one (row, column) per thread: a warp covers 32/bc rows, each gathered
+  // Y row segment is one coalesced transaction; 8 slots per round trip
   for (int it = threadIdx.x; it < nl * bc; it += blockDim.x) {
     const int rho = x.r0 + it / bc, jj = it % bc, j = c0 + jj;
-    double w = 0.0;
-    const double* Fr = d.F + (size_t)rho * ld;
-    for (int l = 0; l < rF; ++l) if (s.lamF[l] != 0.0) w = fma(Fr[l], s.T[l * bc + jj], w);
-    const double* Vr = d.V + (size_t)rho * ld;
-    for (int l = 0; l < nlock; ++l) w = fma(Vr[l], s.T[(rF + l) * bc + jj], w);
+    const int e1 = d.zptr[rho + 1] - zoff;
+    int e = d.zptr[rho] - zoff;
     double z = 0.0;
-    const int e1 = d.zptr[rho + 1];
-    for (int e = d.zptr[rho]; e < e1; ++e) z = fma(zv[e], Yin[(size_t)d.zcol[e] * ld + j], z);
+    for (; e + 8 <= e1; e += 8) {
+      double y[8], v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { v[u] = zval[e + u]; y[u] = Yin[(size_t)zcol[e + u] * ld + j]; }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) z = fma(v[u], y[u], z);
+    }
+    if (e < e1) {
+      double y[8], v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = e + u < e1;
+        v[u] = ok ? zval[e + u] : 0.0;
+        y[u] = ok ? Yin[(size_t)zcol[e + u] * ld + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) z = fma(v[u], y[u], z);
+    }
+    const double yin = (cb != 0.0) ? Yin[(size_t)rho * ld + j] : 0.0;
+    const double ypr = (cd != 0.0) ? Yprev[(size_t)rho * ld + j] : 0.0;
+    double w = 0.0;
+    const double* __restrict__ Fr = d.F + (size_t)rho * ld;
+#pragma unroll 4
+    for (int l = 0; l < rF; ++l) w = fma(Fr[l], s.T[l * bc + jj], w);
+    const double* __restrict__ Vr = d.V + (size_t)rho * ld;
+#pragma unroll 4
+    for (int l = 0; l < nlock; ++l) w = fma(Vr[l], s.T[(rF + l) * bc + jj], w);
     w = fma(-alpha, z, w);
     double o = ca * w;
-    if (cb != 0.0) o = fma(cb, Yin[(size_t)rho * ld + j], o);
-    if (cd != 0.0) o = fma(cd, Yprev[(size_t)rho * ld + j], o);
+    if (cb != 0.0) o = fma(cb, yin, o);
+    if (cd != 0.0) o = fma(cd, ypr, o);
     out[(size_t)rho * ld + j] = o;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+
+// Same contract as apply_rows, but the operand block Yin is first copied
+// into shared memory for ALL n rows (column chunks of width s.ycw, 16-byte
+// cp.async, every load independent), so the sparse product reads its
+// gathered rows from smem instead of issuing dependent L2 round trips.
+__device__ void apply_rows_staged(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
+                                  const double* __restrict__ Yin, const double* __restrict__ Yprev,
+                                  double* __restrict__ out, int c0, int bc, int rF, int nlock,
+                                  double ca, double cb, double cd) {
+  const int ld = d.ld, n = d.n;
+  const int nl = x.r1 - x.r0;
+  const double alpha = d.alpha;
+  const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
+  const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
+  const int zoff = s.zstaged ? s.zoff : 0;
+  double* ys = s.ys;
+  const int cw = s.ycw;                       // even
+  const int a0 = c0 & ~1, a1 = c0 + bc;       // aligned column span [a0, a1)
+  for (int cs0 = a0; cs0 < a1; cs0 += cw) {
+    const int pairs = cw >> 1;
+    for (int idx = threadIdx.x; idx < n * pairs; idx += blockDim.x) {
+      const int row = idx / pairs, pr = idx - row * pairs;
+      cp_async16(ys + (size_t)row * cw + 2 * pr, Yin + (size_t)row * ld + cs0 + 2 * pr);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int jlo = max(cs0, c0), jhi = min(cs0 + cw, a1), w_ = jhi - jlo;
+    for (int it = threadIdx.x; it < nl * w_; it += blockDim.x) {
+      const int rho = x.r0 + it / w_, j = jlo + it % w_, jj = j - c0, js = j - cs0;
+      const int e1 = d.zptr[rho + 1] - zoff;
+      int e = d.zptr[rho] - zoff;
+      double z0 = 0.0, z1 = 0.0;
+      for (; e + 2 <= e1; e += 2) {
+        z0 = fma(zval[e], ys[(size_t)zcol[e] * cw + js], z0);
+        z1 = fma(zval[e + 1], ys[(size_t)zcol[e + 1] * cw + js], z1);
+      }
+      if (e < e1) z0 = fma(zval[e], ys[(size_t)zcol[e] * cw + js], z0);
+      const double z = z0 + z1;
+      const double ypr = (cd != 0.0) ? Yprev[(size_t)rho * ld + j] : 0.0;
+      double w = 0.0;
+      const double* __restrict__ Fr = d.F + (size_t)rho * ld;
+#pragma unroll 4
+      for (int l = 0; l < rF; ++l) w = fma(Fr[l], s.T[l * bc + jj], w);
+      const double* __restrict__ Vr = d.V + (size_t)rho * ld;
+#pragma unroll 4
+      for (int l = 0; l < nlock; ++l) w = fma(Vr[l], s.T[(rF + l) * bc + jj], w);
+      w = fma(-alpha, z, w);
+      double o = ca * w;
+      if (cb != 0.0) o = fma(cb, ys[(size_t)rho * cw + js], o);
+      if (cd != 0.0) o = fma(cd, ypr, o);
+      out[(size_t)rho * ld + j] = o;
+    }
+    __syncthreads();
   }
 }
 
@@ -178,6 +371,7 @@ __device__ void rotate_rows(const Inst& d, const Cta& x, const double* __restric
     const int rho = x.r0 + it / b, j = it % b;
     const double* row = In + (size_t)rho * ld;
     double acc = 0.0;
+#pragma unroll 8
     for (int t = 0; t < b; ++t) acc = fma(row[t], Msm[t * lds + j], acc);
     out[(size_t)rho * ld + j] = acc;
   }
@@ -197,13 +391,17 @@ __device__ void scale_T(const Sm& s, int rF, int nlock, int bc) {
 // (one cluster barrier, which also publishes Yin to every CTA), then rows.
 __device__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* zv, const double* Yin,
                               const double* Yprev, double* out, int c0, int bc, int rF, int nlock,
-                              double ca, double cb, double cd) {
+                              double ca, double cb, double cd, Prof& pf) {
+  prof_mark(pf, 1);
   double* slot = red_slot(d, x, x.c);
-  gram_partial(d.F, rF, Yin + c0, bc, d.ld, x.r0, x.r1, slot, s.scr);
-  gram_partial(d.V, nlock, Yin + c0, bc, d.ld, x.r0, x.r1, slot + rF * bc, s.scr);
+  gram_mma(d.F, rF, Yin + c0, bc, d.ld, x.r0, x.r1, slot, s.gsc);
+  gram_mma(d.V, nlock, Yin + c0, bc, d.ld, x.r0, x.r1, slot + rF * bc, s.gsc);
+  prof_mark(pf, 2);
   cluster_reduce(d, x, (rF + nlock) * bc, 0, s.T);
   scale_T(s, rF, nlock, bc);
-  apply_rows(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
+  prof_mark(pf, 3);
+  if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
+  else apply_rows(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
 }
 
 // Convergence state of the Ritz block (identical in every thread).
@@ -268,9 +466,9 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
 }
 
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
-inline size_t iterate_smem_bytes(int lds) {
-  return (size_t)(5 * lds * lds + PDSDP_NTHR + 11 * PDSDP_BMAX) * sizeof(double) +
-         (size_t)(3 * PDSDP_BMAX + 8) * sizeof(int) + 64;
+inline size_t iterate_smem_bytes(int lds, int zcap, int ycap) {
+  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 11 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap) * sizeof(double) +
+         (size_t)(3 * PDSDP_BMAX + 8 + zcap) * sizeof(int) + 64;
 }
 
 __device__ int choose_block(int k, int n) {
@@ -285,7 +483,8 @@ __device__ int choose_block(int k, int n) {
 
 __global__ void __launch_bounds__(PDSDP_NTHR, 1)
 lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,
-                      const int* __restrict__ active, int lds) {
+                      const int* __restrict__ active, int lcap, int zcap, int ycap) {
+  const int lds = lcap + 1;   // odd stride of the b x b workspaces (no bank conflicts)
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cl = cg::this_cluster();
   Cta x;
@@ -300,18 +499,32 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   x.r1 = (int)(((long long)n * (x.c + 1)) / x.C);
   x.par = 0;
 
+  Prof pf;
+  pf.last = clock64(); pf.cur = 0;
+  for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
   Sm s;
   s.lds = lds;
   {
     double* p = smem;
-    const int sq = lds * lds;
+    const int sq = lcap * lds;
     s.A = p; p += sq; s.Q = p; p += sq; s.L = p; p += sq; s.M = p; p += sq; s.T = p; p += sq;
     s.scr = p; p += PDSDP_NTHR;
     s.theta = p; p += PDSDP_BMAX; s.res = p; p += PDSDP_BMAX; s.lamF = p; p += PDSDP_BMAX;
     s.lamN = p; p += PDSDP_BMAX; s.dsc = p; p += PDSDP_BMAX; s.cs = p; p += 2 * PDSDP_BMAX;
     s.red1 = p; p += 4 * PDSDP_BMAX;
+    s.gsc = p; p += PDSDP_GRAM_SCR;
+    s.ys = p; p += ycap;
+    double* zvs = p; p += zcap;
     int* ip = (int*)p;
     s.perm = ip; ip += PDSDP_BMAX; s.pq = ip; ip += 2 * PDSDP_BMAX; s.flag = ip; ip += 8;
+    int* zc = ip; ip += zcap;
+    s.zc = zc; s.zvs = zvs;
+    s.zoff = d.zptr[x.r0];
+    s.zstaged = (d.zptr[x.r1] - s.zoff) <= zcap ? 1 : 0;
+    int cw = ycap / d.n;
+    cw &= ~1;
+    if (cw > d.ld) cw = d.ld;
+    s.ycw = (cw >= 2) ? cw : 0;
   }
   double* buf[5] = {d.V, d.AV, d.Y0, d.Y1, d.Y2};
 
@@ -340,14 +553,22 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.lamF[i] = rerun ? st->lamF[i] : ((i < rF && th > 0.0) ? th : 0.0);
     s.res[i] = (!cold && i < b_old) ? st->res[i] : 1.0e300;
   }
+  __syncthreads();
   const double lo = st->lo_par[ctl.ypar & 1];
   const double alpha = d.alpha;
   const double* zv = (ctl.ypar & 1) ? d.zbuf1 : d.zbuf0;     // Z_k  = C + M^T y_k
   double* zvn = (ctl.ypar & 1) ? d.zbuf0 : d.zbuf1;          // Z_k+1
+  if (s.zstaged) {
+    const int nzl = d.zptr[x.r1] - s.zoff;
+    for (int e = tid; e < nzl; e += blockDim.x) {
+      ((int*)s.zc)[e] = d.zcol[s.zoff + e];
+      ((double*)s.zvs)[e] = zv[s.zoff + e];
+    }
+  }
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
     const int rho = x.r0 + it / b, j = it % b;
     double* Vr = d.V + (size_t)rho * ld;
-    if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = Vr[j];
+    if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = (s.lamF[j] != 0.0) ? Vr[j] : 0.0;
     if (j >= b_old) Vr[j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
   }
   __syncthreads();
@@ -424,13 +645,13 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
               buf[io][o] = fma(ca, buf[iav][o], cb * d.V[o]);
             }
           } else {
-            operator_step(d, x, s, zv, d.V, nullptr, buf[io], c0, bc, rF, nlock, ca, cb, 0.0);
+            operator_step(d, x, s, zv, d.V, nullptr, buf[io], c0, bc, rF, nlock, ca, cb, 0.0, pf);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step(d, x, s, zv, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], c0, bc, rF, nlock, ca, cb, cd);
+          operator_step(d, x, s, zv, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], c0, bc, rF, nlock, ca, cb, cd, pf);
           ++matvecs;
           sg = sn;
         }
@@ -455,14 +676,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     for (int q2 = 0; q2 < 3; ++q2) if (fre[q2] != iy && fre[q2] != iw) { iw1 = fre[q2]; break; }
     {
       double* slot = red_slot(d, x, x.c);
-      gram_partial(buf[iy], b, buf[iy], b, ld, x.r0, x.r1, slot, s.scr);
-      gram_partial(d.F, rF, buf[iy], b, ld, x.r0, x.r1, slot + b * b, s.scr);
+      prof_mark(pf, 1);
+      gram_mma(buf[iy], b, buf[iy], b, ld, x.r0, x.r1, slot, s.gsc);
+      gram_mma(d.F, rF, buf[iy], b, ld, x.r0, x.r1, slot + b * b, s.gsc);
       // reduce into A (G1) and T
       cg::this_cluster().sync();
       const int q = b * b + rF * b;
       for (int i = tid; i < q; i += blockDim.x) {
-        double acc = 0.0;
-        for (int cc = 0; cc < x.C; ++cc) acc += red_slot(d, x, cc)[i];
+        const double acc = cluster_sum(d, x, i, false);
         if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
         else s.T[i - b * b] = acc;
       }
@@ -470,7 +691,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
     }
     scale_T(s, rF, 0, b);
-    apply_rows(d, x, s, zv, buf[iy], nullptr, buf[iw], 0, b, rF, 0, 1.0, 0.0, 0.0);
+    prof_mark(pf, 3);
+    if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf[iy], nullptr, buf[iw], 0, b, rF, 0, 1.0, 0.0, 0.0);
+    else apply_rows(d, x, s, zv, buf[iy], nullptr, buf[iw], 0, b, rF, 0, 1.0, 0.0, 0.0);
+    prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
     bool okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
@@ -481,6 +705,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
       continue;
     }
+    prof_mark(pf, 9);
     tri_inv_lower(s.A, s.L, b, lds);
     for (int e = tid; e < b * b; e += blockDim.x) {
       int i = e / b, j = e % b;
@@ -488,19 +713,19 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     __syncthreads();
     // Y1 = Y M1 -> buf[iav] ; W1 = W M1 -> buf[iw1]
+    prof_mark(pf, 5);
     rotate_rows(d, x, buf[iy], s.M, lds, buf[iav], b);
     rotate_rows(d, x, buf[iw], s.M, lds, buf[iw1], b);
     __syncthreads();
     // ---- R2: G2 = Y1^T Y1, H = Y1^T W1 ----
     {
       double* slot = red_slot(d, x, x.c);
-      gram_partial(buf[iav], b, buf[iav], b, ld, x.r0, x.r1, slot, s.scr);
-      gram_partial(buf[iav], b, buf[iw1], b, ld, x.r0, x.r1, slot + b * b, s.scr);
+      gram_mma(buf[iav], b, buf[iav], b, ld, x.r0, x.r1, slot, s.gsc);
+      gram_mma(buf[iav], b, buf[iw1], b, ld, x.r0, x.r1, slot + b * b, s.gsc);
       cg::this_cluster().sync();
       const int q = 2 * b * b;
       for (int i = tid; i < q; i += blockDim.x) {
-        double acc = 0.0;
-        for (int cc = 0; cc < x.C; ++cc) acc += red_slot(d, x, cc)[i];
+        const double acc = cluster_sum(d, x, i, false);
         if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
         else { int e = i - b * b; s.Q[(e / b) * lds + (e % b)] = acc; }
       }
@@ -508,6 +733,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
     }
     // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe
+    prof_mark(pf, 8);
     okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
     if (!okc) {
       if (++fails >= 8 || m == 0) break;
@@ -515,7 +741,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       continue;
     }
     if (nlock == 0) msucc += m;
+    prof_mark(pf, 9);
     tri_inv_lower(s.A, s.L, b, lds);            // L = L2^-1
+    prof_mark(pf, 10);
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
       s.Q[i * lds + j] *= s.dsc[i] * s.dsc[j];
@@ -534,7 +762,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       if (j > i) { double v = 0.5 * (s.A[i * lds + j] + s.A[j * lds + i]); s.A[i * lds + j] = v; s.A[j * lds + i] = v; }
     }
     __syncthreads();
-    jacobi_eig(s.A, s.Q, b, lds, s.cs, s.pq, s.flag);
+    if ((ctl.flags & 16) && x.c == 0) {
+      for (int e = tid; e < b * b; e += blockDim.x) st->hdump[e] = s.A[(e / b) * lds + (e % b)];
+      if (tid == 0) st->hdump[PDSDP_BMAX * PDSDP_BMAX] = b;
+    }
+    prof_mark(pf, 11);
+    // pairs among the trailing guard columns only need loose accuracy (their
+    // Ritz pairs are not used; residuals are recomputed honestly below)
+    jacobi_eig(s.A, s.Q, b, lds, s.cs, s.pq, s.flag, need_cert ? b : min(b, r + 1));
+    prof_mark(pf, 12);
+    if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];
     sort_desc(s.A, b, lds, s.theta, s.perm);
     // B = D L^-T Q[:, perm]  -> s.M
     for (int e = tid; e < b * b; e += blockDim.x) {
@@ -546,6 +783,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     __syncthreads();
     // V = Y1 B ; AV = W1 B  (AV goes to buf[iw], which becomes the AV buffer)
+    prof_mark(pf, 5);
     rotate_rows(d, x, buf[iav], s.M, lds, d.V, b);
     rotate_rows(d, x, buf[iw1], s.M, lds, buf[iw], b);
     iav = iw;
@@ -575,6 +813,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) s.lamN[i] = (i < r && i < b && s.theta[i] > 0.0) ? s.theta[i] : 0.0;
   __syncthreads();
 
+  prof_mark(pf, 6);
   // ---------------- dual step: y+ = u - alpha proj_box(u/alpha) ----------------
   const double* yk = ctl.ypar ? d.ybuf1 : d.ybuf0;
   double* yn = ctl.ypar ? d.ybuf0 : d.ybuf1;
@@ -640,6 +879,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   double fin_tot = -s.red1[1];
   for (int i = 0; i < rN; ++i) if (s.theta[i] > 0.0 && !isfinite(s.theta[i])) fin_tot = 0.0;
 
+  prof_mark(pf, 7);
   // ---------------- adjoint gather: Z_{k+1} = C + M^T y+, support correction ----------------
   double corr = 0.0;
   {
@@ -692,6 +932,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   cluster_reduce(d, x, 1, 1, s.red1);
 
   // ---------------- epilogue: state for the next iteration + scalars ----------------
+  prof_mark(pf, 0);
+  if (x.c == 0 && tid == 0)
+    for (int q = 0; q < 15; ++q) st->prof[q] = (double)pf.acc[q];
   if (x.c == 0) {
     for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
       st->theta[i] = (i < b) ? s.theta[i] : 0.0;

@@ -53,6 +53,7 @@ struct Arena {
 
 struct Instance {
   int n = 0, m = 0, p = 0, mp = 0, ld = 0;
+  int bmax = 0;          // largest eigen block used so far (smem workspace size)
   long long nz = 0;
   int group = 1;
   int ntile = 0;
@@ -90,6 +91,8 @@ struct pdsdp_batch {
   unsigned* d_objcnt = nullptr;
   double* d_objres = nullptr;
   int max_tiles = 1;
+  long long zmax = 0;    // largest per-CTA slice of Z rows over the batch
+  int nmax = 0, ldmax = 0;
   int timing = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0;
@@ -361,11 +364,23 @@ int check_inst(pdsdp_batch* b, int inst) {
   return PDSDP_OK;
 }
 
-int launch_iterate(pdsdp_batch* b, int nact) {
+int launch_iterate(pdsdp_batch* b, int nact, int lds) {
+  // shared memory beyond the fixed workspaces: first the CTA's Z rows (zcap
+  // slots, all-or-nothing), then the staged operand block (ycap doubles: up to
+  // n x min(ld, 16) so that a block of <= 16 columns is staged in one chunk)
+  const size_t base = iterate_smem_bytes(lds, 0, 0);
+  const size_t limit = b->smem;
+  size_t avail = limit > base ? limit - base : 0;
+  int zcap = (int)std::min<long long>(b->zmax, (long long)(avail / 12));
+  if (zcap < b->zmax) zcap = 0;
+  avail -= (size_t)zcap * 12;
+  long long want = (long long)b->nmax * std::min(b->ldmax, 16);
+  int ycap = (int)std::min<long long>(want, (long long)(avail / 8));
+  if (ycap < 2 * b->nmax) ycap = 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nact * b->C);
   cfg.blockDim = dim3(PDSDP_NTHR);
-  cfg.dynamicSmemBytes = b->smem;
+  cfg.dynamicSmemBytes = iterate_smem_bytes(lds, zcap, ycap);
   cfg.stream = b->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -375,7 +390,7 @@ int launch_iterate(pdsdp_batch* b, int nact) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, lrpdhg_iterate_kernel, (const Inst*)b->d_insts, (const Ctl*)b->d_ctl,
-                        (const int*)b->d_active, b->lds));
+                        (const int*)b->d_active, lds, zcap, ycap));
   return PDSDP_OK;
 }
 
@@ -411,7 +426,11 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
   b->C = C;
   int lds = std::min(maxn, PDSDP_BMAX);
   b->lds = lds < 4 ? 4 : lds;
-  b->smem = iterate_smem_bytes(b->lds);
+  {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, lrpdhg_iterate_kernel));
+    b->smem = 227 * 1024 - fa.sharedSizeBytes;   // dynamic limit next to the static part
+  }
   CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
   CK(cudaHostAlloc((void**)&b->h_out, (size_t)count * PDSDP_OUT_LEN * sizeof(double), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&b->d_out, b->h_out, 0));
@@ -435,6 +454,12 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
     if (rc) { std::string e = g_err; pdsdp_batch_destroy(b); g_err = e; return rc; }
     descs[k] = I->desc;
     b->max_tiles = std::max(b->max_tiles, I->ntile);
+    b->nmax = std::max(b->nmax, I->n);
+    b->ldmax = std::max(b->ldmax, I->ld);
+    for (int c = 0; c < C; ++c) {
+      const long long r0 = (long long)I->n * c / C, r1 = (long long)I->n * (c + 1) / C;
+      b->zmax = std::max<long long>(b->zmax, (long long)I->zptr[r1] - I->zptr[r0]);
+    }
   }
   CK(cudaMemcpy(b->d_insts, descs.data(), count * sizeof(Inst), cudaMemcpyHostToDevice));
   if (C > 8) CK(cudaFuncSetAttribute(lrpdhg_iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -545,6 +570,7 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed) {
   int rc = check_inst(b, inst);
   if (rc) return rc;
   Instance* I = b->inst[inst];
+  I->bmax = 0;
   CK(cudaMemsetAsync(I->desc.st, 0, sizeof(State), b->stream));
   CK(cudaMemsetAsync(I->desc.V, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
   CK(cudaMemsetAsync(I->desc.F, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
@@ -577,7 +603,16 @@ int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t*
   CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, N * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
   CK(cudaMemcpyAsync(b->d_active, b->h_active, nact * sizeof(int), cudaMemcpyHostToDevice, b->stream));
   if (b->timing) CK(cudaEventRecord(b->ev[0], b->stream));
-  int rc = launch_iterate(b, nact);
+  int lds = 4;
+  for (int a = 0; a < nact; ++a) {
+    Instance* I = b->inst[insts[a]];
+    const int kk = std::min(rank[a] + 1, I->n);
+    int g = std::max(kk / 4, 4);
+    int bb = std::min(std::min((kk + g + 3) & ~3, PDSDP_BMAX), I->n);
+    I->bmax = std::max(I->bmax, bb);
+    lds = std::max(lds, I->bmax);
+  }
+  int rc = launch_iterate(b, nact, lds);
   if (rc) return rc;
   if (b->timing) CK(cudaEventRecord(b->ev[1], b->stream));
   int maxr = 1;
@@ -617,6 +652,11 @@ int pdsdp_debug(pdsdp_batch* b, int inst, double* out) {
   memcpy(out, h.dbg, sizeof(h.dbg));
   memcpy(out + 256, h.theta, sizeof(h.theta));
   memcpy(out + 320, h.res, sizeof(h.res));
+  memcpy(out + 384, h.prof, sizeof(h.prof));
+  memcpy(out + 400, h.hdump, sizeof(h.hdump));
+  // reset the per-launch accumulators that the kernel adds into
+  State* dst = b->inst[inst]->desc.st;
+  CK(cudaMemset(&dst->prof[15], 0, sizeof(double)));
   return PDSDP_OK;
 }
 

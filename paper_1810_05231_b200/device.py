@@ -162,9 +162,12 @@ class DeviceBatch:
                 "residual_ms": out[2], "residual_launches": int(out[3])}
 
     def debug(self, inst: int = 0) -> dict:
-        out = np.zeros(384)
+        out = np.zeros(4504)
         _check(self.lib.pdsdp_debug(self.h, inst, _ptr(out)))
-        return {"passes": out[:256].reshape(32, 8), "theta": out[256:320], "res": out[320:384]}
+        bh = int(out[400 + 4096])
+        return {"passes": out[:256].reshape(32, 8), "theta": out[256:320], "res": out[320:384],
+                "prof_cycles": out[384:400],
+                "H": out[400:400 + bh * bh].reshape(bh, bh) if bh > 0 else None}
 
     # ---- operator norm (problem.py:157-185) ----
     def opnorm_positions(self, inst: int) -> np.ndarray:
