@@ -33,6 +33,7 @@ extern "C" {
 
 #define PDSDP_BLOCK_MAX 64
 #define PDSDP_OUT_LEN 16
+#define PDSDP_KMAX 64
 
 /* Output slots of one iteration (doubles, PDSDP_OUT_LEN per instance). */
 enum {
@@ -47,7 +48,8 @@ enum {
   PDSDP_OUT_DENSE = 8,
   PDSDP_OUT_CORR = 9,
   PDSDP_OUT_ED2 = 10,
-  PDSDP_OUT_BLOCK = 11   /* eigen block size b                              */
+  PDSDP_OUT_BLOCK = 11,  /* eigen block size b                              */
+  PDSDP_OUT_DONE = 12    /* 1 if the step executed (pdsdp_iterate_many)      */
 };
 
 /* One SDP in the reference's general form (problem.py:73-105). */
@@ -93,6 +95,19 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed);
  * per listed instance; out: nact * PDSDP_OUT_LEN doubles (host). */
 int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank,
                   const int32_t* ypar, const int32_t* flags, int32_t maxpass, double* out);
+
+/* Up to K (<= 64) consecutive iterations with one host synchronisation.
+ * Step j of listed instance a runs with y parity ypar0[a]^j.  The device
+ * pauses an instance after the first step whose combined residual
+ * eps_p + eps_d is <= conv_thr[a] or >= stall_thr[a*K + j], or whose iterate
+ * is not finite -- exactly the steps at which the host's Algorithm-2 logic
+ * (lowrank.py:145-185) may act.  out: nact * K * PDSDP_OUT_LEN doubles;
+ * steps_done[a] = executed steps.  The rank-adaptation decisions stay on the
+ * host; the device only reports scalars. */
+int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank,
+                       const int32_t* ypar0, const int32_t* flags, int32_t maxpass, int32_t K,
+                       const double* conv_thr, const double* stall_thr, double* out,
+                       int32_t* steps_done);
 
 /* tr(C X) (lowrank.py:159,168,191) for X = the newest iterate (which = 0)
  * or the previous one (which = 1). */

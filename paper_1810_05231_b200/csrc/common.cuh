@@ -19,7 +19,8 @@
 #define PDSDP_BMAX 64          // largest eigen block (k = r+1 plus guard vectors)
 #define PDSDP_NTHR 512         // threads per CTA of the cluster kernel
 #define PDSDP_RED_MAX (2 * PDSDP_BMAX * PDSDP_BMAX + 64)
-#define PDSDP_OUT_LEN 16       // doubles per instance in the host-mapped output
+#define PDSDP_OUT_LEN 16       // doubles per instance and step in the host-mapped output
+#define PDSDP_KMAX 64          // iterations per pdsdp_iterate_many call
 
 namespace pdsdp {
 
@@ -97,20 +98,23 @@ struct Inst {
   double* rpart;       // residual kernel tile partials
   unsigned int* rcount;
   State* st;
-  double* out;         // host-mapped [OUT_LEN]
+  double* out;         // host-mapped [KMAX][OUT_LEN]
+  int* stopf;          // device flag: an event may fire, skip the remaining steps
 };
 
 // Per-launch control for one instance.
 struct Ctl {
   int r;       // target rank for this iteration
   int ypar;    // y_k lives in ybuf[ypar], y_{k+1} goes to ybuf[ypar^1]
-  int flags;   // bit0: cold start (reset V/theta)
+  int flags;   // bit0 cold, bit1 certificate, bit2 re-run, bit3 tight certificate, bit4 dump
   int maxpass;
+  double conv_thr;    // stop when eps_p + eps_d <= conv_thr  (lowrank.py:161)
+  double stall_thr;   // stop when eps_p + eps_d >= stall_thr (lowrank.py:64-69, 181)
 };
 
 // output slots
 enum { O_EPS_P = 0, O_EPS_D, O_LAM, O_FIN, O_PASSES, O_MATVECS, O_EIGCONV, O_EIGRES,
-       O_DENSE, O_CORR, O_ED2, O_BLK };
+       O_DENSE, O_CORR, O_ED2, O_BLK, O_DONE };
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -483,7 +483,7 @@ __device__ int choose_block(int k, int n) {
 
 __global__ void __launch_bounds__(PDSDP_NTHR, 1)
 lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,
-                      const int* __restrict__ active, int lcap, int zcap, int ycap) {
+                      const int* __restrict__ active, int step, int lcap, int zcap, int ycap) {
   const int lds = lcap + 1;   // odd stride of the b x b workspaces (no bank conflicts)
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -492,7 +492,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   x.c = (int)cl.block_rank();
   const int inst_id = active[blockIdx.x / x.C];
   const Inst d = insts[inst_id];
-  const Ctl ctl = ctls[inst_id];
+  if (*(volatile int*)d.stopf) return;            // an earlier step of this chunk ended it
+  const Ctl ctl = ctls[inst_id * PDSDP_KMAX + step];
   State* st = d.st;
   const int n = d.n, ld = d.ld, tid = threadIdx.x;
   x.r0 = (int)(((long long)n * x.c) / x.C);
@@ -951,7 +952,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       st->corr = s.red1[0];
       st->lo_par[(ctl.ypar & 1) ^ 1] = -alpha * s.red1[1];
       st->finite = fin_tot;
-      double* o = d.out;
+      double* o = d.out + step * PDSDP_OUT_LEN;
       o[O_LAM] = s.theta[k - 1];
       o[O_FIN] = fin_tot;
       o[O_PASSES] = passes;

@@ -85,7 +85,8 @@ struct pdsdp_batch {
   Ctl* d_ctl = nullptr;
   int* h_active = nullptr;
   int* d_active = nullptr;
-  double* h_out = nullptr;   // mapped pinned, count * OUT_LEN
+  double* h_out = nullptr;   // mapped pinned, count * KMAX * OUT_LEN
+  int* d_stop = nullptr;     // per-instance chunk stop flags
   double* d_out = nullptr;
   double* d_objpart = nullptr;
   unsigned* d_objcnt = nullptr;
@@ -364,7 +365,7 @@ int check_inst(pdsdp_batch* b, int inst) {
   return PDSDP_OK;
 }
 
-int launch_iterate(pdsdp_batch* b, int nact, int lds) {
+int launch_iterate(pdsdp_batch* b, int nact, int lds, int step) {
   // shared memory beyond the fixed workspaces: first the CTA's Z rows (zcap
   // slots, all-or-nothing), then the staged operand block (ycap doubles: up to
   // n x min(ld, 16) so that a block of <= 16 columns is staged in one chunk)
@@ -390,7 +391,7 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, lrpdhg_iterate_kernel, (const Inst*)b->d_insts, (const Ctl*)b->d_ctl,
-                        (const int*)b->d_active, lds, zcap, ycap));
+                        (const int*)b->d_active, step, lds, zcap, ycap));
   return PDSDP_OK;
 }
 
@@ -432,12 +433,16 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
     b->smem = 227 * 1024 - fa.sharedSizeBytes;   // dynamic limit next to the static part
   }
   CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
-  CK(cudaHostAlloc((void**)&b->h_out, (size_t)count * PDSDP_OUT_LEN * sizeof(double), cudaHostAllocMapped));
+  const size_t outn = (size_t)count * PDSDP_KMAX * PDSDP_OUT_LEN;
+  CK(cudaHostAlloc((void**)&b->h_out, outn * sizeof(double), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&b->d_out, b->h_out, 0));
-  memset(b->h_out, 0, (size_t)count * PDSDP_OUT_LEN * sizeof(double));
-  CK(cudaHostAlloc((void**)&b->h_ctl, (size_t)count * sizeof(Ctl), 0));
+  memset(b->h_out, 0, outn * sizeof(double));
+  CK(cudaHostAlloc((void**)&b->h_ctl, (size_t)count * PDSDP_KMAX * sizeof(Ctl), 0));
+  memset(b->h_ctl, 0, (size_t)count * PDSDP_KMAX * sizeof(Ctl));
+  CK(cudaMalloc(&b->d_stop, (size_t)count * sizeof(int)));
+  CK(cudaMemset(b->d_stop, 0, (size_t)count * sizeof(int)));
   CK(cudaHostAlloc((void**)&b->h_active, (size_t)count * sizeof(int), 0));
-  CK(cudaMalloc(&b->d_ctl, (size_t)count * sizeof(Ctl)));
+  CK(cudaMalloc(&b->d_ctl, (size_t)count * PDSDP_KMAX * sizeof(Ctl)));
   CK(cudaMalloc(&b->d_active, (size_t)count * sizeof(int)));
   CK(cudaMalloc(&b->d_insts, (size_t)count * sizeof(Inst)));
   CK(cudaMalloc(&b->d_objpart, (size_t)count * 256 * sizeof(double)));
@@ -450,7 +455,8 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
     b->inst.push_back(I);
     int rc = build_instance(problems[k], *I);
     if (rc) { pdsdp_batch_destroy(b); return rc; }
-    rc = alloc_instance(*I, C, b->d_out + (size_t)k * PDSDP_OUT_LEN);
+    rc = alloc_instance(*I, C, b->d_out + (size_t)k * PDSDP_KMAX * PDSDP_OUT_LEN);
+    I->desc.stopf = b->d_stop + k;
     if (rc) { std::string e = g_err; pdsdp_batch_destroy(b); g_err = e; return rc; }
     descs[k] = I->desc;
     b->max_tiles = std::max(b->max_tiles, I->ntile);
@@ -490,6 +496,7 @@ int pdsdp_batch_destroy(pdsdp_batch* b) {
   if (b->d_objpart) cudaFree(b->d_objpart);
   if (b->d_objcnt) cudaFree(b->d_objcnt);
   if (b->d_objres) cudaFree(b->d_objres);
+  if (b->d_stop) cudaFree(b->d_stop);
   for (int k = 0; k < 3; ++k) if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   if (b->stream) cudaStreamDestroy(b->stream);
   delete b;
@@ -581,57 +588,76 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed) {
   return PDSDP_OK;
 }
 
-int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank, const int32_t* ypar,
-                  const int32_t* flags, int32_t maxpass, double* out) {
-  if (!b || nact < 1 || nact > (int)b->inst.size() || !insts || !rank || !ypar || !out)
+int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank, const int32_t* ypar0,
+                       const int32_t* flags, int32_t maxpass, int32_t K, const double* conv_thr,
+                       const double* stall_thr, double* out, int32_t* steps_done) {
+  if (!b || nact < 1 || nact > (int)b->inst.size() || !insts || !rank || !ypar0 || !out)
     return fail(PDSDP_EINVAL, "bad iterate arguments");
+  if (K < 1 || K > PDSDP_KMAX) return fail(PDSDP_EINVAL, "K must lie in [1, 64]");
   const int N = (int)b->inst.size();
+  int lds = 4, maxr = 1;
   for (int a = 0; a < nact; ++a) {
     const int k = insts[a];
     if (k < 0 || k >= N) return fail(PDSDP_EINVAL, "instance index out of range");
-    const Instance* I = b->inst[k];
+    Instance* I = b->inst[k];
     if (rank[a] < 1 || rank[a] > I->n)
       return fail(PDSDP_EINVAL, "rank r=" + std::to_string(rank[a]) + " outside [1, " + std::to_string(I->n) + "]");
     const int kk = std::min(rank[a] + 1, I->n);
     if (kk > PDSDP_BMAX) return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + " needs an eigen block above 64");
-    b->h_ctl[k].r = rank[a];
-    b->h_ctl[k].ypar = ypar[a] & 1;
-    b->h_ctl[k].flags = flags ? flags[a] : 0;
-    b->h_ctl[k].maxpass = maxpass;
+    for (int j = 0; j < K; ++j) {
+      Ctl& c = b->h_ctl[(size_t)k * PDSDP_KMAX + j];
+      c.r = rank[a];
+      c.ypar = (ypar0[a] ^ j) & 1;
+      c.flags = flags ? flags[a] : 0;
+      c.maxpass = maxpass;
+      c.conv_thr = conv_thr ? conv_thr[a] : -1.0;
+      c.stall_thr = stall_thr ? stall_thr[(size_t)a * K + j] : HUGE_VAL;
+      b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_DONE] = 0.0;
+    }
     b->h_active[a] = k;
-  }
-  CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, N * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
-  CK(cudaMemcpyAsync(b->d_active, b->h_active, nact * sizeof(int), cudaMemcpyHostToDevice, b->stream));
-  if (b->timing) CK(cudaEventRecord(b->ev[0], b->stream));
-  int lds = 4;
-  for (int a = 0; a < nact; ++a) {
-    Instance* I = b->inst[insts[a]];
-    const int kk = std::min(rank[a] + 1, I->n);
-    int g = std::max(kk / 4, 4);
-    int bb = std::min(std::min((kk + g + 3) & ~3, PDSDP_BMAX), I->n);
+    const int g = std::max(kk / 4, 4);
+    const int bb = std::min(std::min((kk + g + 3) & ~3, PDSDP_BMAX), I->n);
     I->bmax = std::max(I->bmax, bb);
     lds = std::max(lds, I->bmax);
+    maxr = std::max(maxr, (int)rank[a]);
   }
-  int rc = launch_iterate(b, nact, lds);
-  if (rc) return rc;
-  if (b->timing) CK(cudaEventRecord(b->ev[1], b->stream));
-  int maxr = 1;
-  for (int a = 0; a < nact; ++a) maxr = std::max(maxr, (int)rank[a]);
+  CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, (size_t)N * PDSDP_KMAX * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(b->d_active, b->h_active, nact * sizeof(int), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemsetAsync(b->d_stop, 0, (size_t)N * sizeof(int), b->stream));
   const int kp = std::min(RES_KMAX, (2 * std::min(maxr, PDSDP_BMAX) + 3) & ~3);
   const size_t rsm = (size_t)2 * RES_TILE * (kp + 1) * sizeof(double);
-  residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_active);
-  CK(cudaGetLastError());
-  if (b->timing) CK(cudaEventRecord(b->ev[2], b->stream));
+  for (int j = 0; j < K; ++j) {
+    const bool tm = b->timing && j == 0;
+    if (tm) CK(cudaEventRecord(b->ev[0], b->stream));
+    int rc = launch_iterate(b, nact, lds, j);
+    if (rc) return rc;
+    if (tm) CK(cudaEventRecord(b->ev[1], b->stream));
+    residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_ctl, b->d_active, j);
+    CK(cudaGetLastError());
+    if (tm) CK(cudaEventRecord(b->ev[2], b->stream));
+  }
   CK(cudaStreamSynchronize(b->stream));
   if (b->timing) {
-    float a = 0.f, c = 0.f;
-    CK(cudaEventElapsedTime(&a, b->ev[0], b->ev[1]));
-    CK(cudaEventElapsedTime(&c, b->ev[1], b->ev[2]));
-    b->t_iter += a; b->n_iter += 1; b->t_res += c; b->n_res += 1;
+    float t1 = 0.f, t2 = 0.f;
+    CK(cudaEventElapsedTime(&t1, b->ev[0], b->ev[1]));
+    CK(cudaEventElapsedTime(&t2, b->ev[1], b->ev[2]));
+    b->t_iter += t1; b->n_iter += 1; b->t_res += t2; b->n_res += 1;
   }
-  for (int a = 0; a < nact; ++a)
-    memcpy(out + (size_t)a * PDSDP_OUT_LEN, b->h_out + (size_t)insts[a] * PDSDP_OUT_LEN, PDSDP_OUT_LEN * sizeof(double));
+  for (int a = 0; a < nact; ++a) {
+    int done = 0;
+    for (int j = 0; j < K; ++j) {
+      const double* src = b->h_out + ((size_t)insts[a] * PDSDP_KMAX + j) * PDSDP_OUT_LEN;
+      memcpy(out + ((size_t)a * K + j) * PDSDP_OUT_LEN, src, PDSDP_OUT_LEN * sizeof(double));
+      if (src[O_DONE] == 1.0) done = j + 1;
+    }
+    if (steps_done) steps_done[a] = done;
+  }
   return PDSDP_OK;
+}
+
+int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank, const int32_t* ypar,
+                  const int32_t* flags, int32_t maxpass, double* out) {
+  return pdsdp_iterate_many(b, nact, insts, rank, ypar, flags, maxpass, 1, nullptr, nullptr, out, nullptr);
 }
 
 int pdsdp_set_timing(pdsdp_batch* b, int enable) {

@@ -33,9 +33,12 @@ __device__ __forceinline__ void tile_of(int t, int nt, int& I, int& J) {
 
 // grid: (max tiles, active instances); block RES_THREADS (4 warps)
 __global__ void __launch_bounds__(RES_THREADS)
-residual_kernel(const Inst* __restrict__ insts, const int* __restrict__ active) {
+residual_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls, const int* __restrict__ active,
+                int step) {
   extern __shared__ __align__(16) double rsm[];
-  const Inst d = insts[active[blockIdx.y]];
+  const int inst_id = active[blockIdx.y];
+  const Inst d = insts[inst_id];
+  if (*(volatile int*)d.stopf) return;
   const State* st = d.st;
   const int n = d.n, ld = d.ld;
   const int nt = (n + RES_TILE - 1) / RES_TILE;
@@ -127,11 +130,17 @@ residual_kernel(const Inst* __restrict__ insts, const int* __restrict__ active) 
     double dense = 0.0;
     for (int w = 0; w < RES_THREADS / 32; ++w) dense += wsum[w];
     const double ep2 = dense + st->corr;
-    double* o = d.out;
+    double* o = d.out + step * PDSDP_OUT_LEN;
+    const double ep = sqrt(fmax(ep2, 0.0)), ed = sqrt(fmax(st->ed2, 0.0));
     o[O_DENSE] = dense;
-    o[O_EPS_P] = sqrt(fmax(ep2, 0.0));
-    o[O_EPS_D] = sqrt(fmax(st->ed2, 0.0));
+    o[O_EPS_P] = ep;
+    o[O_EPS_D] = ed;
+    o[O_DONE] = 1.0;
     *d.rcount = 0u;
+    // pause the chunk where the host's control logic may act (lowrank.py:145-185)
+    const Ctl c = ctls[inst_id * PDSDP_KMAX + step];
+    const double ec = ep + ed;
+    if (st->finite != 1.0 || ec <= c.conv_thr || ec >= c.stall_thr) *d.stopf = 1;
   }
 }
 

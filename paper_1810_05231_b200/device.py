@@ -22,7 +22,9 @@ OUT_LEN = 16
 OUT_EPS_P, OUT_EPS_D, OUT_LAMBDA, OUT_FINITE = 0, 1, 2, 3
 OUT_PASSES, OUT_MATVECS, OUT_EIGCONV, OUT_EIGRES = 4, 5, 6, 7
 OUT_BLOCK = 11
+OUT_DONE = 12
 BLOCK_MAX = 64
+KMAX = 64
 
 EINVAL, ECUDA, ENOMEM, ERANK = -1, -2, -3, -4
 
@@ -32,7 +34,7 @@ EXPORTED = (
     "pdsdp_iterate", "pdsdp_objective", "pdsdp_download_x", "pdsdp_download_y",
     "pdsdp_apply_M", "pdsdp_apply_M_adjoint", "pdsdp_aproj_psd", "pdsdp_strerror",
     "pdsdp_last_error", "pdsdp_version", "pdsdp_set_timing", "pdsdp_kernel_times",
-    "pdsdp_debug",
+    "pdsdp_debug", "pdsdp_iterate_many",
 )
 
 
@@ -82,6 +84,7 @@ def load_library(path: str = LIB_PATH):
             "pdsdp_set_timing": (ct.c_int, [P, ct.c_int]),
             "pdsdp_kernel_times": (ct.c_int, [P, P]),
             "pdsdp_debug": (ct.c_int, [P, ct.c_int, P]),
+            "pdsdp_iterate_many": (ct.c_int, [P, ct.c_int, P, P, P, P, I32, I32, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -201,6 +204,22 @@ class DeviceBatch:
         _check(self.lib.pdsdp_iterate(self.h, insts.size, _ptr(insts), _ptr(ranks), _ptr(ypars),
                                       _ptr(fl), int(maxpass), _ptr(out)))
         return out
+
+    def iterate_many(self, insts, ranks, ypar0, K: int, conv_thr, stall_thr, flags=None,
+                     maxpass: int = 60):
+        """Up to K steps per instance; returns (out[nact, K, OUT_LEN], steps_done[nact])."""
+        insts = np.ascontiguousarray(insts, dtype=np.int32)
+        ranks = np.ascontiguousarray(ranks, dtype=np.int32)
+        ypar0 = np.ascontiguousarray(ypar0, dtype=np.int32)
+        fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.int32)
+        conv = np.ascontiguousarray(conv_thr, dtype=np.float64)
+        stall = np.ascontiguousarray(stall_thr, dtype=np.float64).reshape(insts.size, K)
+        out = np.zeros((insts.size, K, OUT_LEN))
+        done = np.zeros(insts.size, dtype=np.int32)
+        _check(self.lib.pdsdp_iterate_many(self.h, insts.size, _ptr(insts), _ptr(ranks), _ptr(ypar0),
+                                           _ptr(fl), int(maxpass), int(K), _ptr(conv), _ptr(stall),
+                                           _ptr(out), _ptr(done)))
+        return out, done
 
     def objective(self, inst: int, which: int = 0) -> float:
         v = np.zeros(1)

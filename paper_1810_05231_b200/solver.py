@@ -32,7 +32,7 @@ from .config import (
     update_rank,
 )
 from .device import (
-    OUT_EIGCONV, OUT_EPS_D, OUT_EPS_P, OUT_FINITE, OUT_LAMBDA, OUT_MATVECS, OUT_PASSES,
+    KMAX, OUT_EIGCONV, OUT_EPS_D, OUT_EPS_P, OUT_FINITE, OUT_LAMBDA, OUT_MATVECS, OUT_PASSES,
     DeviceBatch,
 )
 from .layout import SymMatrix, approx_error_bound
@@ -138,11 +138,31 @@ class LoopOutcome:
         self.__dict__.update(kw)
 
 
+def _stall_thresholds(controller: RankController, n: int, K: int) -> np.ndarray:
+    """Smallest combined residual at which the stall rule (reference
+    ``lowrank.py:64-69,181``) would fire at each of the next K steps: step j
+    compares against the value ell steps back, already in the window when
+    K <= ell; +inf where the rule cannot fire."""
+    thr = np.full(K, np.inf)
+    if controller.r >= n:
+        return thr
+    h = controller.history
+    L, ell = len(h), controller.ell
+    for j in range(K):
+        if L + j + 1 >= ell + 1:
+            thr[j] = h[L + j - ell]
+    return thr
+
+
 def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverConfig,
                 alpha: float, callback: ProgressCallback | None = None,
-                t0: float | None = None) -> LoopOutcome:
+                t0: float | None = None, chunk: int = KMAX) -> LoopOutcome:
     """The ``for k`` loop of reference ``lowrank.py:125-190`` on a resident
-    instance: one device call per iteration, scalars back, host decisions."""
+    instance.  Iterations run on the device in chunks of up to ``chunk``; the
+    device pauses at the first step where a convergence check, a stall or a
+    divergence can fire, and the host then applies the reference's control
+    logic to every executed step in order -- so every decision is taken at the
+    same iteration, on the same scalars, as with one call per iteration."""
     t0 = time.perf_counter() if t0 is None else t0
     n = prob.n
     eps_lambda = (config.eps_lambda if config.eps_lambda is not None
@@ -156,57 +176,73 @@ def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverC
     res = (math.nan, math.nan, math.nan)
     scale = 1.0
     eig_passes = eig_matvecs = eig_unconverged = 0
-    for k in range(1, config.max_iter + 1):
-        out = batch.iterate([inst], [controller.r], [it.ypar])[0]
-        eig_passes += int(out[OUT_PASSES])
-        eig_matvecs += int(out[OUT_MATVECS])
-        if out[OUT_FINITE] == 1.0:
-            ec = float(out[OUT_EPS_P]) + float(out[OUT_EPS_D])
-            sc = (1.0 + ec) if (k == 1 and config.relative_residuals) else scale
-            if ec <= config.eps_tol * sc:
-                # checkpoint iteration: the certificate needs lambda_{r+1} to the
-                # reference's accuracy; re-run this iteration from the same
-                # (X_k, y_k) with the certificate eigenpair converged too
-                out = batch.iterate([inst], [controller.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
-                eig_passes += int(out[OUT_PASSES])
-                eig_matvecs += int(out[OUT_MATVECS])
-        if out[OUT_EIGCONV] == 0:
-            eig_unconverged += 1
-            logger.info("eigensolver hit its pass limit at k=%d (r=%d)", k, controller.r)
-        if out[OUT_FINITE] != 1.0:                       # _finite, lowrank.py:145-147
-            status = SolveStatus.DIVERGED
-            it.which = 1
-            break
-        it.k = k                                         # state.advance, pdhg.py:113-118
-        it.ypar ^= 1
-        it.which = 0
-        lambda_r = float(out[OUT_LAMBDA])
-        controller.last_lambda_r = lambda_r
-        ep, ed = float(out[OUT_EPS_P]), float(out[OUT_EPS_D])
-        res = (ep, ed, ep + ed)
-        controller.history.append(res[2])
-        if k == 1 and config.relative_residuals:
-            scale = 1.0 + res[2]
-        if callback is not None and k % config.progress_every == 0:
-            callback(ProgressInfo(k, *res, controller.r, it.objective()))
-        if res[2] <= config.eps_tol * scale:
-            Xc = it.X()
-            controller.checkpoints.append(
-                Checkpoint(controller.r, Xc, it.y(), prob.C.inner(Xc)))
-            if rank_certificate_satisfied(n, controller.r, lambda_r, eps_lambda):
-                status = SolveStatus.OPTIMAL
+    k = 1
+    while k <= config.max_iter and status is None:
+        # chunk length: the first iteration alone (it fixes the relative
+        # scale); never across a progress callback; at most window_ell
+        K = 1 if k == 1 else min(chunk, config.max_iter - k + 1, controller.ell)
+        if callback is not None:
+            K = min(K, config.progress_every - (k - 1) % config.progress_every)
+        conv = config.eps_tol * scale if k > 1 else -1.0
+        stall = _stall_thresholds(controller, n, K)
+        outs, done = batch.iterate_many([inst], [controller.r], [it.ypar], K, [conv], stall)
+        outs, done = outs[0], int(done[0])
+        for j in range(done):
+            out = outs[j]
+            eig_passes += int(out[OUT_PASSES])
+            eig_matvecs += int(out[OUT_MATVECS])
+            if out[OUT_FINITE] == 1.0:
+                ec = float(out[OUT_EPS_P]) + float(out[OUT_EPS_D])
+                sc = (1.0 + ec) if (k == 1 and config.relative_residuals) else scale
+                if ec <= config.eps_tol * sc:
+                    # checkpoint iteration: the certificate needs lambda_{r+1} to the
+                    # reference's accuracy; re-run this iteration from the same
+                    # (X_k, y_k) with the certificate eigenpair converged too
+                    assert j == done - 1, "device chunk ran past a checkpoint"
+                    out = batch.iterate([inst], [controller.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
+                    eig_passes += int(out[OUT_PASSES])
+                    eig_matvecs += int(out[OUT_MATVECS])
+            if out[OUT_EIGCONV] == 0:
+                eig_unconverged += 1
+                logger.info("eigensolver hit its pass limit at k=%d (r=%d)", k, controller.r)
+            if out[OUT_FINITE] != 1.0:                   # _finite, lowrank.py:145-147
+                status = SolveStatus.DIVERGED
+                it.which = 1
                 break
-            logger.debug("converged at rank %d but certificate %.3e > %.3e; doubling",
-                         controller.r, approx_error_bound(n, controller.r, lambda_r), eps_lambda)
-            update_rank(controller, n)
-            rank_path.append((k, controller.r))
-        elif controller.r < n and stall_detected(controller.history, controller.ell):
-            logger.debug("stalled at rank %d after %d iterations; doubling", controller.r, k)
-            update_rank(controller, n)
-            rank_path.append((k, controller.r))
-        if time.perf_counter() - t0 > config.time_limit_s:
+            it.k = k                                     # state.advance, pdhg.py:113-118
+            it.ypar ^= 1
+            it.which = 0
+            lambda_r = float(out[OUT_LAMBDA])
+            controller.last_lambda_r = lambda_r
+            ep, ed = float(out[OUT_EPS_P]), float(out[OUT_EPS_D])
+            res = (ep, ed, ep + ed)
+            controller.history.append(res[2])
+            if k == 1 and config.relative_residuals:
+                scale = 1.0 + res[2]
+            if callback is not None and k % config.progress_every == 0:
+                callback(ProgressInfo(k, *res, controller.r, it.objective()))
+            if res[2] <= config.eps_tol * scale:
+                Xc = it.X()
+                controller.checkpoints.append(
+                    Checkpoint(controller.r, Xc, it.y(), prob.C.inner(Xc)))
+                if rank_certificate_satisfied(n, controller.r, lambda_r, eps_lambda):
+                    status = SolveStatus.OPTIMAL
+                    break
+                logger.debug("converged at rank %d but certificate %.3e > %.3e; doubling",
+                             controller.r, approx_error_bound(n, controller.r, lambda_r), eps_lambda)
+                update_rank(controller, n)
+                rank_path.append((k, controller.r))
+                assert j == done - 1, "device chunk ran past a rank change"
+            elif controller.r < n and stall_detected(controller.history, controller.ell):
+                logger.debug("stalled at rank %d after %d iterations; doubling", controller.r, k)
+                update_rank(controller, n)
+                rank_path.append((k, controller.r))
+                assert j == done - 1, "device chunk ran past a stall"
+            k += 1
+        # time limit: checked at chunk granularity (the device pauses only at
+        # algorithmic events)
+        if status is None and time.perf_counter() - t0 > config.time_limit_s:
             status = SolveStatus.TIME_LIMIT
-            break
     if status is None:
         status = SolveStatus.MAX_ITERATIONS
     return LoopOutcome(status=status, it=it, res=res, rank_path=rank_path, controller=controller,
