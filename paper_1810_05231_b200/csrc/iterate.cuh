@@ -467,7 +467,7 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
 
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
 inline size_t iterate_smem_bytes(int lds, int zcap, int ycap) {
-  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 11 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap) * sizeof(double) +
+  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 13 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap) * sizeof(double) +
          (size_t)(3 * PDSDP_BMAX + 8 + zcap) * sizeof(int) + 64;
 }
 
@@ -511,7 +511,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.A = p; p += sq; s.Q = p; p += sq; s.L = p; p += sq; s.M = p; p += sq; s.T = p; p += sq;
     s.scr = p; p += PDSDP_NTHR;
     s.theta = p; p += PDSDP_BMAX; s.res = p; p += PDSDP_BMAX; s.lamF = p; p += PDSDP_BMAX;
-    s.lamN = p; p += PDSDP_BMAX; s.dsc = p; p += PDSDP_BMAX; s.cs = p; p += 2 * PDSDP_BMAX;
+    s.lamN = p; p += PDSDP_BMAX; s.dsc = p; p += PDSDP_BMAX; s.cs = p; p += 4 * PDSDP_BMAX;
     s.red1 = p; p += 4 * PDSDP_BMAX;
     s.gsc = p; p += PDSDP_GRAM_SCR;
     s.ys = p; p += ycap;
@@ -698,7 +698,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
-    bool okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
+    bool okc = chol_scaled_1s(s.A, b, lds, s.dsc);
     if (!okc) {
       // breakdown: the filtered block lost rank; retry from V with half the degree
       if (++fails >= 8 || m == 0) break;
@@ -707,7 +707,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       continue;
     }
     prof_mark(pf, 9);
-    tri_inv_lower(s.A, s.L, b, lds);
+    tri_inv_lower_1s(s.A, s.L, b, lds);
     for (int e = tid; e < b * b; e += blockDim.x) {
       int i = e / b, j = e % b;
       s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
@@ -735,7 +735,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe
     prof_mark(pf, 8);
-    okc = chol_scaled(s.A, b, lds, s.dsc, s.flag);
+    okc = chol_scaled_1s(s.A, b, lds, s.dsc);
     if (!okc) {
       if (++fails >= 8 || m == 0) break;
       force_m = m / 2;
@@ -743,7 +743,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     if (nlock == 0) msucc += m;
     prof_mark(pf, 9);
-    tri_inv_lower(s.A, s.L, b, lds);            // L = L2^-1
+    tri_inv_lower_1s(s.A, s.L, b, lds);            // L = L2^-1
     prof_mark(pf, 10);
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
@@ -770,23 +770,25 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     prof_mark(pf, 11);
     // pairs among the trailing guard columns only need loose accuracy (their
     // Ritz pairs are not used; residuals are recomputed honestly below)
-    jacobi_eig(s.A, s.Q, b, lds, s.cs, s.pq, s.flag, need_cert ? b : min(b, r + 1));
+    double *Aj, *Qj;
+    jacobi_eig2(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     prof_mark(pf, 12);
     if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];
-    sort_desc(s.A, b, lds, s.theta, s.perm);
-    // B = D L^-T Q[:, perm]  -> s.M
+    sort_desc(Aj, b, lds, s.theta, s.perm);
+    // B = D L^-T Q[:, perm]  -> the Jacobi scratch that does not hold Q
+    double* Bm = (Qj == s.Q) ? s.M : s.Q;
     for (int e = tid; e < b * b; e += blockDim.x) {
       int i = e / b, j = e % b;
       const int pj = s.perm[j];
       double acc = 0.0;
-      for (int t = i; t < b; ++t) acc += s.L[t * lds + i] * s.Q[t * lds + pj];
-      s.M[i * lds + j] = s.dsc[i] * acc;
+      for (int t = i; t < b; ++t) acc += s.L[t * lds + i] * Qj[t * lds + pj];
+      Bm[i * lds + j] = s.dsc[i] * acc;
     }
     __syncthreads();
     // V = Y1 B ; AV = W1 B  (AV goes to buf[iw], which becomes the AV buffer)
     prof_mark(pf, 5);
-    rotate_rows(d, x, buf[iav], s.M, lds, d.V, b);
-    rotate_rows(d, x, buf[iw1], s.M, lds, buf[iw], b);
+    rotate_rows(d, x, buf[iav], Bm, lds, d.V, b);
+    rotate_rows(d, x, buf[iw1], Bm, lds, buf[iw], b);
     iav = iw;
     av_valid = true;
     theta_valid = true;

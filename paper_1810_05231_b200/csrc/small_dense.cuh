@@ -296,4 +296,455 @@ __device__ int jacobi_eig_warp(double* A, double* Q, int b, int lds, double* cs,
   return sweeps;
 }
 
+
+// ---------------------------------------------------------------------------
+// One-barrier-per-step variants (all threads of the CTA).
+
+// Scaled Cholesky with a single __syncthreads per column: step j updates the
+// trailing columns from the (final) column j without normalising it; the
+// normalisation happens once at the end.  Same contract as chol_scaled.
+__device__ bool chol_scaled_1s(double* G, int b, int lds, double* dsc) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < b; i += nt) {
+    const double g = G[i * lds + i];
+    dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    G[i * lds + j] = (j <= i) ? G[i * lds + j] * dsc[i] * dsc[j] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    const double djj = G[j * lds + j];
+    if (!(djj > 1e-28)) { __syncthreads(); return false; }
+    const double inv = 1.0 / djj;
+    const int rem = b - j - 1;
+    for (int e = tid; e < rem * rem; e += nt) {
+      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+      if (k <= i) G[i * lds + k] -= G[i * lds + j] * G[k * lds + j] * inv;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    if (j <= i) {
+      const double sj = sqrt(G[j * lds + j]);
+      if (i != j) G[i * lds + j] = G[i * lds + j] / sj;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < b; j += nt) G[j * lds + j] = sqrt(G[j * lds + j]);
+  __syncthreads();
+  return true;
+}
+
+// X = L^{-1} (lower) by row elimination, one barrier per row.
+__device__ void tri_inv_lower_1s(const double* L, double* X, int b, int lds) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < b * b; e += nt) X[(e / b) * lds + (e % b)] = (e / b == e % b) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int kk = 0; kk < b - 1; ++kk) {
+    const double lkk = L[kk * lds + kk];
+    const int rows = b - kk - 1, cols = kk + 1;
+    for (int e = tid; e < rows * cols; e += nt) {
+      const int i = kk + 1 + e / cols, c = e % cols;
+      X[i * lds + c] -= L[i * lds + kk] * (X[kk * lds + c] / lkk);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, c = e % b;
+    X[i * lds + c] = (c <= i) ? X[i * lds + c] / L[i * lds + i] : 0.0;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int jac_partner(int i, int t, int bb) {
+  if (i == 0) return 1 + (bb - 2 + t) % (bb - 1);
+  const int u = 1 + (((i - 1 - t) % (bb - 1)) + (bb - 1)) % (bb - 1);
+  const int v = bb - 1 - u;
+  return (v == 0) ? 0 : 1 + (v - 1 + t) % (bb - 1);
+}
+
+__device__ __forceinline__ void jac_rot(double app, double aqq, double apq, double thr, double& c, double& s) {
+  c = 1.0; s = 0.0;
+  if (fabs(apq) > thr) {
+    const double tau = (aqq - app) / (2.0 * apq);
+    double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+    if (!isfinite(tau)) t = 0.0;
+    c = rsqrt(1.0 + t * t);
+    s = t * c;
+  }
+}
+
+// Cyclic two-sided Jacobi with one __syncthreads per round: every thread
+// forms its elements of J^T A J and Q J in one pass (ping-pong buffers), and
+// the threads owning the entries of next round's pairs form next round's
+// rotations directly.  Same thresholds as jacobi_eig.  On return *Aout / *Qout
+// point at the buffers holding the diagonalised matrix and the eigenvectors;
+// sflag[0] = sweeps.
+__device__ void jacobi_eig_1s(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* csn,
+                              int* sflag, int nimp, double** Aout, double** Qout) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double fro_part[32];
+  double f = 0.0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
+    const double v = A[i * lds + j];
+    f = fma(v, v, f);
+  }
+  f = warp_sum(f);
+  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
+  __syncthreads();
+  double fro = 0.0;
+  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
+  fro = sqrt(fro);
+  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  *Aout = A; *Qout = Q;
+  if (tid == 0) sflag[0] = 0;
+  if (b == 1) { __syncthreads(); return; }
+  const int bb = b + (b & 1);
+  // rotation tables indexed by the smaller index p of a pair: csn[2][2*BMAX]
+  double* cur = csn;
+  double* nxt = csn + 2 * PDSDP_BMAX;
+  // rotations of round 0
+  int any = 0;
+  for (int p = tid; p < b; p += nt) {
+    const int q = jac_partner(p, 0, bb);
+    double c = 1.0, sn = 0.0;
+    if (p < q && q < b) jac_rot(A[p * lds + p], A[q * lds + q], A[p * lds + q], (p < nimp) ? thr_imp : thr_guard, c, sn);
+    if (sn != 0.0) any = 1;
+    cur[2 * p] = c; cur[2 * p + 1] = sn;
+  }
+  any = __syncthreads_or(any);
+  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
+  int sweeps = 0, sweep_any = any;
+  for (int it = 0; it < 40 * (bb - 1); ++it) {
+    const int t = it % (bb - 1);
+    const int t1 = (t + 1) % (bb - 1);
+    int nany = 0;
+    for (int e = tid; e < 2 * b * b; e += nt) {
+      const bool isQ = e >= b * b;
+      const int ee = isQ ? e - b * b : e;
+      const int i = ee / b, j = ee % b;
+      // column coefficients (J[.][j])
+      const int pj = jac_partner(j, t, bb);
+      double cj0 = 1.0, cj1 = 0.0;       // J[j][j], J[pj][j]
+      if (pj < b) {
+        const int pp = min(j, pj);
+        const double c = cur[2 * pp], sn = cur[2 * pp + 1];
+        cj0 = c;
+        cj1 = (j == pp) ? -sn : sn;
+      }
+      if (isQ) {
+        const double v = cj0 * Qc[i * lds + j] + ((pj < b) ? cj1 * Qc[i * lds + pj] : 0.0);
+        Qn[i * lds + j] = v;
+        continue;
+      }
+      const int pi = jac_partner(i, t, bb);
+      double ri0 = 1.0, ri1 = 0.0;       // J[i][i], J[pi][i]
+      if (pi < b) {
+        const int pp = min(i, pi);
+        const double c = cur[2 * pp], sn = cur[2 * pp + 1];
+        ri0 = c;
+        ri1 = (i == pp) ? -sn : sn;
+      }
+      auto elem = [&](int ii, int jj) {
+        const int pii = jac_partner(ii, t, bb), pjj = jac_partner(jj, t, bb);
+        double a0 = 1.0, a1 = 0.0, b0 = 1.0, b1 = 0.0;
+        if (pii < b) { const int pp = min(ii, pii); a0 = cur[2 * pp]; a1 = (ii == pp) ? -cur[2 * pp + 1] : cur[2 * pp + 1]; }
+        if (pjj < b) { const int pp = min(jj, pjj); b0 = cur[2 * pp]; b1 = (jj == pp) ? -cur[2 * pp + 1] : cur[2 * pp + 1]; }
+        double v = a0 * (b0 * Ac[ii * lds + jj] + ((pjj < b) ? b1 * Ac[ii * lds + pjj] : 0.0));
+        if (pii < b) v += a1 * (b0 * Ac[pii * lds + jj] + ((pjj < b) ? b1 * Ac[pii * lds + pjj] : 0.0));
+        if (pii == jj && pii < b) {
+          const int pp = min(ii, pii);
+          if (cur[2 * pp + 1] != 0.0) v = 0.0;       // the rotated pair is annihilated
+        }
+        return v;
+      };
+      (void)ri0; (void)ri1;
+      const double v = elem(i, j);
+      An[i * lds + j] = v;
+      // owner of next round's pair (p', q') with p' = i < q' = j forms its rotation
+      const int q1 = jac_partner(i, t1, bb);
+      if (j == q1 && i < j) {
+        const double app = elem(i, i), aqq = elem(j, j);
+        double c, sn;
+        jac_rot(app, aqq, v, (i < nimp) ? thr_imp : thr_guard, c, sn);
+        nxt[2 * i] = c; nxt[2 * i + 1] = sn;
+        if (sn != 0.0) nany = 1;
+      }
+    }
+    // indices whose next partner is the dummy (odd b) or >= b: no rotation
+    for (int p = tid; p < b; p += nt) {
+      const int q = jac_partner(p, t1, bb);
+      if (q >= b && p < q) { nxt[2 * p] = 1.0; nxt[2 * p + 1] = 0.0; }
+    }
+    nany = __syncthreads_or(nany);
+    { double* tmp = Ac; Ac = An; An = tmp; tmp = Qc; Qc = Qn; Qn = tmp; tmp = cur; cur = nxt; nxt = tmp; }
+    if (t == bb - 2) {                  // a full sweep finished
+      ++sweeps;
+      if (!sweep_any) break;
+      sweep_any = nany;                 // rotations already decided for the next sweep's round 0
+    } else {
+      sweep_any |= nany;
+    }
+  }
+  *Aout = Ac; *Qout = Qc;
+  if (tid == 0) sflag[0] = sweeps;
+  __syncthreads();
+}
+
+
+// Fast, deterministic FP64 reciprocal / reciprocal square root: hardware
+// approximation + Newton steps (full double accuracy to within a few ulp).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r;
+}
+
+// Two-barrier-per-round cyclic Jacobi: (1) one thread per pair forms the
+// rotation from a precomputed pairing table, (2) every thread forms its
+// elements of J^T A J and Q J in one pass into ping-pong buffers.  The
+// rotation only needs to be an exact orthogonal matrix (c^2 + s^2 = 1 to
+// rounding); residual off-diagonals are removed by later sweeps.
+// Thresholds as jacobi_eig.  tab: >= (bb-1) * bb ints of scratch.
+__device__ void jacobi_eig2(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
+                            int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double fro_part[32];
+  double f = 0.0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
+    const double v = A[i * lds + j];
+    f = fma(v, v, f);
+  }
+  f = warp_sum(f);
+  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
+  const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
+  // pairing table: tab[t * bb + i] = partner of i in round t (>= b: none)
+  for (int e = tid; e < R * bb; e += nt) {
+    const int t = e / bb, j = e % bb;
+    if (j < np) {
+      const int t0 = j, t1 = bb - 1 - j;
+      const int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + t) % R;
+      const int q = 1 + (t1 - 1 + t) % R;
+      tab[t * bb + p] = q;
+      tab[t * bb + q] = p;
+    }
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
+  fro = sqrt(fro);
+  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
+  int sweeps = 0;
+  if (b > 1) {
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      int any = 0;
+      for (int t = 0; t < R; ++t) {
+        const int* pt = tab + t * bb;
+        // (1) rotations, indexed by the smaller index of each pair
+        for (int p = tid; p < b; p += nt) {
+          const int q = pt[p];
+          if (p < q) {
+            double c = 1.0, sn = 0.0;
+            if (q < b) {
+              const double apq = Ac[p * lds + q];
+              if (fabs(apq) > ((p < nimp) ? thr_imp : thr_guard)) {
+                const double tau = (Ac[q * lds + q] - Ac[p * lds + p]) * fast_rcp(2.0 * apq);
+                const double at = fabs(tau);
+                double tt;
+                if (at < 1e150) {
+                  const double u = fma(tau, tau, 1.0);
+                  tt = fast_rcp(at + u * fast_rsqrt(u));
+                } else {
+                  tt = 0.5 * fast_rcp(at);
+                }
+                tt = (tau >= 0.0) ? tt : -tt;
+                if (!isfinite(tau)) tt = 0.0;
+                c = fast_rsqrt(fma(tt, tt, 1.0));
+                sn = tt * c;
+                if (sn != 0.0) any = 1;
+              }
+            }
+            cs[2 * p] = c;
+            cs[2 * p + 1] = sn;
+          }
+        }
+        __syncthreads();
+        // (2) A' = J^T A J and Q' = Q J, element-wise
+        for (int e = tid; e < 2 * b * b; e += nt) {
+          const bool isQ = e >= b * b;
+          const int ee = isQ ? e - b * b : e;
+          const int i = ee / b, j = ee % b;
+          const int pj = pt[j];
+          double b0 = 1.0, b1 = 0.0;
+          if (pj < b) {
+            const int pp = min(j, pj);
+            b0 = cs[2 * pp];
+            b1 = (j == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
+          }
+          if (isQ) {
+            double v = b0 * Qc[i * lds + j];
+            if (pj < b) v = fma(b1, Qc[i * lds + pj], v);
+            Qn[i * lds + j] = v;
+            continue;
+          }
+          const int pi = pt[i];
+          double a0 = 1.0, a1 = 0.0;
+          if (pi < b) {
+            const int pp = min(i, pi);
+            a0 = cs[2 * pp];
+            a1 = (i == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
+          }
+          double v = b0 * Ac[i * lds + j];
+          if (pj < b) v = fma(b1, Ac[i * lds + pj], v);
+          v *= a0;
+          if (pi < b) {
+            double w = b0 * Ac[pi * lds + j];
+            if (pj < b) w = fma(b1, Ac[pi * lds + pj], w);
+            v = fma(a1, w, v);
+            if (pi == j && cs[2 * min(i, pi) + 1] != 0.0) v = 0.0;   // annihilated pair
+          }
+          An[i * lds + j] = v;
+        }
+        __syncthreads();
+        { double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp; }
+      }
+      ++sweeps;
+      if (!__syncthreads_or(any)) break;
+    }
+  }
+  *Aout = Ac; *Qout = Qc;
+  if (tid == 0) sflag[0] = sweeps;
+  __syncthreads();
+}
+
+
+// Same as jacobi_eig2, executed by warp 0 alone (warp-synchronous).
+__device__ void jacobi_eig2_warp(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
+                            int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
+  const int tid = threadIdx.x & 31, nt = 32;
+  double f = 0.0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
+    const double v = A[i * lds + j];
+    f = fma(v, v, f);
+  }
+  f = warp_sum(f);
+  const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
+  // pairing table: tab[t * bb + i] = partner of i in round t (>= b: none)
+  for (int e = tid; e < R * bb; e += nt) {
+    const int t = e / bb, j = e % bb;
+    if (j < np) {
+      const int t0 = j, t1 = bb - 1 - j;
+      const int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + t) % R;
+      const int q = 1 + (t1 - 1 + t) % R;
+      tab[t * bb + p] = q;
+      tab[t * bb + q] = p;
+    }
+  }
+  __syncwarp();
+  const double fro = sqrt(f);
+  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
+  int sweeps = 0;
+  if (b > 1) {
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      int any = 0;
+      for (int t = 0; t < R; ++t) {
+        const int* pt = tab + t * bb;
+        // (1) rotations, indexed by the smaller index of each pair
+        for (int p = tid; p < b; p += nt) {
+          const int q = pt[p];
+          if (p < q) {
+            double c = 1.0, sn = 0.0;
+            if (q < b) {
+              const double apq = Ac[p * lds + q];
+              if (fabs(apq) > ((p < nimp) ? thr_imp : thr_guard)) {
+                const double tau = (Ac[q * lds + q] - Ac[p * lds + p]) * fast_rcp(2.0 * apq);
+                const double at = fabs(tau);
+                double tt;
+                if (at < 1e150) {
+                  const double u = fma(tau, tau, 1.0);
+                  tt = fast_rcp(at + u * fast_rsqrt(u));
+                } else {
+                  tt = 0.5 * fast_rcp(at);
+                }
+                tt = (tau >= 0.0) ? tt : -tt;
+                if (!isfinite(tau)) tt = 0.0;
+                c = fast_rsqrt(fma(tt, tt, 1.0));
+                sn = tt * c;
+                if (sn != 0.0) any = 1;
+              }
+            }
+            cs[2 * p] = c;
+            cs[2 * p + 1] = sn;
+          }
+        }
+        __syncwarp();
+        // (2) A' = J^T A J and Q' = Q J, element-wise
+        for (int e = tid; e < 2 * b * b; e += nt) {
+          const bool isQ = e >= b * b;
+          const int ee = isQ ? e - b * b : e;
+          const int i = ee / b, j = ee % b;
+          const int pj = pt[j];
+          double b0 = 1.0, b1 = 0.0;
+          if (pj < b) {
+            const int pp = min(j, pj);
+            b0 = cs[2 * pp];
+            b1 = (j == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
+          }
+          if (isQ) {
+            double v = b0 * Qc[i * lds + j];
+            if (pj < b) v = fma(b1, Qc[i * lds + pj], v);
+            Qn[i * lds + j] = v;
+            continue;
+          }
+          const int pi = pt[i];
+          double a0 = 1.0, a1 = 0.0;
+          if (pi < b) {
+            const int pp = min(i, pi);
+            a0 = cs[2 * pp];
+            a1 = (i == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
+          }
+          double v = b0 * Ac[i * lds + j];
+          if (pj < b) v = fma(b1, Ac[i * lds + pj], v);
+          v *= a0;
+          if (pi < b) {
+            double w = b0 * Ac[pi * lds + j];
+            if (pj < b) w = fma(b1, Ac[pi * lds + pj], w);
+            v = fma(a1, w, v);
+            if (pi == j && cs[2 * min(i, pi) + 1] != 0.0) v = 0.0;   // annihilated pair
+          }
+          An[i * lds + j] = v;
+        }
+        __syncwarp();
+        { double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp; }
+      }
+      ++sweeps;
+      if (!__any_sync(0xffffffffu, any)) break;
+    }
+  }
+  *Aout = Ac; *Qout = Qc;
+  if (tid == 0) sflag[0] = sweeps;
+  __syncwarp();
+}
+
 }  // namespace pdsdp
