@@ -102,6 +102,8 @@ struct Inst {
   int* stopf;          // device flag: an event may fire, skip the remaining steps
 };
 
+static_assert(sizeof(Inst) % 8 == 0, "Inst is copied as 8-byte words");
+
 // Per-launch control for one instance.
 struct Ctl {
   int r;       // target rank for this iteration

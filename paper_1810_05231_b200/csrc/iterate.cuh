@@ -54,6 +54,9 @@ struct Sm {
   double *A, *Q, *L, *M, *T;   // lds x lds each
   double *gsc;                 // PDSDP_GRAM_SCR
   double* ys;                  // staged operand block (n x ycw)
+  double *SF, *SYc, *SYp;      // own rows of F, Y_j, Y_{j-1} (smem-resident filter state)
+  int* szp;                    // own rows of zptr
+  int own, sld;                // own-row buffers valid; their stride
   int ycw;                     // staged column chunk width (even; 0 = gather path)
   const int* zc;               // staged Z columns of own rows
   const double* zvs;           // staged Z values of own rows
@@ -140,7 +143,7 @@ __device__ void gram_partial(const double* __restrict__ A, int na, const double*
   }
 }
 
-#define PDSDP_GRAM_SCR 4096     // doubles of smem for the cross-warp Gram reduction
+#define PDSDP_GRAM_SCR 2048     // doubles of smem for the cross-warp Gram reduction
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -151,59 +154,72 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // on FP64 tensor cores: warps take (tile group, row chunk) work items, each
 // accumulating up to four 8x8 DMMA tiles over its rows (k = 4 rows per
 // mma.m8n8k4); chunks are then added in a fixed order through shared memory.
-__device__ void gram_mma(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
-                         int ld, int r0, int r1, double* gout, double* wsm) {
+__device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const double* __restrict__ B, int ldb,
+                          int nb, int r0, int r1, double* gout, double* wsm);
+
+__device__ __forceinline__ void gram_mma(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
+                                         int ld, int r0, int r1, double* gout, double* wsm) {
+  gram_mma2(A, ld, na, B, ld, nb, r0, r1, gout, wsm);
+}
+
+__device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const double* __restrict__ B, int ldb,
+                          int nb, int r0, int r1, double* gout, double* wsm) {
   const int q = na * nb;
   if (q == 0) return;
   const int mt = (na + 7) >> 3, ntl = (nb + 7) >> 3, tiles = mt * ntl;
   const int NG = (tiles + 3) >> 2;
   const int nw = blockDim.x >> 5;
-  // partial tiles live in wsm (PDSDP_GRAM_SCR doubles = 16 work items of 4 tiles)
-  const int chunks = max(1, min(nw, PDSDP_GRAM_SCR / 256) / NG);
+  const int cap = PDSDP_GRAM_SCR / 256;          // work items whose partial tiles fit in wsm
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int nrows = r1 - r0;
-  const int clen = (((nrows + chunks - 1) / chunks) + 3) & ~3;
-  for (int wk = warp; wk < NG * chunks; wk += nw) {
-    const int grp = wk % NG, ch = wk / NG;
-    const int ra = r0 + ch * clen, rb = min(r1, ra + clen);
-    double acc[4][2];
-    int ti[4], tj[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      acc[t][0] = 0.0; acc[t][1] = 0.0;
-      const int tt = grp * 4 + t;
-      ti[t] = (tt < tiles) ? (tt / ntl) * 8 + g : 1 << 30;
-      tj[t] = (tt < tiles) ? (tt % ntl) * 8 + g : 1 << 30;
-    }
-    for (int rho0 = ra; rho0 < rb; rho0 += 4) {
-      const int rho = rho0 + tq;
-      const bool rv = rho < rb;
-      double av[4], bv[4];
+  for (int g0 = 0; g0 < NG; g0 += cap) {
+    const int ng = min(cap, NG - g0);
+    const int chunks = max(1, min(nw, cap) / ng);
+    const int clen = (((nrows + chunks - 1) / chunks) + 3) & ~3;
+    for (int wk = warp; wk < ng * chunks; wk += nw) {
+      const int grp = g0 + wk % ng, ch = wk / ng;
+      const int ra = r0 + ch * clen, rb = min(r1, ra + clen);
+      double acc[4][2];
+      int ti[4], tj[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        av[t] = (rv && ti[t] < na) ? A[(size_t)rho * ld + ti[t]] : 0.0;
-        bv[t] = (rv && tj[t] < nb) ? B[(size_t)rho * ld + tj[t]] : 0.0;
+        acc[t][0] = 0.0; acc[t][1] = 0.0;
+        const int tt = grp * 4 + t;
+        ti[t] = (tt < tiles) ? (tt / ntl) * 8 + g : 1 << 30;
+        tj[t] = (tt < tiles) ? (tt % ntl) * 8 + g : 1 << 30;
+      }
+      for (int rho0 = ra; rho0 < rb; rho0 += 4) {
+        const int rho = rho0 + tq;
+        const bool rv = rho < rb;
+        double av[4], bv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          av[t] = (rv && ti[t] < na) ? A[(size_t)rho * lda + ti[t]] : 0.0;
+          bv[t] = (rv && tj[t] < nb) ? B[(size_t)rho * ldb + tj[t]] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma884(acc[t][0], acc[t][1], av[t], bv[t]);
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) dmma884(acc[t][0], acc[t][1], av[t], bv[t]);
+      for (int t = 0; t < 4; ++t) {
+        double* w = wsm + ((size_t)(ch * ng + (grp - g0)) * 4 + t) * 64 + g * 8 + 2 * tq;
+        w[0] = acc[t][0];
+        w[1] = acc[t][1];
+      }
     }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      double* w = wsm + ((size_t)(ch * NG + grp) * 4 + t) * 64 + g * 8 + 2 * tq;
-      w[0] = acc[t][0];
-      w[1] = acc[t][1];
+    __syncthreads();
+    for (int o = threadIdx.x; o < q; o += blockDim.x) {
+      const int i = o / nb, j = o % nb;
+      const int t = (i >> 3) * ntl + (j >> 3);
+      const int grp = t >> 2;
+      if (grp < g0 || grp >= g0 + ng) continue;
+      const int slot = t & 3, el = (i & 7) * 8 + (j & 7);
+      double sum = 0.0;
+      for (int ch = 0; ch < chunks; ++ch) sum += wsm[((size_t)(ch * ng + (grp - g0)) * 4 + slot) * 64 + el];
+      gout[o] = sum;
     }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int o = threadIdx.x; o < q; o += blockDim.x) {
-    const int i = o / nb, j = o % nb;
-    const int t = (i >> 3) * ntl + (j >> 3);
-    const int grp = t >> 2, slot = t & 3, el = (i & 7) * 8 + (j & 7);
-    double sum = 0.0;
-    for (int ch = 0; ch < chunks; ++ch) sum += wsm[((size_t)(ch * NG + grp) * 4 + slot) * 64 + el];
-    gout[o] = sum;
-  }
-  __syncthreads();
 }
 
 // column sums of squares of (P[:, j] - th[j] * Q[:, j]) over own rows
@@ -404,6 +420,97 @@ __device__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* 
   else apply_rows(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
 }
 
+// Operator step with the CTA's rows resident in shared memory: the Gram
+// partial reads F and Y_j from smem, the operand block is staged for all n
+// rows, and the result is written both to global (for the other CTAs) and
+// into the Y_{j-1} smem slot, which becomes Y_{j+1} (caller swaps SYc/SYp).
+__device__ void operator_step_own(const Inst& d, Cta& x, Sm& s, const double* zv, const double* Yin,
+                                  double* out, int c0, int bc, int rF, int nlock, double ca, double cb,
+                                  double cd, Prof& pf) {
+  prof_mark(pf, 1);
+  const int nl = x.r1 - x.r0, sl = s.sld, ld = d.ld, n = d.n, tid = threadIdx.x;
+  double* slot = red_slot(d, x, x.c);
+  gram_mma2(s.SF, sl, rF, s.SYc + c0, sl, bc, 0, nl, slot, s.gsc);
+  gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, s.SYc + c0, sl, bc, 0, nl, slot + rF * bc, s.gsc);
+  prof_mark(pf, 2);
+  cg::this_cluster().sync();                 // publishes Yin and the partials
+  double* ys = s.ys;
+  const int cw = s.ycw;
+  const int a0 = c0 & ~1, a1 = c0 + bc;
+  const int pairs = cw >> 1;
+  // first operand chunk in flight while the partials are summed
+  const float inv_pairs = 1.0f / (float)pairs;
+  for (int idx = tid; idx < n * pairs; idx += blockDim.x) {
+    const int row = (int)(((float)idx + 0.5f) * inv_pairs), pr = idx - row * pairs;
+    cp_async16(ys + (size_t)row * cw + 2 * pr, Yin + (size_t)row * ld + a0 + 2 * pr);
+  }
+  const int q = (rF + nlock) * bc;
+  for (int i = tid; i < q; i += blockDim.x) {
+    const int l = i / bc;
+    const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
+    const double v = cluster_sum(d, x, i, false);
+    s.T[i] = (c == 0.0) ? 0.0 : v * c;
+  }
+  x.par ^= 1;
+  prof_mark(pf, 3);
+  const double alpha = d.alpha;
+  const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
+  const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
+  const int zoff = s.zstaged ? s.zoff : 0;
+  const int jl = tid & 15, rs = tid >> 4, rstep = blockDim.x >> 4;
+  for (int cs0 = a0; cs0 < a1; cs0 += cw) {
+    if (cs0 != a0) {
+      for (int idx = tid; idx < n * pairs; idx += blockDim.x) {
+        const int row = (int)(((float)idx + 0.5f) * inv_pairs), pr = idx - row * pairs;
+        cp_async16(ys + (size_t)row * cw + 2 * pr, Yin + (size_t)row * ld + cs0 + 2 * pr);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int jlo = max(cs0, c0), jhi = min(cs0 + cw, a1), w_ = jhi - jlo;
+    // thread -> (row slot, column): 16 columns per row pass, 4 slots per round trip
+    for (int cb0 = 0; cb0 < w_; cb0 += 16) {
+      const int jc = cb0 + jl;
+      if (jc >= w_) continue;
+      const int j = jlo + jc, jj = j - c0, js = j - cs0;
+      for (int lr = rs; lr < nl; lr += rstep) {
+        const int e1 = s.szp[lr + 1] - zoff;
+        int e = s.szp[lr] - zoff;
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+        for (; e + 4 <= e1; e += 4) {
+          const int q0 = zcol[e], q1 = zcol[e + 1], q2 = zcol[e + 2], q3 = zcol[e + 3];
+          const double v0 = zval[e], v1 = zval[e + 1], v2 = zval[e + 2], v3 = zval[e + 3];
+          const double y0 = ys[(size_t)q0 * cw + js], y1 = ys[(size_t)q1 * cw + js];
+          const double y2 = ys[(size_t)q2 * cw + js], y3 = ys[(size_t)q3 * cw + js];
+          z0 = fma(v0, y0, z0); z1 = fma(v1, y1, z1); z2 = fma(v2, y2, z2); z3 = fma(v3, y3, z3);
+        }
+        for (; e < e1; ++e) z0 = fma(zval[e], ys[(size_t)zcol[e] * cw + js], z0);
+        const double* Fr = s.SF + (size_t)lr * sl;
+        double w0 = 0.0, w1 = 0.0;
+        int l = 0;
+        for (; l + 2 <= rF; l += 2) {
+          w0 = fma(Fr[l], s.T[l * bc + jj], w0);
+          w1 = fma(Fr[l + 1], s.T[(l + 1) * bc + jj], w1);
+        }
+        if (l < rF) w0 = fma(Fr[l], s.T[l * bc + jj], w0);
+        double w = w0 + w1;
+        if (nlock) {
+          const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
+          for (int t = 0; t < nlock; ++t) w = fma(Vr[t], s.T[(rF + t) * bc + jj], w);
+        }
+        w = fma(-alpha, (z0 + z1) + (z2 + z3), w);
+        double o = ca * w;
+        if (cb != 0.0) o = fma(cb, s.SYc[(size_t)lr * sl + j], o);
+        if (cd != 0.0) o = fma(cd, s.SYp[(size_t)lr * sl + j], o);
+        out[(size_t)(x.r0 + lr) * ld + j] = o;
+        s.SYp[(size_t)lr * sl + j] = o;
+      }
+    }
+    __syncthreads();
+  }
+  double* t = s.SYc; s.SYc = s.SYp; s.SYp = t;
+}
+
 // Convergence state of the Ritz block (identical in every thread).
 struct Assess {
   int last_bad;     // last kept column (< r) still needing work, -1 if none
@@ -466,9 +573,10 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
 }
 
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
-inline size_t iterate_smem_bytes(int lds, int zcap, int ycap) {
-  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 13 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap) * sizeof(double) +
-         (size_t)(3 * PDSDP_BMAX + 8 + zcap) * sizeof(int) + 64;
+inline size_t iterate_smem_bytes(int lds, int zcap, int ycap, int owncap, int nlmax) {
+  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 13 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap + 3 * owncap) *
+             sizeof(double) +
+         (size_t)(3 * PDSDP_BMAX + 8 + zcap + (owncap ? nlmax + 2 : 0)) * sizeof(int) + 64;
 }
 
 __device__ int choose_block(int k, int n) {
@@ -483,7 +591,8 @@ __device__ int choose_block(int k, int n) {
 
 __global__ void __launch_bounds__(PDSDP_NTHR, 1)
 lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,
-                      const int* __restrict__ active, int step, int lcap, int zcap, int ycap) {
+                      const int* __restrict__ active, int step, int lcap, int zcap, int ycap, int owncap,
+                      int nlmax) {
   const int lds = lcap + 1;   // odd stride of the b x b workspaces (no bank conflicts)
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -491,7 +600,17 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   x.C = (int)cl.num_blocks();
   x.c = (int)cl.block_rank();
   const int inst_id = active[blockIdx.x / x.C];
-  const Inst d = insts[inst_id];
+  // the descriptor lives in shared memory: as a local struct it would sit in
+  // (L1-backed) local memory, which every cluster barrier invalidates
+  __shared__ __align__(16) Inst d_sm;
+  {
+    const int nw8 = (int)(sizeof(Inst) / 8);
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(insts + inst_id);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&d_sm);
+    for (int i = threadIdx.x; i < nw8; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const Inst& d = d_sm;
   if (*(volatile int*)d.stopf) return;            // an earlier step of this chunk ended it
   const Ctl ctl = ctls[inst_id * PDSDP_KMAX + step];
   State* st = d.st;
@@ -515,10 +634,12 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.red1 = p; p += 4 * PDSDP_BMAX;
     s.gsc = p; p += PDSDP_GRAM_SCR;
     s.ys = p; p += ycap;
+    s.SF = p; p += owncap; s.SYc = p; p += owncap; s.SYp = p; p += owncap;
     double* zvs = p; p += zcap;
     int* ip = (int*)p;
     s.perm = ip; ip += PDSDP_BMAX; s.pq = ip; ip += 2 * PDSDP_BMAX; s.flag = ip; ip += 8;
     int* zc = ip; ip += zcap;
+    s.szp = ip; ip += (owncap ? nlmax + 2 : 0);
     s.zc = zc; s.zvs = zvs;
     s.zoff = d.zptr[x.r0];
     s.zstaged = (d.zptr[x.r1] - s.zoff) <= zcap ? 1 : 0;
@@ -526,6 +647,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     cw &= ~1;
     if (cw > d.ld) cw = d.ld;
     s.ycw = (cw >= 2) ? cw : 0;
+    s.sld = lcap;
+    s.own = (owncap > 0 && s.ycw >= 2 && (x.r1 - x.r0) * lcap <= owncap && (x.r1 - x.r0) <= nlmax) ? 1 : 0;
   }
   double* buf[5] = {d.V, d.AV, d.Y0, d.Y1, d.Y2};
 
@@ -566,10 +689,13 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       ((double*)s.zvs)[e] = zv[s.zoff + e];
     }
   }
+  if (s.own)
+    for (int lr = tid; lr <= x.r1 - x.r0; lr += blockDim.x) s.szp[lr] = d.zptr[x.r0 + lr];
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
     const int rho = x.r0 + it / b, j = it % b;
     double* Vr = d.V + (size_t)rho * ld;
     if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = (s.lamF[j] != 0.0) ? Vr[j] : 0.0;
+    if (s.own && j < rF) s.SF[(size_t)(rho - x.r0) * s.sld + j] = rerun ? d.F[(size_t)rho * ld + j] : ((s.lamF[j] != 0.0) ? Vr[j] : 0.0);
     if (j >= b_old) Vr[j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
   }
   __syncthreads();
@@ -634,7 +760,54 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     int iyp = -1;                     // buffer holding Y_{j-1}
     int fre[3], nf = 0;
     for (int q = 1; q <= 4; ++q) if (q != iav) fre[nf++] = q;
-    if (m > 0) {
+    if (m > 0 && s.own) {
+      // own rows of V (the recurrence's Y_0) into smem
+      const int nl = x.r1 - x.r0;
+      for (int it = tid; it < nl * bc; it += blockDim.x) {
+        const int lr = it / bc, j = c0 + (it - lr * bc);
+        s.SYc[(size_t)lr * s.sld + j] = d.V[(size_t)(x.r0 + lr) * ld + j];
+      }
+      __syncthreads();
+      double sg = sig1;
+      for (int j = 1; j <= m; ++j) {
+        int io = fre[(j - 1) % 3];
+        if (j == 1) {
+          const double ca = sig1 / fe, cb = -fc * sig1 / fe;
+          if (av_valid) {
+            for (int it = tid; it < nl * bc; it += blockDim.x) {
+              const int lr = it / bc, jc = c0 + (it - lr * bc);
+              const size_t o = (size_t)(x.r0 + lr) * ld + jc;
+              const double v = fma(ca, buf[iav][o], cb * s.SYc[(size_t)lr * s.sld + jc]);
+              buf[io][o] = v;
+              s.SYp[(size_t)lr * s.sld + jc] = v;
+            }
+            __syncthreads();
+            double* t = s.SYc; s.SYc = s.SYp; s.SYp = t;
+          } else {
+            operator_step_own(d, x, s, zv, d.V, buf[io], c0, bc, rF, nlock, ca, cb, 0.0, pf);
+            ++matvecs;
+          }
+        } else {
+          const double sn = 1.0 / (2.0 / sig1 - sg);
+          const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
+          operator_step_own(d, x, s, zv, buf[iy], buf[io], c0, bc, rF, nlock, ca, cb, cd, pf);
+          ++matvecs;
+          sg = sn;
+        }
+        iyp = iy;
+        iy = io;
+        __syncthreads();
+      }
+      if (bc < b) {
+        for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
+          const int jj = it % b;
+          if (jj >= c0 && jj < c0 + bc) continue;
+          const size_t o = (size_t)(x.r0 + it / b) * ld + jj;
+          buf[iy][o] = d.V[o];
+        }
+        __syncthreads();
+      }
+    } else if (m > 0) {
       double sg = sig1;
       for (int j = 1; j <= m; ++j) {
         int io = fre[(j - 1) % 3];

@@ -366,22 +366,29 @@ int check_inst(pdsdp_batch* b, int inst) {
 }
 
 int launch_iterate(pdsdp_batch* b, int nact, int lds, int step) {
-  // shared memory beyond the fixed workspaces: first the CTA's Z rows (zcap
-  // slots, all-or-nothing), then the staged operand block (ycap doubles: up to
-  // n x min(ld, 16) so that a block of <= 16 columns is staged in one chunk)
-  const size_t base = iterate_smem_bytes(lds, 0, 0);
+  // shared memory plan beyond the fixed workspaces, in priority order:
+  // (1) the CTA's Z rows (all-or-nothing; they feed every sparse product),
+  // (2) own rows of F, Y_j, Y_{j-1} (smem-resident filter recurrence),
+  // (3) the staged operand block (n rows x up to 16 columns, >= 2 columns).
+  const int nlmax = (b->nmax + b->C - 1) / b->C;
   const size_t limit = b->smem;
+  const size_t base = iterate_smem_bytes(lds, 0, 0, 0, 0);
   size_t avail = limit > base ? limit - base : 0;
   int zcap = (int)std::min<long long>(b->zmax, (long long)(avail / 12));
   if (zcap < b->zmax) zcap = 0;
   avail -= (size_t)zcap * 12;
+  int owncap = nlmax * lds;
+  size_t need_own = iterate_smem_bytes(lds, 0, 0, owncap, nlmax) - base;
+  if (need_own + 16 * (size_t)b->nmax > avail) { owncap = 0; need_own = 0; }
+  avail -= need_own;
   long long want = (long long)b->nmax * std::min(b->ldmax, 16);
   int ycap = (int)std::min<long long>(want, (long long)(avail / 8));
-  if (ycap < 2 * b->nmax) ycap = 0;
+  ycap &= ~1;
+  if (ycap < 2 * b->nmax) { ycap = 0; owncap = 0; }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nact * b->C);
   cfg.blockDim = dim3(PDSDP_NTHR);
-  cfg.dynamicSmemBytes = iterate_smem_bytes(lds, zcap, ycap);
+  cfg.dynamicSmemBytes = iterate_smem_bytes(lds, zcap, ycap, owncap, nlmax);
   cfg.stream = b->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -391,7 +398,7 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds, int step) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, lrpdhg_iterate_kernel, (const Inst*)b->d_insts, (const Ctl*)b->d_ctl,
-                        (const int*)b->d_active, step, lds, zcap, ycap));
+                        (const int*)b->d_active, step, lds, zcap, ycap, owncap, nlmax));
   return PDSDP_OK;
 }
 
