@@ -154,6 +154,116 @@ def _stall_thresholds(controller: RankController, n: int, K: int) -> np.ndarray:
     return thr
 
 
+class _InstanceRun:
+    """Host-side Algorithm-2 state of one instance (reference lowrank.py:115-190)."""
+
+    def __init__(self, batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverConfig,
+                 alpha: float, callback: ProgressCallback | None, t0: float):
+        self.batch, self.inst, self.prob, self.config = batch, inst, prob, config
+        self.callback, self.t0 = callback, t0
+        n = prob.n
+        self.n = n
+        self.eps_lambda = (config.eps_lambda if config.eps_lambda is not None
+                           else DEFAULT_EPS_LAMBDA_PER_N * n)
+        self.controller = RankController(r=min(max(config.initial_rank, 1), n), ell=config.window_ell)
+        batch.set_alpha(inst, alpha)
+        batch.reset(inst, 0.0)
+        self.it = _DeviceIterate(batch, inst)
+        self.rank_path = [(0, self.controller.r)]
+        self.status = None
+        self.res = (math.nan, math.nan, math.nan)
+        self.scale = 1.0
+        self.k = 1
+        self.eig_passes = self.eig_matvecs = self.eig_unconverged = 0
+
+    def max_chunk(self, chunk: int) -> int:
+        """Steps the device may run before the host must look: the first
+        iteration alone (it fixes the relative scale), never past max_iter, a
+        progress callback, or window_ell steps (the stall thresholds must be
+        known in advance)."""
+        c = self.config
+        if self.k == 1:
+            return 1
+        K = min(chunk, c.max_iter - self.k + 1, self.controller.ell)
+        if self.callback is not None:
+            K = min(K, c.progress_every - (self.k - 1) % c.progress_every)
+        return max(K, 1)
+
+    def thresholds(self, K: int):
+        conv = self.config.eps_tol * self.scale if self.k > 1 else -1.0
+        return conv, _stall_thresholds(self.controller, self.n, K)
+
+    def consume(self, outs, done: int) -> None:
+        """Apply the reference's per-iteration control logic to the executed
+        steps, in order (lowrank.py:141-188)."""
+        c, ctl, it, n = self.config, self.controller, self.it, self.n
+        for j in range(done):
+            out = outs[j]
+            self.eig_passes += int(out[OUT_PASSES])
+            self.eig_matvecs += int(out[OUT_MATVECS])
+            if out[OUT_FINITE] == 1.0:
+                ec = float(out[OUT_EPS_P]) + float(out[OUT_EPS_D])
+                sc = (1.0 + ec) if (self.k == 1 and c.relative_residuals) else self.scale
+                if ec <= c.eps_tol * sc:
+                    # checkpoint iteration: the certificate needs lambda_{r+1} to the
+                    # reference's accuracy; re-run this iteration from the same
+                    # (X_k, y_k) with the certificate eigenpair converged too
+                    assert j == done - 1, "device chunk ran past a checkpoint"
+                    out = self.batch.iterate([self.inst], [ctl.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
+                    self.eig_passes += int(out[OUT_PASSES])
+                    self.eig_matvecs += int(out[OUT_MATVECS])
+            if out[OUT_EIGCONV] == 0:
+                self.eig_unconverged += 1
+                logger.info("eigensolver hit its pass limit at k=%d (r=%d)", self.k, ctl.r)
+            if out[OUT_FINITE] != 1.0:                   # _finite, lowrank.py:145-147
+                self.status = SolveStatus.DIVERGED
+                it.which = 1
+                return
+            it.k = self.k                                # state.advance, pdhg.py:113-118
+            it.ypar ^= 1
+            it.which = 0
+            lambda_r = float(out[OUT_LAMBDA])
+            ctl.last_lambda_r = lambda_r
+            ep, ed = float(out[OUT_EPS_P]), float(out[OUT_EPS_D])
+            self.res = (ep, ed, ep + ed)
+            ctl.history.append(self.res[2])
+            if self.k == 1 and c.relative_residuals:
+                self.scale = 1.0 + self.res[2]
+            if self.callback is not None and self.k % c.progress_every == 0:
+                self.callback(ProgressInfo(self.k, *self.res, ctl.r, it.objective()))
+            k = self.k
+            self.k += 1
+            if self.res[2] <= c.eps_tol * self.scale:
+                Xc = it.X()
+                ctl.checkpoints.append(Checkpoint(ctl.r, Xc, it.y(), self.prob.C.inner(Xc)))
+                if rank_certificate_satisfied(n, ctl.r, lambda_r, self.eps_lambda):
+                    self.status = SolveStatus.OPTIMAL
+                    return
+                logger.debug("converged at rank %d but certificate %.3e > %.3e; doubling",
+                             ctl.r, approx_error_bound(n, ctl.r, lambda_r), self.eps_lambda)
+                update_rank(ctl, n)
+                self.rank_path.append((k, ctl.r))
+                assert j == done - 1, "device chunk ran past a rank change"
+            elif ctl.r < n and stall_detected(ctl.history, ctl.ell):
+                logger.debug("stalled at rank %d after %d iterations; doubling", ctl.r, k)
+                update_rank(ctl, n)
+                self.rank_path.append((k, ctl.r))
+                assert j == done - 1, "device chunk ran past a stall"
+
+    def check_time(self) -> None:
+        # time limit at chunk granularity (the device pauses only at algorithmic events)
+        if self.status is None and time.perf_counter() - self.t0 > self.config.time_limit_s:
+            self.status = SolveStatus.TIME_LIMIT
+        if self.status is None and self.k > self.config.max_iter:
+            self.status = SolveStatus.MAX_ITERATIONS
+
+    def outcome(self) -> LoopOutcome:
+        return LoopOutcome(status=self.status or SolveStatus.MAX_ITERATIONS, it=self.it, res=self.res,
+                           rank_path=self.rank_path, controller=self.controller, scale=self.scale,
+                           eig_passes=self.eig_passes, eig_matvecs=self.eig_matvecs,
+                           eig_unconverged=self.eig_unconverged)
+
+
 def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverConfig,
                 alpha: float, callback: ProgressCallback | None = None,
                 t0: float | None = None, chunk: int = KMAX) -> LoopOutcome:
@@ -163,91 +273,41 @@ def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverC
     divergence can fire, and the host then applies the reference's control
     logic to every executed step in order -- so every decision is taken at the
     same iteration, on the same scalars, as with one call per iteration."""
+    run = _InstanceRun(batch, inst, prob, config, alpha, callback,
+                       time.perf_counter() if t0 is None else t0)
+    while run.status is None:
+        K = run.max_chunk(chunk)
+        conv, stall = run.thresholds(K)
+        outs, done = batch.iterate_many([inst], [run.controller.r], [run.it.ypar], K, [conv], stall)
+        run.consume(outs[0], int(done[0]))
+        run.check_time()
+    return run.outcome()
+
+
+def run_lr_batch(batch: DeviceBatch, insts, config: SolverConfig, alphas,
+                 chunk: int = KMAX, t0: float | None = None) -> list:
+    """Algorithm 2 on many resident instances at once: every chunk launches
+    all still-running instances together (one cluster per instance); each
+    instance pauses on the device at its own events and keeps its own host
+    controller, exactly as in run_lr_loop."""
     t0 = time.perf_counter() if t0 is None else t0
-    n = prob.n
-    eps_lambda = (config.eps_lambda if config.eps_lambda is not None
-                  else DEFAULT_EPS_LAMBDA_PER_N * n)
-    controller = RankController(r=min(max(config.initial_rank, 1), n), ell=config.window_ell)
-    batch.set_alpha(inst, alpha)
-    batch.reset(inst, 0.0)
-    it = _DeviceIterate(batch, inst)
-    rank_path = [(0, controller.r)]
-    status = None
-    res = (math.nan, math.nan, math.nan)
-    scale = 1.0
-    eig_passes = eig_matvecs = eig_unconverged = 0
-    k = 1
-    while k <= config.max_iter and status is None:
-        # chunk length: the first iteration alone (it fixes the relative
-        # scale); never across a progress callback; at most window_ell
-        K = 1 if k == 1 else min(chunk, config.max_iter - k + 1, controller.ell)
-        if callback is not None:
-            K = min(K, config.progress_every - (k - 1) % config.progress_every)
-        conv = config.eps_tol * scale if k > 1 else -1.0
-        stall = _stall_thresholds(controller, n, K)
-        outs, done = batch.iterate_many([inst], [controller.r], [it.ypar], K, [conv], stall)
-        outs, done = outs[0], int(done[0])
-        for j in range(done):
-            out = outs[j]
-            eig_passes += int(out[OUT_PASSES])
-            eig_matvecs += int(out[OUT_MATVECS])
-            if out[OUT_FINITE] == 1.0:
-                ec = float(out[OUT_EPS_P]) + float(out[OUT_EPS_D])
-                sc = (1.0 + ec) if (k == 1 and config.relative_residuals) else scale
-                if ec <= config.eps_tol * sc:
-                    # checkpoint iteration: the certificate needs lambda_{r+1} to the
-                    # reference's accuracy; re-run this iteration from the same
-                    # (X_k, y_k) with the certificate eigenpair converged too
-                    assert j == done - 1, "device chunk ran past a checkpoint"
-                    out = batch.iterate([inst], [controller.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
-                    eig_passes += int(out[OUT_PASSES])
-                    eig_matvecs += int(out[OUT_MATVECS])
-            if out[OUT_EIGCONV] == 0:
-                eig_unconverged += 1
-                logger.info("eigensolver hit its pass limit at k=%d (r=%d)", k, controller.r)
-            if out[OUT_FINITE] != 1.0:                   # _finite, lowrank.py:145-147
-                status = SolveStatus.DIVERGED
-                it.which = 1
-                break
-            it.k = k                                     # state.advance, pdhg.py:113-118
-            it.ypar ^= 1
-            it.which = 0
-            lambda_r = float(out[OUT_LAMBDA])
-            controller.last_lambda_r = lambda_r
-            ep, ed = float(out[OUT_EPS_P]), float(out[OUT_EPS_D])
-            res = (ep, ed, ep + ed)
-            controller.history.append(res[2])
-            if k == 1 and config.relative_residuals:
-                scale = 1.0 + res[2]
-            if callback is not None and k % config.progress_every == 0:
-                callback(ProgressInfo(k, *res, controller.r, it.objective()))
-            if res[2] <= config.eps_tol * scale:
-                Xc = it.X()
-                controller.checkpoints.append(
-                    Checkpoint(controller.r, Xc, it.y(), prob.C.inner(Xc)))
-                if rank_certificate_satisfied(n, controller.r, lambda_r, eps_lambda):
-                    status = SolveStatus.OPTIMAL
-                    break
-                logger.debug("converged at rank %d but certificate %.3e > %.3e; doubling",
-                             controller.r, approx_error_bound(n, controller.r, lambda_r), eps_lambda)
-                update_rank(controller, n)
-                rank_path.append((k, controller.r))
-                assert j == done - 1, "device chunk ran past a rank change"
-            elif controller.r < n and stall_detected(controller.history, controller.ell):
-                logger.debug("stalled at rank %d after %d iterations; doubling", controller.r, k)
-                update_rank(controller, n)
-                rank_path.append((k, controller.r))
-                assert j == done - 1, "device chunk ran past a stall"
-            k += 1
-        # time limit: checked at chunk granularity (the device pauses only at
-        # algorithmic events)
-        if status is None and time.perf_counter() - t0 > config.time_limit_s:
-            status = SolveStatus.TIME_LIMIT
-    if status is None:
-        status = SolveStatus.MAX_ITERATIONS
-    return LoopOutcome(status=status, it=it, res=res, rank_path=rank_path, controller=controller,
-                       scale=scale, eig_passes=eig_passes, eig_matvecs=eig_matvecs,
-                       eig_unconverged=eig_unconverged)
+    runs = [_InstanceRun(batch, i, batch.problems[i], config, a, None, t0) for i, a in zip(insts, alphas)]
+    while True:
+        live = [r for r in runs if r.status is None]
+        if not live:
+            break
+        K = min(r.max_chunk(chunk) for r in live)
+        convs, stalls = [], []
+        for r in live:
+            cthr, sthr = r.thresholds(K)
+            convs.append(cthr)
+            stalls.append(sthr)
+        outs, done = batch.iterate_many([r.inst for r in live], [r.controller.r for r in live],
+                                        [r.it.ypar for r in live], K, convs, np.concatenate(stalls))
+        for a, r in enumerate(live):
+            r.consume(outs[a], int(done[a]))
+            r.check_time()
+    return [r.outcome() for r in runs]
 
 
 def solve_lr_pd_sdp(
@@ -265,6 +325,10 @@ def solve_lr_pd_sdp(
     batch = _device_batch(prob)
     alpha = step_size(prob, config)
     o = run_lr_loop(batch, 0, prob, config, alpha, callback, t0)
+    return _result(prob, config, o, alpha, t0, stats)
+
+
+def _result(prob, config, o, alpha, t0, stats=None) -> SolveResult:
     X = o.it.X()
     y = o.it.y()
     pobj = prob.C.inner(X)                               # lowrank.py:191-194
@@ -278,3 +342,20 @@ def solve_lr_pd_sdp(
         checkpoints=o.controller.checkpoints, wall_time_s=time.perf_counter() - t0,
         residual_scale=o.scale, objective_sign=prob.objective_sign,
     )
+
+
+def solve_lr_pd_sdp_batch(problems, config: SolverConfig | None = None) -> list:
+    """Independent instances solved together on this GPU (BASELINE config 5):
+    one resident batch, one cluster per instance per iteration, host control
+    per instance.  Returns one SolveResult per problem, as solve_lr_pd_sdp."""
+    config = config or SolverConfig()
+    config.validate()
+    t0 = time.perf_counter()
+    batch = DeviceBatch(list(problems))
+    alphas = [config.alpha_override if config.alpha_override is not None else
+              config.alpha_safety / operator_norm_on_device(batch, i, config.seed)
+              for i in range(batch.count)]
+    outs = run_lr_batch(batch, list(range(batch.count)), config, alphas, t0=t0)
+    results = [_result(p, config, o, a, t0) for p, o, a in zip(problems, outs, alphas)]
+    batch.close()
+    return results

@@ -221,3 +221,18 @@ def test_time_limit_and_max_iter_status():
     assert res.status.value == "max_iterations" and res.iterations == 7
     res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, 100000, time_limit_s=1e-9))
     assert res.status.value == "time_limit" and res.iterations == 1
+
+
+def test_batched_solve_matches_single_instance_solves():
+    """config-5 style batch: independent instances solved together give the
+    same iterations, rank paths and iterates as one-at-a-time solves."""
+    probs = [workloads.maxcut_problem(100, 0.1, seed, signed=True) for seed in range(4)]
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=600, initial_rank=2, window_ell=100)
+    batch = pk.solve_lr_pd_sdp_batch(probs, cfg)
+    for p, rb in zip(probs, batch):
+        rs = pk.solve_lr_pd_sdp(p, cfg)
+        ro = orc.solve_lr(p, cfg)
+        assert rb.status == rs.status and rb.iterations == rs.iterations == ro.iterations
+        assert rb.rank_path == rs.rank_path == ro.rank_path
+        assert rel(rb.X.data, rs.X.data) <= 1e-12
+        assert rel(rb.X.data, ro.X) <= ITER_TOL
