@@ -91,6 +91,7 @@ struct Inst {
   double* Y1;
   double* Y2;
   double* F;
+  double* Yc;          // compact (stride = active width) copy of the filter block for TMA multicast
   double* ybuf0;
   double* ybuf1;
   double* dy;

@@ -57,6 +57,7 @@ struct Sm {
   double *SF, *SYc, *SYp;      // own rows of F, Y_j, Y_{j-1} (smem-resident filter state)
   int* szp;                    // own rows of zptr
   int own, sld;                // own-row buffers valid; their stride
+  int ycap;                    // doubles in the staging buffer
   int ycw;                     // staged column chunk width (even; 0 = gather path)
   const int* zc;               // staged Z columns of own rows
   const double* zvs;           // staged Z values of own rows
@@ -90,7 +91,7 @@ __device__ __forceinline__ double cluster_sum(const Inst& d, const Cta& x, int i
 
 // Finish a cluster reduction whose per-CTA partial (q_sum sums followed by
 // q_max maxima) is already in red_slot(x, x.c).  Result -> dst (smem).
-__device__ void cluster_reduce(const Inst& d, Cta& x, int q_sum, int q_max, double* dst) {
+__device__ __forceinline__ void cluster_reduce(const Inst& d, Cta& x, int q_sum, int q_max, double* dst) {
   cg::this_cluster().sync();
   const int q = q_sum + q_max;
   for (int i = threadIdx.x; i < q; i += blockDim.x) dst[i] = cluster_sum(d, x, i, i >= q_sum);
@@ -261,7 +262,7 @@ __device__ void colres_partial(const double* __restrict__ P, const double* __res
 //   S_d Yin = F T_F + Vl T_V - alpha Z Yin
 // with T (smem, (rF + nlock) x bc, flat) already scaled: T_F = diag(lamF) F^T Yin
 // and T_V = -diag(theta) Vl^T Yin (deflation of locked Ritz pairs, nlock may be 0).
-__device__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
+__device__ __forceinline__ void apply_rows(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
                            const double* __restrict__ Yin, const double* __restrict__ Yprev,
                            double* __restrict__ out, int c0, int bc, int rF, int nlock,
                            double ca, double cb, double cd) {
@@ -323,11 +324,33 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
 }
 
+// --- TMA bulk multicast + mbarrier (cluster all-gather of the operand block) ---
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase) {
+  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}"
+               ::"r"(smem_u32(mb)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_multicast(void* dst_smem, const void* src_gmem, unsigned bytes,
+                                               unsigned long long* mb, unsigned short mask) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+               " [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(mb)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 // Same contract as apply_rows, but the operand block Yin is first copied
 // into shared memory for ALL n rows (column chunks of width s.ycw, 16-byte
 // cp.async, every load independent), so the sparse product reads its
 // gathered rows from smem instead of issuing dependent L2 round trips.
-__device__ void apply_rows_staged(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
+__device__ __forceinline__ void apply_rows_staged(const Inst& d, const Cta& x, const Sm& s, const double* __restrict__ zv,
                                   const double* __restrict__ Yin, const double* __restrict__ Yprev,
                                   double* __restrict__ out, int c0, int bc, int rF, int nlock,
                                   double ca, double cb, double cd) {
@@ -379,7 +402,7 @@ __device__ void apply_rows_staged(const Inst& d, const Cta& x, const Sm& s, cons
 }
 
 // out = In * Msm (b x b in smem), own rows; In and out must differ.
-__device__ void rotate_rows(const Inst& d, const Cta& x, const double* __restrict__ In, const double* Msm,
+__device__ __forceinline__ void rotate_rows(const Inst& d, const Cta& x, const double* __restrict__ In, const double* Msm,
                             int lds, double* __restrict__ out, int b) {
   const int ld = d.ld;
   const int nl = x.r1 - x.r0;
@@ -405,7 +428,7 @@ __device__ void scale_T(const Sm& s, int rF, int nlock, int bc) {
 
 // One operator product on columns [c0, c0+bc): reduction of [F | Vl]^T Yin
 // (one cluster barrier, which also publishes Yin to every CTA), then rows.
-__device__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* zv, const double* Yin,
+__device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* zv, const double* Yin,
                               const double* Yprev, double* out, int c0, int bc, int rF, int nlock,
                               double ca, double cb, double cd, Prof& pf) {
   prof_mark(pf, 1);
@@ -424,26 +447,27 @@ __device__ void operator_step(const Inst& d, Cta& x, const Sm& s, const double* 
 // partial reads F and Y_j from smem, the operand block is staged for all n
 // rows, and the result is written both to global (for the other CTAs) and
 // into the Y_{j-1} smem slot, which becomes Y_{j+1} (caller swaps SYc/SYp).
-__device__ void operator_step_own(const Inst& d, Cta& x, Sm& s, const double* zv, const double* Yin,
-                                  double* out, int c0, int bc, int rF, int nlock, double ca, double cb,
-                                  double cd, Prof& pf) {
+// Operator step with the CTA's rows resident in shared memory.  The operand
+// block Y_j (active columns, compact stride bcp) is all-gathered inside the
+// cluster with TMA bulk multicast: every CTA broadcasts its own rows from the
+// compact global copy into every CTA's staging buffer (one L2 read per row
+// block, no per-thread loads), in row groups that fit the buffer.  The
+// result is written to global (row-major, for the Rayleigh-Ritz step), to the
+// compact copy (next step's multicast source) and into the Y_{j-1} smem slot,
+// which becomes Y_{j+1} (SYc/SYp swapped).
+__device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
+                                                  double* out, int c0, int bc, int rF, int nlock,
+                                                  double ca, double cb, double cd, Prof& pf,
+                                                  double*& SYc, double*& SYp, unsigned long long* mbar,
+                                                  unsigned& mphase) {
   prof_mark(pf, 1);
   const int nl = x.r1 - x.r0, sl = s.sld, ld = d.ld, n = d.n, tid = threadIdx.x;
+  const int bcp = (bc + 1) & ~1;
   double* slot = red_slot(d, x, x.c);
-  gram_mma2(s.SF, sl, rF, s.SYc + c0, sl, bc, 0, nl, slot, s.gsc);
-  gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, s.SYc + c0, sl, bc, 0, nl, slot + rF * bc, s.gsc);
+  gram_mma2(s.SF, sl, rF, SYc + c0, sl, bc, 0, nl, slot, s.gsc);
+  gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, SYc + c0, sl, bc, 0, nl, slot + rF * bc, s.gsc);
   prof_mark(pf, 2);
-  cg::this_cluster().sync();                 // publishes Yin and the partials
-  double* ys = s.ys;
-  const int cw = s.ycw;
-  const int a0 = c0 & ~1, a1 = c0 + bc;
-  const int pairs = cw >> 1;
-  // first operand chunk in flight while the partials are summed
-  const float inv_pairs = 1.0f / (float)pairs;
-  for (int idx = tid; idx < n * pairs; idx += blockDim.x) {
-    const int row = (int)(((float)idx + 0.5f) * inv_pairs), pr = idx - row * pairs;
-    cp_async16(ys + (size_t)row * cw + 2 * pr, Yin + (size_t)row * ld + a0 + 2 * pr);
-  }
+  cg::this_cluster().sync();                 // publishes Yc rows and the partials
   const int q = (rF + nlock) * bc;
   for (int i = tid; i < q; i += blockDim.x) {
     const int l = i / bc;
@@ -457,58 +481,93 @@ __device__ void operator_step_own(const Inst& d, Cta& x, Sm& s, const double* zv
   const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
   const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
   const int zoff = s.zstaged ? s.zoff : 0;
-  const int jl = tid & 15, rs = tid >> 4, rstep = blockDim.x >> 4;
-  for (int cs0 = a0; cs0 < a1; cs0 += cw) {
-    if (cs0 != a0) {
-      for (int idx = tid; idx < n * pairs; idx += blockDim.x) {
-        const int row = (int)(((float)idx + 0.5f) * inv_pairs), pr = idx - row * pairs;
-        cp_async16(ys + (size_t)row * cw + 2 * pr, Yin + (size_t)row * ld + cs0 + 2 * pr);
+  double* ys = s.ys;
+  const int C = x.C;
+  const int rows_cap = s.ycap / bcp;           // rows of the staged block per round
+  const unsigned short mask = (unsigned short)((1u << C) - 1u);
+  const int nitems = nl * bc;
+  // per-thread partial sparse products of up to 4 items (nl*bc <= 4*blockDim)
+  double zacc[4] = {0.0, 0.0, 0.0, 0.0};
+  int g0 = 0;
+  while (g0 < C) {
+    // group of CTAs g0..g1-1 whose row blocks fit the staging buffer together
+    const int R0 = (int)(((long long)n * g0) / C);
+    int g1 = g0 + 1;
+    while (g1 < C && (int)(((long long)n * (g1 + 1)) / C) - R0 <= rows_cap) ++g1;
+    const int R1 = (int)(((long long)n * g1) / C);
+    if (tid == 0) {
+      mbar_expect_tx(mbar, (unsigned)((R1 - R0) * bcp * 8));
+      if (x.c >= g0 && x.c < g1) {
+        const char* src = reinterpret_cast<const char*>(d.Yc + (size_t)x.r0 * bcp);
+        char* dst = reinterpret_cast<char*>(ys + (size_t)(x.r0 - R0) * bcp);
+        unsigned left = (unsigned)(nl * bcp * 8), off = 0;
+        while (left > 0) {
+          const unsigned piece = left > 65536u ? 65536u : left;
+          bulk_multicast(dst + off, src + off, piece, mbar, mask);
+          off += piece; left -= piece;
+        }
       }
     }
-    cp_async_wait_all();
-    __syncthreads();
-    const int jlo = max(cs0, c0), jhi = min(cs0 + cw, a1), w_ = jhi - jlo;
-    // thread -> (row slot, column): 16 columns per row pass, 4 slots per round trip
-    for (int cb0 = 0; cb0 < w_; cb0 += 16) {
-      const int jc = cb0 + jl;
-      if (jc >= w_) continue;
-      const int j = jlo + jc, jj = j - c0, js = j - cs0;
-      for (int lr = rs; lr < nl; lr += rstep) {
-        const int e1 = s.szp[lr + 1] - zoff;
-        int e = s.szp[lr] - zoff;
-        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-        for (; e + 4 <= e1; e += 4) {
-          const int q0 = zcol[e], q1 = zcol[e + 1], q2 = zcol[e + 2], q3 = zcol[e + 3];
-          const double v0 = zval[e], v1 = zval[e + 1], v2 = zval[e + 2], v3 = zval[e + 3];
-          const double y0 = ys[(size_t)q0 * cw + js], y1 = ys[(size_t)q1 * cw + js];
-          const double y2 = ys[(size_t)q2 * cw + js], y3 = ys[(size_t)q3 * cw + js];
-          z0 = fma(v0, y0, z0); z1 = fma(v1, y1, z1); z2 = fma(v2, y2, z2); z3 = fma(v3, y3, z3);
+    prof_mark(pf, 13);
+    mbar_wait(mbar, mphase);
+    mphase ^= 1u;
+    prof_mark(pf, 14);
+    const bool all = (R0 == 0 && R1 == n);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int it = tid + u * blockDim.x;
+      if (it >= nitems) break;
+      const int lr = it / bc, jj = it - lr * bc;
+      const int e1 = s.szp[lr + 1] - zoff;
+      int e = s.szp[lr] - zoff;
+      double z0 = 0.0, z1 = 0.0;
+      if (all) {
+        for (; e + 2 <= e1; e += 2) {
+          z0 = fma(zval[e], ys[(size_t)zcol[e] * bcp + jj], z0);
+          z1 = fma(zval[e + 1], ys[(size_t)zcol[e + 1] * bcp + jj], z1);
         }
-        for (; e < e1; ++e) z0 = fma(zval[e], ys[(size_t)zcol[e] * cw + js], z0);
-        const double* Fr = s.SF + (size_t)lr * sl;
-        double w0 = 0.0, w1 = 0.0;
-        int l = 0;
-        for (; l + 2 <= rF; l += 2) {
-          w0 = fma(Fr[l], s.T[l * bc + jj], w0);
-          w1 = fma(Fr[l + 1], s.T[(l + 1) * bc + jj], w1);
+        if (e < e1) z0 = fma(zval[e], ys[(size_t)zcol[e] * bcp + jj], z0);
+      } else {
+        for (; e < e1; ++e) {
+          const int qc = zcol[e];
+          if (qc >= R0 && qc < R1) z0 = fma(zval[e], ys[(size_t)(qc - R0) * bcp + jj], z0);
         }
-        if (l < rF) w0 = fma(Fr[l], s.T[l * bc + jj], w0);
-        double w = w0 + w1;
-        if (nlock) {
-          const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
-          for (int t = 0; t < nlock; ++t) w = fma(Vr[t], s.T[(rF + t) * bc + jj], w);
-        }
-        w = fma(-alpha, (z0 + z1) + (z2 + z3), w);
-        double o = ca * w;
-        if (cb != 0.0) o = fma(cb, s.SYc[(size_t)lr * sl + j], o);
-        if (cd != 0.0) o = fma(cd, s.SYp[(size_t)lr * sl + j], o);
-        out[(size_t)(x.r0 + lr) * ld + j] = o;
-        s.SYp[(size_t)lr * sl + j] = o;
       }
+      zacc[u] += z0 + z1;
     }
-    __syncthreads();
+    g0 = g1;
+    if (g0 < C) cg::this_cluster().sync();   // everyone done with ys before it is overwritten
+    prof_mark(pf, 3);
   }
-  double* t = s.SYc; s.SYc = s.SYp; s.SYp = t;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int it = tid + u * blockDim.x;
+    if (it >= nitems) break;
+    const int lr = it / bc, jj = it - lr * bc, j = c0 + jj;
+    const double* Fr = s.SF + (size_t)lr * sl;
+    double w0 = 0.0, w1 = 0.0;
+    int l = 0;
+    for (; l + 2 <= rF; l += 2) {
+      w0 = fma(Fr[l], s.T[l * bc + jj], w0);
+      w1 = fma(Fr[l + 1], s.T[(l + 1) * bc + jj], w1);
+    }
+    if (l < rF) w0 = fma(Fr[l], s.T[l * bc + jj], w0);
+    double w = w0 + w1;
+    if (nlock) {
+      const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
+      for (int t = 0; t < nlock; ++t) w = fma(Vr[t], s.T[(rF + t) * bc + jj], w);
+    }
+    w = fma(-alpha, zacc[u], w);
+    double o = ca * w;
+    if (cb != 0.0) o = fma(cb, SYc[(size_t)lr * sl + j], o);
+    if (cd != 0.0) o = fma(cd, SYp[(size_t)lr * sl + j], o);
+    out[(size_t)(x.r0 + lr) * ld + j] = o;
+    d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = o;
+    SYp[(size_t)lr * sl + j] = o;
+  }
+  fence_proxy_async();
+  __syncthreads();
+  double* t = SYc; SYc = SYp; SYp = t;
 }
 
 // Convergence state of the Ritz block (identical in every thread).
@@ -619,12 +678,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   x.r1 = (int)(((long long)n * (x.c + 1)) / x.C);
   x.par = 0;
 
-  Prof pf;
-  pf.last = clock64(); pf.cur = 0;
-  for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
-  Sm s;
-  s.lds = lds;
-  {
+  __shared__ Prof pf_sm;                 // thread-0 phase timer (kept out of local memory)
+  Prof& pf = pf_sm;
+  if (threadIdx.x == 0) {
+    pf.last = clock64(); pf.cur = 0;
+    for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
+  }
+  __shared__ Sm s_sm;
+  Sm& s = s_sm;
+  if (threadIdx.x == 0) {
+    s.lds = lds;
     double* p = smem;
     const int sq = lcap * lds;
     s.A = p; p += sq; s.Q = p; p += sq; s.L = p; p += sq; s.M = p; p += sq; s.T = p; p += sq;
@@ -648,9 +711,19 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (cw > d.ld) cw = d.ld;
     s.ycw = (cw >= 2) ? cw : 0;
     s.sld = lcap;
-    s.own = (owncap > 0 && s.ycw >= 2 && (x.r1 - x.r0) * lcap <= owncap && (x.r1 - x.r0) <= nlmax) ? 1 : 0;
+    s.ycap = ycap;
+    s.own = (owncap > 0 && s.ycw >= 2 && (x.r1 - x.r0) * lcap <= owncap && (x.r1 - x.r0) <= nlmax &&
+             (x.r1 - x.r0 + 1) * 64 <= ycap && (x.r1 - x.r0) * lcap <= 4 * PDSDP_NTHR) ? 1 : 0;
   }
-  double* buf[5] = {d.V, d.AV, d.Y0, d.Y1, d.Y2};
+  __shared__ __align__(8) unsigned long long mbar_sm;   // completion barrier of the operand all-gather
+  if (threadIdx.x == 0) mbar_init(&mbar_sm, 1);
+  unsigned mphase = 0;
+  __syncthreads();
+  double* SYc = s.SYc;   // own rows of Y_j / Y_{j-1}: per-thread pointers (swapped each step)
+  double* SYp = s.SYp;
+  auto buf = [&](int i) -> double* {
+    return i == 0 ? d.V : i == 1 ? d.AV : i == 2 ? d.Y0 : i == 3 ? d.Y1 : d.Y2;
+  };
 
   // ---------------- prologue: F <- V[:, :rF] (X_k), block setup ----------------
   // flags: bit0 cold start; bit1 the certificate eigenvalue lambda_{r+1} must be
@@ -758,39 +831,46 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // ---- Chebyshev filter on the active columns:  Y_m = p_m(S_d) V ----
     int iy = 0;                       // buffer index holding Y_j (0 == V)
     int iyp = -1;                     // buffer holding Y_{j-1}
-    int fre[3], nf = 0;
-    for (int q = 1; q <= 4; ++q) if (q != iav) fre[nf++] = q;
+    // the three buffers other than V and AV (ring for the recurrence)
+    auto fre = [&](int t) -> int { const int q = 1 + t; return q >= iav ? q + 1 : q; };
     if (m > 0 && s.own) {
-      // own rows of V (the recurrence's Y_0) into smem
+      // own rows of V (the recurrence's Y_0) into smem and into the compact
+      // multicast source
       const int nl = x.r1 - x.r0;
+      const int bcp = (bc + 1) & ~1;
       for (int it = tid; it < nl * bc; it += blockDim.x) {
-        const int lr = it / bc, j = c0 + (it - lr * bc);
-        s.SYc[(size_t)lr * s.sld + j] = d.V[(size_t)(x.r0 + lr) * ld + j];
+        const int lr = it / bc, jj = it - lr * bc, j = c0 + jj;
+        const double v = d.V[(size_t)(x.r0 + lr) * ld + j];
+        SYc[(size_t)lr * s.sld + j] = v;
+        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
       }
+      fence_proxy_async();
       __syncthreads();
       double sg = sig1;
       for (int j = 1; j <= m; ++j) {
-        int io = fre[(j - 1) % 3];
+        int io = fre((j - 1) % 3);
         if (j == 1) {
           const double ca = sig1 / fe, cb = -fc * sig1 / fe;
           if (av_valid) {
             for (int it = tid; it < nl * bc; it += blockDim.x) {
-              const int lr = it / bc, jc = c0 + (it - lr * bc);
+              const int lr = it / bc, jj = it - lr * bc, jc = c0 + jj;
               const size_t o = (size_t)(x.r0 + lr) * ld + jc;
-              const double v = fma(ca, buf[iav][o], cb * s.SYc[(size_t)lr * s.sld + jc]);
-              buf[io][o] = v;
-              s.SYp[(size_t)lr * s.sld + jc] = v;
+              const double v = fma(ca, buf(iav)[o], cb * SYc[(size_t)lr * s.sld + jc]);
+              buf(io)[o] = v;
+              SYp[(size_t)lr * s.sld + jc] = v;
+              d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
             }
+            fence_proxy_async();
             __syncthreads();
-            double* t = s.SYc; s.SYc = s.SYp; s.SYp = t;
+            double* t = SYc; SYc = SYp; SYp = t;
           } else {
-            operator_step_own(d, x, s, zv, d.V, buf[io], c0, bc, rF, nlock, ca, cb, 0.0, pf);
+            operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, 0.0, pf, SYc, SYp, &mbar_sm, mphase);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step_own(d, x, s, zv, buf[iy], buf[io], c0, bc, rF, nlock, ca, cb, cd, pf);
+          operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, cd, pf, SYc, SYp, &mbar_sm, mphase);
           ++matvecs;
           sg = sn;
         }
@@ -803,29 +883,29 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const int jj = it % b;
           if (jj >= c0 && jj < c0 + bc) continue;
           const size_t o = (size_t)(x.r0 + it / b) * ld + jj;
-          buf[iy][o] = d.V[o];
+          buf(iy)[o] = d.V[o];
         }
         __syncthreads();
       }
     } else if (m > 0) {
       double sg = sig1;
       for (int j = 1; j <= m; ++j) {
-        int io = fre[(j - 1) % 3];
+        int io = fre((j - 1) % 3);
         if (j == 1) {
           const double ca = sig1 / fe, cb = -fc * sig1 / fe;
           if (av_valid) {
             for (int it = tid; it < (x.r1 - x.r0) * bc; it += blockDim.x) {
               const size_t o = (size_t)(x.r0 + it / bc) * ld + c0 + it % bc;
-              buf[io][o] = fma(ca, buf[iav][o], cb * d.V[o]);
+              buf(io)[o] = fma(ca, buf(iav)[o], cb * d.V[o]);
             }
           } else {
-            operator_step(d, x, s, zv, d.V, nullptr, buf[io], c0, bc, rF, nlock, ca, cb, 0.0, pf);
+            operator_step(d, x, s, zv, d.V, nullptr, buf(io), c0, bc, rF, nlock, ca, cb, 0.0, pf);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step(d, x, s, zv, buf[iy], buf[iyp < 0 ? 0 : iyp], buf[io], c0, bc, rF, nlock, ca, cb, cd, pf);
+          operator_step(d, x, s, zv, buf(iy), buf(iyp < 0 ? 0 : iyp), buf(io), c0, bc, rF, nlock, ca, cb, cd, pf);
           ++matvecs;
           sg = sn;
         }
@@ -839,20 +919,20 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const int jj = it % b;
           if (jj >= c0 && jj < c0 + bc) continue;
           const size_t o = (size_t)(x.r0 + it / b) * ld + jj;
-          buf[iy][o] = d.V[o];
+          buf(iy)[o] = d.V[o];
         }
         __syncthreads();
       }
     }
     // ---- R1: G1 = Y^T Y, T = F^T Y ; W = S Y ----
-    const int iw = (iy == 0) ? fre[0] : fre[(m) % 3];          // free of {Y_m, Y_{m-1}} ring
+    const int iw = (iy == 0) ? fre(0) : fre((m) % 3);          // free of {Y_m, Y_{m-1}} ring
     int iw1 = -1;
-    for (int q2 = 0; q2 < 3; ++q2) if (fre[q2] != iy && fre[q2] != iw) { iw1 = fre[q2]; break; }
+    for (int q2 = 0; q2 < 3; ++q2) if (fre(q2) != iy && fre(q2) != iw) { iw1 = fre(q2); break; }
     {
       double* slot = red_slot(d, x, x.c);
       prof_mark(pf, 1);
-      gram_mma(buf[iy], b, buf[iy], b, ld, x.r0, x.r1, slot, s.gsc);
-      gram_mma(d.F, rF, buf[iy], b, ld, x.r0, x.r1, slot + b * b, s.gsc);
+      gram_mma(buf(iy), b, buf(iy), b, ld, x.r0, x.r1, slot, s.gsc);
+      gram_mma(d.F, rF, buf(iy), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
       // reduce into A (G1) and T
       cg::this_cluster().sync();
       const int q = b * b + rF * b;
@@ -866,8 +946,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     scale_T(s, rF, 0, b);
     prof_mark(pf, 3);
-    if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf[iy], nullptr, buf[iw], 0, b, rF, 0, 1.0, 0.0, 0.0);
-    else apply_rows(d, x, s, zv, buf[iy], nullptr, buf[iw], 0, b, rF, 0, 1.0, 0.0, 0.0);
+    if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rF, 0, 1.0, 0.0, 0.0);
+    else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rF, 0, 1.0, 0.0, 0.0);
     prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
@@ -886,16 +966,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
     }
     __syncthreads();
-    // Y1 = Y M1 -> buf[iav] ; W1 = W M1 -> buf[iw1]
+    // Y1 = Y M1 -> buf(iav) ; W1 = W M1 -> buf(iw1)
     prof_mark(pf, 5);
-    rotate_rows(d, x, buf[iy], s.M, lds, buf[iav], b);
-    rotate_rows(d, x, buf[iw], s.M, lds, buf[iw1], b);
+    rotate_rows(d, x, buf(iy), s.M, lds, buf(iav), b);
+    rotate_rows(d, x, buf(iw), s.M, lds, buf(iw1), b);
     __syncthreads();
     // ---- R2: G2 = Y1^T Y1, H = Y1^T W1 ----
     {
       double* slot = red_slot(d, x, x.c);
-      gram_mma(buf[iav], b, buf[iav], b, ld, x.r0, x.r1, slot, s.gsc);
-      gram_mma(buf[iav], b, buf[iw1], b, ld, x.r0, x.r1, slot + b * b, s.gsc);
+      gram_mma(buf(iav), b, buf(iav), b, ld, x.r0, x.r1, slot, s.gsc);
+      gram_mma(buf(iav), b, buf(iw1), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
       cg::this_cluster().sync();
       const int q = 2 * b * b;
       for (int i = tid; i < q; i += blockDim.x) {
@@ -958,16 +1038,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       Bm[i * lds + j] = s.dsc[i] * acc;
     }
     __syncthreads();
-    // V = Y1 B ; AV = W1 B  (AV goes to buf[iw], which becomes the AV buffer)
+    // V = Y1 B ; AV = W1 B  (AV goes to buf(iw), which becomes the AV buffer)
     prof_mark(pf, 5);
-    rotate_rows(d, x, buf[iav], Bm, lds, d.V, b);
-    rotate_rows(d, x, buf[iw1], Bm, lds, buf[iw], b);
+    rotate_rows(d, x, buf(iav), Bm, lds, d.V, b);
+    rotate_rows(d, x, buf(iw1), Bm, lds, buf(iw), b);
     iav = iw;
     av_valid = true;
     theta_valid = true;
     __syncthreads();
     // ---- R3: residual norms ----
-    colres_partial(buf[iav], d.V, s.theta, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
+    colres_partial(buf(iav), d.V, s.theta, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
     cluster_reduce(d, x, b, 0, s.red1);
     ++passes;
     {
