@@ -91,7 +91,7 @@ struct Inst {
   double* Y1;
   double* Y2;
   double* F;
-  double* Yc;          // compact (stride = active width) copy of the filter block for TMA multicast
+  double* Yc;          // 2 x compact (stride = active width) copies of the filter block (TMA multicast sources)
   double* ybuf0;
   double* ybuf1;
   double* dy;

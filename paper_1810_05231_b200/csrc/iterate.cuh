@@ -54,7 +54,7 @@ struct Sm {
   double *A, *Q, *L, *M, *T;   // lds x lds each
   double *gsc;                 // PDSDP_GRAM_SCR
   double* ys;                  // staged operand block (n x ycw)
-  double *SF, *SYc, *SYp;      // own rows of F, Y_j, Y_{j-1} (smem-resident filter state)
+  double *SF, *SYc, *SYp;      // own rows of F (SYc/SYp unused)
   int* szp;                    // own rows of zptr
   int own, sld;                // own-row buffers valid; their stride
   int ycap;                    // doubles in the staging buffer
@@ -447,50 +447,55 @@ __device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s
 // partial reads F and Y_j from smem, the operand block is staged for all n
 // rows, and the result is written both to global (for the other CTAs) and
 // into the Y_{j-1} smem slot, which becomes Y_{j+1} (caller swaps SYc/SYp).
-// Operator step with the CTA's rows resident in shared memory.  The operand
-// block Y_j (active columns, compact stride bcp) is all-gathered inside the
-// cluster with TMA bulk multicast: every CTA broadcasts its own rows from the
-// compact global copy into every CTA's staging buffer (one L2 read per row
-// block, no per-thread loads), in row groups that fit the buffer.  The
-// result is written to global (row-major, for the Rayleigh-Ritz step), to the
-// compact copy (next step's multicast source) and into the Y_{j-1} smem slot,
-// which becomes Y_{j+1} (SYc/SYp swapped).
+// Operator step of the Chebyshev recurrence.  The operand block Y_j (active
+// columns, compact stride bcp, global buffer Yc[p]) is all-gathered inside the
+// cluster with TMA bulk multicast: every CTA broadcasts its own rows into every
+// CTA's staging buffer (one L2 read per row block), in row groups that fit the
+// buffer; each own row's Z slots of a group form a contiguous sub-range
+// (columns are sorted).  F's own rows stay in shared memory; the CTA's own
+// items of Y_j and Y_{j-1} are prefetched into registers.  Y_{j+1} goes to
+// global row-major (for Rayleigh-Ritz) and into Yc[p^1] over Y_{j-1}.
 __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
                                                   double* out, int c0, int bc, int rF, int nlock,
                                                   double ca, double cb, double cd, Prof& pf,
-                                                  double*& SYc, double*& SYp, unsigned long long* mbar,
-                                                  unsigned& mphase) {
+                                                  int& ycp, unsigned long long* mbar, unsigned& mphase) {
   prof_mark(pf, 1);
   const int nl = x.r1 - x.r0, sl = s.sld, ld = d.ld, n = d.n, tid = threadIdx.x;
   const int bcp = (bc + 1) & ~1;
-  double* slot = red_slot(d, x, x.c);
-  gram_mma2(s.SF, sl, rF, SYc + c0, sl, bc, 0, nl, slot, s.gsc);
-  gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, SYc + c0, sl, bc, 0, nl, slot + rF * bc, s.gsc);
-  prof_mark(pf, 2);
-  cg::this_cluster().sync();                 // publishes Yc rows and the partials
-  const int q = (rF + nlock) * bc;
-  for (int i = tid; i < q; i += blockDim.x) {
-    const int l = i / bc;
-    const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
-    const double v = cluster_sum(d, x, i, false);
-    s.T[i] = (c == 0.0) ? 0.0 : v * c;
+  const size_t nld = (size_t)n * ld;
+  const double* Ycur = d.Yc + (size_t)ycp * nld;
+  double* Ynxt = d.Yc + (size_t)(ycp ^ 1) * nld;
+  const int nitems = nl * bc;
+  double ycur[4], yprv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int it = tid + u * blockDim.x;
+    ycur[u] = 0.0; yprv[u] = 0.0;
+    if (it < nitems) {
+      const int lr = it / bc, jj = it - lr * bc;
+      const size_t o = (size_t)(x.r0 + lr) * bcp + jj;
+      if (cb != 0.0) ycur[u] = __ldcg(Ycur + o);
+      if (cd != 0.0) yprv[u] = __ldcg(Ynxt + o);
+    }
   }
-  x.par ^= 1;
-  prof_mark(pf, 3);
+  double* slot = red_slot(d, x, x.c);
+  gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
+  gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
+            slot + rF * bc, s.gsc);
+  prof_mark(pf, 2);
+  cg::this_cluster().sync();                 // publishes Y_j rows and the partials
   const double alpha = d.alpha;
+  double* ys = s.ys;
+  const int C = x.C;
+  const int rows_cap = s.ycap / bcp;
+  const unsigned short mask = (unsigned short)((1u << C) - 1u);
+  int g0 = 0;
+  bool first = true;
+  double zacc[4] = {0.0, 0.0, 0.0, 0.0};
   const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
   const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
   const int zoff = s.zstaged ? s.zoff : 0;
-  double* ys = s.ys;
-  const int C = x.C;
-  const int rows_cap = s.ycap / bcp;           // rows of the staged block per round
-  const unsigned short mask = (unsigned short)((1u << C) - 1u);
-  const int nitems = nl * bc;
-  // per-thread partial sparse products of up to 4 items (nl*bc <= 4*blockDim)
-  double zacc[4] = {0.0, 0.0, 0.0, 0.0};
-  int g0 = 0;
   while (g0 < C) {
-    // group of CTAs g0..g1-1 whose row blocks fit the staging buffer together
     const int R0 = (int)(((long long)n * g0) / C);
     int g1 = g0 + 1;
     while (g1 < C && (int)(((long long)n * (g1 + 1)) / C) - R0 <= rows_cap) ++g1;
@@ -498,7 +503,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     if (tid == 0) {
       mbar_expect_tx(mbar, (unsigned)((R1 - R0) * bcp * 8));
       if (x.c >= g0 && x.c < g1) {
-        const char* src = reinterpret_cast<const char*>(d.Yc + (size_t)x.r0 * bcp);
+        const char* src = reinterpret_cast<const char*>(Ycur + (size_t)x.r0 * bcp);
         char* dst = reinterpret_cast<char*>(ys + (size_t)(x.r0 - R0) * bcp);
         unsigned left = (unsigned)(nl * bcp * 8), off = 0;
         while (left > 0) {
@@ -508,9 +513,21 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
         }
       }
     }
+    if (first) {
+      const int q = (rF + nlock) * bc;
+      for (int i = tid; i < q; i += blockDim.x) {
+        const int l = i / bc;
+        const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
+        const double v = cluster_sum(d, x, i, false);
+        s.T[i] = (c == 0.0) ? 0.0 : v * c;
+      }
+      x.par ^= 1;
+      first = false;
+    }
     prof_mark(pf, 13);
     mbar_wait(mbar, mphase);
     mphase ^= 1u;
+    __syncthreads();
     prof_mark(pf, 14);
     const bool all = (R0 == 0 && R1 == n);
 #pragma unroll
@@ -518,25 +535,28 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       const int it = tid + u * blockDim.x;
       if (it >= nitems) break;
       const int lr = it / bc, jj = it - lr * bc;
-      const int e1 = s.szp[lr + 1] - zoff;
-      int e = s.szp[lr] - zoff;
-      double z0 = 0.0, z1 = 0.0;
-      if (all) {
-        for (; e + 2 <= e1; e += 2) {
-          z0 = fma(zval[e], ys[(size_t)zcol[e] * bcp + jj], z0);
-          z1 = fma(zval[e + 1], ys[(size_t)zcol[e + 1] * bcp + jj], z1);
-        }
-        if (e < e1) z0 = fma(zval[e], ys[(size_t)zcol[e] * bcp + jj], z0);
-      } else {
-        for (; e < e1; ++e) {
-          const int qc = zcol[e];
-          if (qc >= R0 && qc < R1) z0 = fma(zval[e], ys[(size_t)(qc - R0) * bcp + jj], z0);
-        }
+      int e = s.szp[lr] - zoff, e1 = s.szp[lr + 1] - zoff;
+      if (!all) {
+        int lo = e, hi = e1;
+        while (lo < hi) { const int md = (lo + hi) >> 1; if (zcol[md] < R0) lo = md + 1; else hi = md; }
+        e = lo;
+        int lo2 = e; hi = e1;
+        while (lo2 < hi) { const int md = (lo2 + hi) >> 1; if (zcol[md] < R1) lo2 = md + 1; else hi = md; }
+        e1 = lo2;
       }
-      zacc[u] += z0 + z1;
+      double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+      for (; e + 4 <= e1; e += 4) {
+        const int q0 = zcol[e] - R0, q1 = zcol[e + 1] - R0, q2 = zcol[e + 2] - R0, q3 = zcol[e + 3] - R0;
+        z0 = fma(zval[e], ys[(size_t)q0 * bcp + jj], z0);
+        z1 = fma(zval[e + 1], ys[(size_t)q1 * bcp + jj], z1);
+        z2 = fma(zval[e + 2], ys[(size_t)q2 * bcp + jj], z2);
+        z3 = fma(zval[e + 3], ys[(size_t)q3 * bcp + jj], z3);
+      }
+      for (; e < e1; ++e) z0 = fma(zval[e], ys[(size_t)(zcol[e] - R0) * bcp + jj], z0);
+      zacc[u] += (z0 + z1) + (z2 + z3);
     }
     g0 = g1;
-    if (g0 < C) cg::this_cluster().sync();   // everyone done with ys before it is overwritten
+    if (g0 < C) cg::this_cluster().sync();
     prof_mark(pf, 3);
   }
 #pragma unroll
@@ -559,15 +579,14 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     w = fma(-alpha, zacc[u], w);
     double o = ca * w;
-    if (cb != 0.0) o = fma(cb, SYc[(size_t)lr * sl + j], o);
-    if (cd != 0.0) o = fma(cd, SYp[(size_t)lr * sl + j], o);
+    if (cb != 0.0) o = fma(cb, ycur[u], o);
+    if (cd != 0.0) o = fma(cd, yprv[u], o);
     out[(size_t)(x.r0 + lr) * ld + j] = o;
-    d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = o;
-    SYp[(size_t)lr * sl + j] = o;
+    Ynxt[(size_t)(x.r0 + lr) * bcp + jj] = o;
   }
   fence_proxy_async();
   __syncthreads();
-  double* t = SYc; SYc = SYp; SYp = t;
+  ycp ^= 1;
 }
 
 // Convergence state of the Ritz block (identical in every thread).
@@ -633,7 +652,7 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
 
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
 inline size_t iterate_smem_bytes(int lds, int zcap, int ycap, int owncap, int nlmax) {
-  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 13 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap + 3 * owncap) *
+  return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 13 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap + owncap) *
              sizeof(double) +
          (size_t)(3 * PDSDP_BMAX + 8 + zcap + (owncap ? nlmax + 2 : 0)) * sizeof(int) + 64;
 }
@@ -697,7 +716,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.red1 = p; p += 4 * PDSDP_BMAX;
     s.gsc = p; p += PDSDP_GRAM_SCR;
     s.ys = p; p += ycap;
-    s.SF = p; p += owncap; s.SYc = p; p += owncap; s.SYp = p; p += owncap;
+    s.SF = p; p += owncap;
     double* zvs = p; p += zcap;
     int* ip = (int*)p;
     s.perm = ip; ip += PDSDP_BMAX; s.pq = ip; ip += 2 * PDSDP_BMAX; s.flag = ip; ip += 8;
@@ -712,15 +731,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.ycw = (cw >= 2) ? cw : 0;
     s.sld = lcap;
     s.ycap = ycap;
-    s.own = (owncap > 0 && s.ycw >= 2 && (x.r1 - x.r0) * lcap <= owncap && (x.r1 - x.r0) <= nlmax &&
-             (x.r1 - x.r0 + 1) * 64 <= ycap && (x.r1 - x.r0) * lcap <= 4 * PDSDP_NTHR) ? 1 : 0;
+    s.own = (owncap > 0 && (x.r1 - x.r0) * lcap <= owncap && (x.r1 - x.r0) <= nlmax &&
+             (x.r1 - x.r0) * lcap <= ycap && (x.r1 - x.r0) * lcap <= 4 * PDSDP_NTHR) ? 1 : 0;
   }
   __shared__ __align__(8) unsigned long long mbar_sm;   // completion barrier of the operand all-gather
   if (threadIdx.x == 0) mbar_init(&mbar_sm, 1);
   unsigned mphase = 0;
   __syncthreads();
-  double* SYc = s.SYc;   // own rows of Y_j / Y_{j-1}: per-thread pointers (swapped each step)
-  double* SYp = s.SYp;
+
   auto buf = [&](int i) -> double* {
     return i == 0 ? d.V : i == 1 ? d.AV : i == 2 ? d.Y0 : i == 3 ? d.Y1 : d.Y2;
   };
@@ -834,15 +852,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // the three buffers other than V and AV (ring for the recurrence)
     auto fre = [&](int t) -> int { const int q = 1 + t; return q >= iav ? q + 1 : q; };
     if (m > 0 && s.own) {
-      // own rows of V (the recurrence's Y_0) into smem and into the compact
-      // multicast source
+      // own rows of V (the recurrence's Y_0) into the compact multicast source
       const int nl = x.r1 - x.r0;
       const int bcp = (bc + 1) & ~1;
+      const size_t nld = (size_t)n * ld;
+      int ycp = 0;
       for (int it = tid; it < nl * bc; it += blockDim.x) {
-        const int lr = it / bc, jj = it - lr * bc, j = c0 + jj;
-        const double v = d.V[(size_t)(x.r0 + lr) * ld + j];
-        SYc[(size_t)lr * s.sld + j] = v;
-        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
+        const int lr = it / bc, jj = it - lr * bc;
+        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = d.V[(size_t)(x.r0 + lr) * ld + c0 + jj];
       }
       fence_proxy_async();
       __syncthreads();
@@ -855,22 +872,21 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             for (int it = tid; it < nl * bc; it += blockDim.x) {
               const int lr = it / bc, jj = it - lr * bc, jc = c0 + jj;
               const size_t o = (size_t)(x.r0 + lr) * ld + jc;
-              const double v = fma(ca, buf(iav)[o], cb * SYc[(size_t)lr * s.sld + jc]);
+              const double v = fma(ca, buf(iav)[o], cb * d.V[o]);
               buf(io)[o] = v;
-              SYp[(size_t)lr * s.sld + jc] = v;
-              d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
+              d.Yc[nld + (size_t)(x.r0 + lr) * bcp + jj] = v;
             }
             fence_proxy_async();
             __syncthreads();
-            double* t = SYc; SYc = SYp; SYp = t;
+            ycp = 1;
           } else {
-            operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, 0.0, pf, SYc, SYp, &mbar_sm, mphase);
+            operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, cd, pf, SYc, SYp, &mbar_sm, mphase);
+          operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase);
           ++matvecs;
           sg = sn;
         }
@@ -1201,7 +1217,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       st->b = b;
       st->rF = rN;
       st->theta_valid = theta_valid ? 1 : 0;
-      if (!rerun && msucc > 0) st->mhint = msucc;
+      // degree hint for the next iteration's first pass: probe one degree lower
+      // after a single-pass convergence, else the total degree this one needed
+      if (!rerun && msucc > 0) st->mhint = (passes == 1 && converged == 1 && fails == 0) ? max(2, msucc - 1) : msucc;
       st->iav = iav;
       st->ed2 = ed2_tot;
       st->corr = s.red1[0];
