@@ -1,7 +1,7 @@
 # Builds the sm_100a C-ABI library in-tree (travels to the GPU box with the snapshot).
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr
+NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr $(EXTRA)
 SRC := paper_1810_05231_b200/csrc/pdsdp_b200.cu
 HDR := $(wildcard paper_1810_05231_b200/csrc/*.cuh) include/pdsdp_b200.h
 LIB := paper_1810_05231_b200/libpdsdp_b200.so

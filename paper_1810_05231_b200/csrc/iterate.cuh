@@ -28,6 +28,9 @@ namespace pdsdp {
 #define PDSDP_TOL_CERT 1e-8
 #define PDSDP_TOL_CLIP 1e-6
 #define PDSDP_MMAX 24
+#ifndef PDSDP_HINT_SAFETY
+#define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
+#endif
 
 // Is Ritz pair i accurate enough?  i < r: kept in X+ (clipped at 0);
 // i == r: the certificate eigenvalue lambda_{r+1} (only its value matters).
@@ -798,7 +801,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   int passes = 0, matvecs = 0, converged = 0;
   double prev_maxres = 1.0e300, maxres = 1.0e300;
   const int maxpass = ctl.maxpass > 0 ? ctl.maxpass : 60;
-  int force_m = -1, msucc = 0, fails = 0;
+  int force_m = -1, msucc = 0, fails = 0, slack = 0;
   const int hint = (int)st->mhint;
   for (int pass = 0; pass < maxpass; ++pass) {
     // ---- pass plan (identical in every thread): degree m, active columns
@@ -1076,7 +1079,22 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
       maxres = as.maxres;
       // a block that was not filtered in this pass (cold RR) is not trusted
-      if (as.last_bad < 0 && !as.cert_bad && !as.tail_bad && (m > 0 || b >= n)) { converged = 1; break; }
+      if (as.last_bad < 0 && !as.cert_bad && !as.tail_bad && (m > 0 || b >= n)) {
+        converged = 1;
+        // degrees of slack: how many fewer filter degrees would still have met
+        // each kept column's tolerance (Chebyshev gain acosh(t) per degree)
+        if (m > 0 && pass == 0) {
+          double sl = 1.0e300;
+          for (int i = 0; i < r && i < b; ++i) {
+            const double t = (s.theta[i] - fc) / fe;
+            if (t <= 1.0 + 1e-6) { sl = 0.0; break; }
+            const double tol = fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
+            sl = fmin(sl, log(tol / fmax(s.res[i], 1e-300)) / acosh(t));
+          }
+          slack = (sl > 0.0 && sl < 64.0) ? (int)floor(sl) : (sl >= 64.0 ? 64 : 0);
+        }
+        break;
+      }
       // stagnation at the rounding floor
       if (pass >= 2 && maxres > 0.5 * prev_maxres && maxres < 1e-10) { converged = 2; break; }
       prev_maxres = maxres;
@@ -1217,9 +1235,13 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       st->b = b;
       st->rF = rN;
       st->theta_valid = theta_valid ? 1 : 0;
-      // degree hint for the next iteration's first pass: probe one degree lower
-      // after a single-pass convergence, else the total degree this one needed
-      if (!rerun && msucc > 0) st->mhint = (passes == 1 && converged == 1 && fails == 0) ? max(2, msucc - 1) : msucc;
+      // degree hint for the next iteration's first pass: after a single-pass
+      // convergence drop the measured slack (less a safety degree), else the
+      // total degree this iteration needed
+      if (!rerun && msucc > 0)
+        st->mhint = (passes == 1 && converged == 1 && fails == 0)
+                        ? max(2, msucc - max(0, slack - PDSDP_HINT_SAFETY))
+                        : msucc;
       st->iav = iav;
       st->ed2 = ed2_tot;
       st->corr = s.red1[0];
