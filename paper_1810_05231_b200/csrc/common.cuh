@@ -21,6 +21,7 @@
 #define PDSDP_RED_MAX (2 * PDSDP_BMAX * PDSDP_BMAX + 64)
 #define PDSDP_OUT_LEN 16       // doubles per instance and step in the host-mapped output
 #define PDSDP_KMAX 64          // iterations per pdsdp_iterate_many call
+#define PDSDP_NDMAX 2          // dense rank-one constraint rows handled as vectors
 
 namespace pdsdp {
 
@@ -67,7 +68,13 @@ struct Inst {
   int n, m, p, mp, ld, C;
   int nz;              // slots of the symmetric Z CSR
   int group;           // lanes per constraint row in the A-map
+  int nd;              // low-rank dense constraint rows (D = sig u u^T), kept out of the CSR
+  int drow[PDSDP_NDMAX];
   int pad0;
+  double dsig[PDSDP_NDMAX];                 // sign sigma of each dense row
+  double dun2[PDSDP_NDMAX];                 // ||u||^2
+  double duu[PDSDP_NDMAX * PDSDP_NDMAX];    // (u_k^T u_l)^2
+  const double* du;    // [nd][n] the vectors u
   const int* zptr;     // [n+1]
   const int* zcol;     // [nz]
   const int* zrow;     // [nz]

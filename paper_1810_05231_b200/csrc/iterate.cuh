@@ -769,9 +769,18 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     double th = (!cold && i < b_old) ? st->theta[i] : 0.0;
     s.theta[i] = th;
     s.lamF[i] = rerun ? st->lamF[i] : ((i < rF && th > 0.0) ? th : 0.0);
+    // dense rank-one rows ride along as extra factor columns of S:
+    // -alpha * sig * y_k[row] * u u^T  (column rF + q of F holds u)
+    if (i >= rF && i < rF + d.nd) {
+      const double* yk0 = (ctl.ypar & 1) ? d.ybuf1 : d.ybuf0;
+      const int q = i - rF;
+      s.lamF[i] = -d.alpha * d.dsig[q] * yk0[d.drow[q]];
+    }
     s.res[i] = (!cold && i < b_old) ? st->res[i] : 1.0e300;
   }
+  if (tid == 0 && s.own && rF + d.nd > s.sld) s.own = 0;
   __syncthreads();
+  const int rFx = rF + d.nd;       // factor columns of the operator S = F_x diag(lamF) F_x^T - alpha Z
   const double lo = st->lo_par[ctl.ypar & 1];
   const double alpha = d.alpha;
   const double* zv = (ctl.ypar & 1) ? d.zbuf1 : d.zbuf0;     // Z_k  = C + M^T y_k
@@ -791,6 +800,12 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = (s.lamF[j] != 0.0) ? Vr[j] : 0.0;
     if (s.own && j < rF) s.SF[(size_t)(rho - x.r0) * s.sld + j] = rerun ? d.F[(size_t)rho * ld + j] : ((s.lamF[j] != 0.0) ? Vr[j] : 0.0);
     if (j >= b_old) Vr[j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
+  }
+  for (int it = tid; it < (x.r1 - x.r0) * d.nd; it += blockDim.x) {
+    const int rho = x.r0 + it / d.nd, q = it % d.nd;
+    const double u = d.du[(size_t)q * n + rho];
+    d.F[(size_t)rho * ld + rF + q] = u;
+    if (s.own) s.SF[(size_t)(rho - x.r0) * s.sld + rF + q] = u;
   }
   __syncthreads();
   if (x.c == 0 && tid < PDSDP_BMAX) st->lamF[tid] = s.lamF[tid];
@@ -883,13 +898,13 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             __syncthreads();
             ycp = 1;
           } else {
-            operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase);
+            operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step_own(d, x, s, zv, buf(io), c0, bc, rF, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase);
+          operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase);
           ++matvecs;
           sg = sn;
         }
@@ -918,13 +933,13 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
               buf(io)[o] = fma(ca, buf(iav)[o], cb * d.V[o]);
             }
           } else {
-            operator_step(d, x, s, zv, d.V, nullptr, buf(io), c0, bc, rF, nlock, ca, cb, 0.0, pf);
+            operator_step(d, x, s, zv, d.V, nullptr, buf(io), c0, bc, rFx, nlock, ca, cb, 0.0, pf);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step(d, x, s, zv, buf(iy), buf(iyp < 0 ? 0 : iyp), buf(io), c0, bc, rF, nlock, ca, cb, cd, pf);
+          operator_step(d, x, s, zv, buf(iy), buf(iyp < 0 ? 0 : iyp), buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf);
           ++matvecs;
           sg = sn;
         }
@@ -951,10 +966,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       double* slot = red_slot(d, x, x.c);
       prof_mark(pf, 1);
       gram_mma(buf(iy), b, buf(iy), b, ld, x.r0, x.r1, slot, s.gsc);
-      gram_mma(d.F, rF, buf(iy), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
+      gram_mma(d.F, rFx, buf(iy), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
       // reduce into A (G1) and T
       cg::this_cluster().sync();
-      const int q = b * b + rF * b;
+      const int q = b * b + rFx * b;
       for (int i = tid; i < q; i += blockDim.x) {
         const double acc = cluster_sum(d, x, i, false);
         if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
@@ -963,10 +978,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       x.par ^= 1;
       __syncthreads();
     }
-    scale_T(s, rF, 0, b);
+    scale_T(s, rFx, 0, b);
     prof_mark(pf, 3);
-    if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rF, 0, 1.0, 0.0, 0.0);
-    else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rF, 0, 1.0, 0.0, 0.0);
+    if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
+    else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
     prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
@@ -1108,6 +1123,32 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   const double* yk = ctl.ypar ? d.ybuf1 : d.ybuf0;
   double* yn = ctl.ypar ? d.ybuf0 : d.ybuf1;
   const int rN = (r < b) ? r : b;
+  // dense rank-one rows: <D, X> = sig u^T X u from p = V^T u (X+) and q = F^T u (X_k)
+  __shared__ double dsum_sm[2 * PDSDP_NDMAX];   // [2q]: sig u^T(2X+ - X)u, [2q+1]: sig u^T(X+ - X)u
+  if (d.nd > 0) {
+    const int nq = rN + rF, qt = d.nd * nq;
+    const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    double* slot = red_slot(d, x, x.c);
+    for (int o = warp; o < qt; o += nw) {
+      const int q = o / nq, l = o % nq;
+      const double* U = (l < rN) ? d.V + l : d.F + (l - rN);
+      const double* u = d.du + (size_t)q * n;
+      double a = 0.0;
+      for (int rho = x.r0 + lane; rho < x.r1; rho += 32) a = fma(U[(size_t)rho * ld], u[rho], a);
+      a = warp_sum(a);
+      if (lane == 0) slot[o] = a;
+    }
+    __syncthreads();
+    cluster_reduce(d, x, qt, 0, s.red1);
+    if (tid < d.nd) {
+      double xn = 0.0, xo = 0.0;
+      for (int l = 0; l < rN; ++l) { const double pv = s.red1[tid * nq + l]; xn = fma(s.lamN[l] * pv, pv, xn); }
+      for (int l = 0; l < rF; ++l) { const double qv = s.red1[tid * nq + rN + l]; xo = fma(s.lamF[l] * qv, qv, xo); }
+      dsum_sm[2 * tid] = d.dsig[tid] * (2.0 * xn - xo);
+      dsum_sm[2 * tid + 1] = d.dsig[tid] * (xn - xo);
+    }
+    __syncthreads();
+  }
   double ed2 = 0.0, fin = 1.0;
   {
     const int G = d.group;
@@ -1135,6 +1176,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         sd += __shfl_down_sync(0xffffffffu, sd, o, G);
       }
       if (i < a1 && sub == 0) {
+        for (int q = 0; q < d.nd; ++q)
+          if (i == d.drow[q]) { s2 = dsum_sm[2 * q]; sd = dsum_sm[2 * q + 1]; }
         const double u = yk[i] + alpha * s2;
         const double pr = (i < d.m) ? d.bv[i] : fmin(u / alpha, d.hv[i - d.m]);
         const double ynew = u - alpha * pr;
@@ -1172,6 +1215,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   prof_mark(pf, 7);
   // ---------------- adjoint gather: Z_{k+1} = C + M^T y+, support correction ----------------
   double corr = 0.0;
+  double cu[PDSDP_NDMAX] = {0.0, 0.0};   // <M^T dy (sparse part), u u^T> per dense row
   {
     const int e0 = d.zptr[x.r0], e1 = d.zptr[x.r1];
     for (int e = e0 + tid; e < e1; e += blockDim.x) {
@@ -1193,6 +1237,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         const double v = (xn - xo) / alpha;
         const double w = (i == j) ? 1.0 : 2.0;
         corr = fma(w * a, a - 2.0 * v, corr);
+        for (int q = 0; q < d.nd; ++q) cu[q] = fma(w * a, d.du[(size_t)q * n + i] * d.du[(size_t)q * n + j], cu[q]);
       }
     }
   }
@@ -1208,18 +1253,41 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     double g = gmax;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
-    if ((tid & 31) == 0) { s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = g; }
+    double cw[PDSDP_NDMAX];
+    for (int q = 0; q < d.nd; ++q) cw[q] = warp_sum(cu[q]);
+    if ((tid & 31) == 0) {
+      s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = g;
+      for (int q = 0; q < d.nd; ++q) s.scr[64 + 32 * q + (tid >> 5)] = cw[q];
+    }
     __syncthreads();
     if (tid == 0) {
       double a = 0.0, gg = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; gg = fmax(gg, s.scr[32 + w]); }
       double* slot = red_slot(d, x, x.c);
       slot[0] = a;
-      slot[1] = gg;
+      for (int q = 0; q < d.nd; ++q) {
+        double c = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += s.scr[64 + 32 * q + w];
+        slot[1 + q] = c;
+      }
+      slot[1 + d.nd] = gg;
     }
     __syncthreads();
   }
-  cluster_reduce(d, x, 1, 1, s.red1);
+  cluster_reduce(d, x, 1 + d.nd, 1, s.red1);
+  // dense rank-one rows: their share of the primal residual and of the
+  // Gershgorin bound.  With A = M^T dy = A_s + sum_q dlt_q u_q u_q^T,
+  // dlt_q = sig_q dy_q and V = dX / alpha:
+  //   ||A||^2 - 2<A, V> = corr_s + sum_q (2 dlt_q <A_s, u_q u_q^T> - 2 dy_q sig_q u_q^T dX u_q / alpha)
+  //                       + sum_{q,l} dlt_q dlt_l (u_q^T u_l)^2
+  // and lambda_max(Z+) <= gersh(Z_s) + sum_q max(0, sig_q y+_q) ||u_q||^2.
+  double corr_tot = s.red1[0], gmax_tot = s.red1[1 + d.nd];
+  for (int q = 0; q < d.nd; ++q) {
+    const double dyq = d.dy[d.drow[q]], dlt = d.dsig[q] * dyq;
+    corr_tot += 2.0 * dlt * s.red1[1 + q] - 2.0 * dyq * dsum_sm[2 * q + 1] / alpha;
+    for (int l = 0; l < d.nd; ++l) corr_tot += dlt * d.dsig[l] * d.dy[d.drow[l]] * d.duu[q * PDSDP_NDMAX + l];
+    gmax_tot += fmax(0.0, d.dsig[q] * yn[d.drow[q]]) * d.dun2[q];
+  }
 
   // ---------------- epilogue: state for the next iteration + scalars ----------------
   prof_mark(pf, 0);
@@ -1244,8 +1312,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
                         : msucc;
       st->iav = iav;
       st->ed2 = ed2_tot;
-      st->corr = s.red1[0];
-      st->lo_par[(ctl.ypar & 1) ^ 1] = -alpha * s.red1[1];
+      st->corr = corr_tot;
+      st->lo_par[(ctl.ypar & 1) ^ 1] = -alpha * gmax_tot;
       st->finite = fin_tot;
       double* o = d.out + step * PDSDP_OUT_LEN;
       o[O_LAM] = s.theta[k - 1];
@@ -1255,7 +1323,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       o[O_EIGCONV] = converged;
       o[O_EIGRES] = maxres;
       o[O_ED2] = ed2_tot;
-      o[O_CORR] = s.red1[0];
+      o[O_CORR] = corr_tot;
       o[O_BLK] = b;
     }
   }

@@ -60,6 +60,11 @@ struct Instance {
   // host copies of the re-indexed problem
   std::vector<int> zptr, zcol, zrow, tptr, trow, aptr, ai, aj;
   std::vector<double> cval, tcoef, ag, bv, hv;
+  // dense rank-one constraint rows  D_r = sig u u^T  (kept out of the CSR)
+  int nd = 0;
+  int drow[PDSDP_NDMAX] = {0};
+  double dsig[PDSDP_NDMAX] = {0}, dun2[PDSDP_NDMAX] = {0}, duu[PDSDP_NDMAX * PDSDP_NDMAX] = {0};
+  std::vector<double> du;
   // operator-norm T-space
   std::vector<long long> tpos;
   std::vector<int> o_seg_lo, o_seg_hi, o_row_seg, o_mcol, o_tptr, o_trow;
@@ -131,25 +136,91 @@ int build_instance(const pdsdp_problem& pr, Instance& I) {
         return fail(PDSDP_EINVAL, "indices must be strictly increasing");
     }
   }
-  // ---- support = nonzeros of C  U  positions of all constraint entries ----
+  // ---- dense rank-one rows: a row whose matrix D (D_ii = a, D_ij = a/sqrt 2,
+  //      the adjoint's scatter coefficients) is exactly sig u u^T is applied
+  //      through u: M^T y gets y sig u u^T, <D, X> = sig u^T X u.  Its n^2/2
+  //      entries would otherwise turn Z into a dense matrix (an equipartition
+  //      row <11^T, X> = 0, BASELINE configs[2]). ----
+  std::vector<char> dense(mp, 0);
+  I.nd = 0;
+  I.du.clear();
+  for (int r = 0; r < mp && I.nd < PDSDP_NDMAX; ++r) {
+    const long long a0 = pr.row_ptr[r], a1 = pr.row_ptr[r + 1];
+    if (a1 - a0 < std::max<long long>(2LL * n, 64)) continue;
+    std::vector<double> dg(n, 0.0), col(n, 0.0);
+    double dmax = 0.0;
+    for (long long e = a0; e < a1; ++e) {
+      int i, j;
+      coords(pr.row_idx[e], i, j);
+      const double v = (i == j) ? pr.row_val[e] : pr.row_val[e] / std::sqrt(2.0);
+      if (i == j) dg[i] = v;
+      dmax = std::max(dmax, std::fabs(v));
+    }
+    int piv = 0;
+    for (int i = 1; i < n; ++i) if (std::fabs(dg[i]) > std::fabs(dg[piv])) piv = i;
+    if (dg[piv] == 0.0 || !std::isfinite(dmax)) continue;
+    for (long long e = a0; e < a1; ++e) {
+      int i, j;
+      coords(pr.row_idx[e], i, j);
+      const double v = (i == j) ? pr.row_val[e] : pr.row_val[e] / std::sqrt(2.0);
+      if (j == piv) col[i] = v;
+      if (i == piv) col[j] = v;
+    }
+    const double sg = dg[piv] > 0.0 ? 1.0 : -1.0, sq = std::sqrt(std::fabs(dg[piv]));
+    std::vector<double> u(n);
+    long long nzu = 0;
+    for (int i = 0; i < n; ++i) { u[i] = col[i] / (sg * sq); if (u[i] != 0.0) ++nzu; }
+    bool ok = true;
+    long long nzv = 0;
+    for (long long e = a0; e < a1 && ok; ++e) {
+      int i, j;
+      coords(pr.row_idx[e], i, j);
+      const double v = (i == j) ? pr.row_val[e] : pr.row_val[e] / std::sqrt(2.0);
+      if (v == 0.0) continue;
+      ++nzv;
+      if (std::fabs(v - sg * u[i] * u[j]) > 1e-13 * dmax) ok = false;
+    }
+    if (!ok || nzv != nzu * (nzu + 1) / 2) continue;   // every pair with u_i u_j != 0 present
+    dense[r] = 1;
+    I.drow[I.nd] = r;
+    I.dsig[I.nd] = sg;
+    double n2 = 0.0;
+    for (int i = 0; i < n; ++i) n2 += u[i] * u[i];
+    I.dun2[I.nd] = n2;
+    I.du.insert(I.du.end(), u.begin(), u.end());
+    ++I.nd;
+  }
+  for (int k = 0; k < I.nd; ++k)
+    for (int l = 0; l < I.nd; ++l) {
+      double g = 0.0;
+      for (int i = 0; i < n; ++i) g += I.du[(size_t)k * n + i] * I.du[(size_t)l * n + i];
+      I.duu[k * PDSDP_NDMAX + l] = g * g;
+    }
+  if (I.nd) I.ld = (std::min(n, PDSDP_BMAX) + I.nd + 1) & ~1;   // F holds the u's after its rF columns
+  // ---- support = nonzeros of C  U  positions of all (sparse) constraint entries ----
   std::vector<int> sid(P, -1);
   std::vector<long long> spos;
   {
     std::vector<unsigned char> mark(P, 0);
     for (long long q = 0; q < P; ++q) if (pr.C_packed[q] != 0.0) mark[q] = 1;
-    for (long long e = 0; e < nnz; ++e) mark[pr.row_idx[e]] = 1;
+    for (int r = 0; r < mp; ++r)
+      if (!dense[r])
+        for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) mark[pr.row_idx[e]] = 1;
     for (long long q = 0; q < P; ++q) if (mark[q]) { sid[q] = (int)spos.size(); spos.push_back(q); }
   }
   const long long U = (long long)spos.size();
   // contributors per support entry
   std::vector<int> ccount(U + 1, 0);
-  for (long long e = 0; e < nnz; ++e) ccount[sid[pr.row_idx[e]] + 1]++;
+  for (int r = 0; r < mp; ++r)
+    if (!dense[r])
+      for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) ccount[sid[pr.row_idx[e]] + 1]++;
   for (long long u = 0; u < U; ++u) ccount[u + 1] += ccount[u];
-  std::vector<int> crow(nnz);
-  std::vector<double> ccoef(nnz);
+  std::vector<int> crow(ccount[U]);
+  std::vector<double> ccoef(ccount[U]);
   {
     std::vector<int> fillp(ccount.begin(), ccount.end() - 1);
     for (int r = 0; r < mp; ++r)
+      if (!dense[r])
       for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) {
         int i, j;
         coords(pr.row_idx[e], i, j);
@@ -198,18 +269,21 @@ int build_instance(const pdsdp_problem& pr, Instance& I) {
     int o = I.tptr[s];
     for (int c = ccount[u]; c < ccount[u + 1]; ++c, ++o) { I.trow[o] = crow[c]; I.tcoef[o] = ccoef[c]; }
   }
-  // ---- constraint rows in dense coordinates ----
-  I.aptr.resize(mp + 1);
-  I.ai.resize(nnz); I.aj.resize(nnz); I.ag.resize(nnz);
+  // ---- constraint rows in dense coordinates (dense rank-one rows left empty) ----
+  I.aptr.assign(mp + 1, 0);
+  I.ai.clear(); I.aj.clear(); I.ag.clear();
   int maxrow = 0;
-  for (int r = 0; r <= mp; ++r) I.aptr[r] = mp ? (int)pr.row_ptr[r] : 0;
-  for (long long e = 0; e < nnz; ++e) {
-    int i, j;
-    coords(pr.row_idx[e], i, j);
-    I.ai[e] = i; I.aj[e] = j;
-    I.ag[e] = (i == j) ? pr.row_val[e] : pr.row_val[e] * std::sqrt(2.0);
+  for (int r = 0; r < mp; ++r) {
+    if (!dense[r])
+      for (long long e = pr.row_ptr[r]; e < pr.row_ptr[r + 1]; ++e) {
+        int i, j;
+        coords(pr.row_idx[e], i, j);
+        I.ai.push_back(i); I.aj.push_back(j);
+        I.ag.push_back((i == j) ? pr.row_val[e] : pr.row_val[e] * std::sqrt(2.0));
+      }
+    I.aptr[r + 1] = (int)I.ai.size();
+    maxrow = std::max(maxrow, I.aptr[r + 1] - I.aptr[r]);
   }
-  for (int r = 0; r < mp; ++r) maxrow = std::max(maxrow, I.aptr[r + 1] - I.aptr[r]);
   I.group = 1;
   while (I.group < maxrow && I.group < 32) I.group <<= 1;
   I.bv.assign(pr.b, pr.b + m);
@@ -279,6 +353,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   add(I.o_tval.size() * 8 + 8); add(I.tpos.size() * 8 + 8); add(I.mp * 8 + 8); add(nseg * 8 + 8);
   add(NORM_BLOCKS * 8); add(64); add(4096 * 8);
   add((size_t)I.P * 8);
+  add(I.du.size() * 8 + 8);
   bytes += 4096;
   CK(cudaMalloc(&I.dmem, bytes));
   I.dbytes = bytes;
@@ -287,6 +362,9 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   Inst& d = I.desc;
   d.n = I.n; d.m = I.m; d.p = I.p; d.mp = I.mp; d.ld = I.ld; d.C = C;
   d.nz = (int)I.nz; d.group = I.group;
+  d.nd = I.nd;
+  for (int k = 0; k < PDSDP_NDMAX; ++k) { d.drow[k] = I.drow[k]; d.dsig[k] = I.dsig[k]; d.dun2[k] = I.dun2[k]; }
+  for (int k = 0; k < PDSDP_NDMAX * PDSDP_NDMAX; ++k) d.duu[k] = I.duu[k];
   int rc;
   int* zptr; int* zcol; int* zrow; double* cval; int* tptr; int* trow; double* tcoef;
   if ((rc = upload(a, zptr, I.zptr))) return rc;
@@ -356,6 +434,9 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   o.scal = a.take<double>(8);
   o.s_hist = a.take<double>(4096);
   I.d_packed = a.take<double>((size_t)I.P);
+  double* du;
+  if ((rc = upload(a, du, I.du))) return rc;
+  d.du = du;
   if (a.off > bytes) return fail(PDSDP_ENOMEM, "arena overflow");
   return PDSDP_OK;
 }

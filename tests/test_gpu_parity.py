@@ -173,6 +173,44 @@ def test_oracle_parity_with_inequalities(rng):
         assert rel(res.y, ref.y) <= ITER_TOL
 
 
+def _rank_one_row(n, u, sig):
+    return pk.SparseRow.from_matrix_entries(
+        n, [(i, j, sig * u[i] * u[j]) for i in range(n) for j in range(i, n) if u[i] * u[j] != 0.0])
+
+
+def test_dense_rank_one_rows_match_oracle(rng):
+    """Dense constraint rows whose matrix is sig u u^T are applied through u on
+    the device (equipartition's <11^T, X> = 0, BASELINE configs[2]); the
+    results must not depend on that.  Covers sig = -1, a u with zeros (a dense
+    sub-block), two such rows, and a dense rank-two row that stays in the CSR."""
+    n = 90
+    prob = workloads.equipartition_problem(n, 0.08, 5)
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=200, initial_rank=4)
+    res = pk.solve_lr_pd_sdp(prob, cfg)
+    ref = orc.solve_lr(prob, cfg)
+    assert res.iterations == ref.iterations and res.rank_path == ref.rank_path
+    assert rel(res.X.data, ref.X) <= ITER_TOL
+    assert rel(res.y, ref.y) <= ITER_TOL
+    np.testing.assert_allclose(res.final_residuals, ref.final_residuals, rtol=1e-7)
+
+    g = workloads.random_graph(n, 0.1, 9, signed=True)
+    C = pk.SymMatrix(n, workloads.laplacian_packed(g, -0.25))
+    u1 = rng.standard_normal(n)
+    u2 = np.where(np.arange(n) < n // 2, 1.0 + rng.random(n), 0.0)
+    w1, w2 = rng.standard_normal(n), rng.standard_normal(n)
+    rank2 = pk.SparseRow.from_matrix_entries(
+        n, [(i, j, w1[i] * w1[j] - w2[i] * w2[j]) for i in range(n) for j in range(i, n)])
+    rows = workloads.diag_pin_rows(n) + [_rank_one_row(n, u1, -1.0), _rank_one_row(n, u2, 1.0), rank2]
+    prob = pk.SdpProblem(n=n, C=C, A=rows, b=np.concatenate([np.ones(n), [-0.5, 2.0, 0.1]]))
+    cfg = SolverConfig(eps_tol=1e-6, max_iter=120, initial_rank=3, window_ell=60)
+    res = pk.solve_lr_pd_sdp(prob, cfg)
+    ref = orc.solve_lr(prob, cfg)
+    assert res.iterations == ref.iterations and res.rank_path == ref.rank_path
+    assert rel(res.X.data, ref.X) <= ITER_TOL
+    assert rel(res.y, ref.y) <= ITER_TOL
+    np.testing.assert_allclose(res.final_residuals, ref.final_residuals, rtol=1e-7)
+
+
 # ---------------------------------------------------------------- edge cases
 
 def test_oversized_steps_follow_reference():
