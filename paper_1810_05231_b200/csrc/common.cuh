@@ -32,7 +32,8 @@ struct State {
   int iav;          // physical buffer (1..4) holding S*V
   int rF_used;      // columns of F (= X_k) used by the last iteration
   int r_cur;        // columns of V (= X_k+1) produced by the last iteration
-  int pad0, pad1;
+  int npos;         // positive kept Ritz values of the last iteration (effective-rank hint)
+  int pad1;
   double theta[PDSDP_BMAX];
   double res[PDSDP_BMAX];
   double lamF[PDSDP_BMAX];   // eigenvalues of X_k   (clipped)
@@ -124,7 +125,7 @@ struct Ctl {
 
 // output slots
 enum { O_EPS_P = 0, O_EPS_D, O_LAM, O_FIN, O_PASSES, O_MATVECS, O_EIGCONV, O_EIGRES,
-       O_DENSE, O_CORR, O_ED2, O_BLK, O_DONE };
+       O_DENSE, O_CORR, O_ED2, O_BLK, O_DONE, O_ERR };
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

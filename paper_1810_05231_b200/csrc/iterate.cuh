@@ -38,6 +38,9 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
                                        double scale, double xnorm, double cert_tol) {
   const double th = theta[i];
   if (!(ri == ri) || !(th == th)) return true;          // non-finite: give up, reported as such
+  // sentinel of an effective-rank block: only its sign matters -- the
+  // eigenvalue within its residual must be negative (with margin)
+  if (i == r && cert_tol < 0.0) return th < 0.0 && ri <= 0.1 * -th;
   // clipped / certificate passes -- only trusted once the pair is nearly
   // invariant (a Ritz value of an unconverged block can sit far below the
   // eigenvalue it will converge to)
@@ -50,7 +53,9 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
     const double impact = ri + 2.0 * fmax(th, 0.0) * fmin(1.0, ri / fmax(gap, 1e-300));
     return impact <= PDSDP_TOL_X * xnorm;
   }
-  return cert_tol <= 0.0 || ri <= cert_tol * scale;
+  // cert_tol < 0: sentinel column of an effective-rank block -- it must be
+  // certified non-positive (the clip rule above), its value is not needed
+  return cert_tol == 0.0 || (cert_tol > 0.0 && ri <= cert_tol * scale);
 }
 
 struct Sm {
@@ -621,7 +626,8 @@ __device__ Assess assess(const double* theta, const double* res, int r, int b, i
     const double lo_k = theta[r - 1] - 2.0 * res[r - 1];
     const double hi_t = theta[r] + 2.0 * res[r];
     if (!(hi_t < lo_k) && res[r] > PDSDP_TOL_CERT * scale &&
-        !(theta[r] + res[r] < 0.0 && res[r] <= PDSDP_TOL_CLIP * scale)) {
+        !(theta[r] + res[r] < 0.0 && res[r] <= PDSDP_TOL_CLIP * scale) &&
+        !(cert_tol < 0.0 && theta[r] < 0.0 && res[r] <= 0.1 * -theta[r])) {
       a.tail_bad = true;
       a.maxres = fmax(a.maxres, res[r] / scale);
     }
@@ -751,16 +757,30 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   // accurate (checkpoint iterations); bit2 re-run of the last iteration from
   // the same (X_k, y_k) (F, lamF, Z_k kept) -- used when a checkpoint turns up
   // in an iteration that ran without bit1.
-  const int r = ctl.r;
-  const int k = (r + 1 < n) ? r + 1 : n;
+  // Effective rank: X+ keeps only positive eigenpairs among the top r, so
+  // when S has far fewer than r positive eigenvalues the block only needs
+  // them plus one "sentinel" pair certified non-positive -- then lambda_{r+1}
+  // <= sentinel <= 0 and the certificate (n-r) max(lambda_{r+1}, 0) is 0, as
+  // in the reference.  The block grows in-kernel whenever the sentinel's Ritz
+  // value is positive (Cauchy interlacing: theta_i <= lambda_i).
+  const int r_t = ctl.r;
+  const bool tight = (ctl.flags & 8) != 0;
+  int r = r_t;
+  {
+    const int np = st->npos;
+    if (!tight && (r_t >= np + 8 || min(r_t + 1, n) > lcap)) r = min(r_t, np + 2);
+  }
+  int k = (r + 1 < n) ? r + 1 : n;
   const bool need_cert = (ctl.flags & 2) != 0;
   // bit3: certificate eigenpair to the kept-pair tolerance (op-level aproj_psd)
-  const double cert_tol = need_cert ? ((ctl.flags & 8) ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) : 0.0;
+  const double cert_tol0 = need_cert ? ((ctl.flags & 8) ? PDSDP_TOL_KEEP : PDSDP_TOL_CERT) : 0.0;
+  double cert_tol = (r < r_t) ? -1.0 : cert_tol0;
   const bool rerun = (ctl.flags & 4) != 0;
   const bool cold = !rerun && ((ctl.flags & 1) || st->b == 0);
   const int rF = cold ? 0 : (rerun ? st->rF_used : st->rF);
   const int b_old = cold ? 0 : st->b;
   int b = choose_block(k, n);
+  if (b > lcap) b = lcap;
   if (b < b_old) b = b_old;
   int iav = cold ? 1 : st->iav;   // physical buffer holding AV
   if (iav < 1 || iav > 4) iav = 1;
@@ -809,7 +829,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   }
   __syncthreads();
   if (x.c == 0 && tid < PDSDP_BMAX) st->lamF[tid] = s.lamF[tid];
-  if (x.c == 0 && tid == 0) { st->rF_used = rF; st->r_cur = r; }
+  if (x.c == 0 && tid == 0) st->rF_used = rF;
+  int grow_err = 0, since_grow = 0;
 
   // ---------------- eigensolver: warm-started Chebyshev-filtered subspace iteration ----
   bool av_valid = false;
@@ -849,7 +870,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       } else if (as.cert_bad || as.tail_bad) {
         // kept pairs converged: lock (deflate) them and filter the tail
         nlock = r; c0 = r; bc = b - r;
-        const double rr = s.res[r] / fmax(fmax(cert_tol, PDSDP_TOL_CERT * 1e-4) * scale, 1e-300);
+        const double ct = (cert_tol < 0.0) ? 0.05 * fabs(s.theta[r]) / scale
+                                            : fmax(cert_tol, PDSDP_TOL_CERT * 1e-4);
+        const double rr = s.res[r] / fmax(ct * scale, 1e-300);
         mcap = cheb_plan(s.theta, b, lo, s.theta[r], s.theta[b - 1], s.theta[r], rr, scale, eps_rel, m, fe, fc, sig1);
         if (m > mcap) m = mcap;
       }
@@ -859,7 +882,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const int last_bad = as.last_bad;
       if (x.c == 0 && tid == 0 && pass < 32) {
         double* g = st->dbg[pass];
-        g[0] = m; g[1] = maxres; g[2] = last_bad; g[3] = c0; g[4] = bc; g[5] = lo; g[6] = fc - fe;
+        g[0] = m; g[1] = maxres; g[2] = last_bad; g[3] = c0 + 1000.0 * r; g[4] = bc + 1000.0 * b; g[5] = lo; g[6] = fc - fe;
         g[7] = xnorm;
       }
     }
@@ -1093,6 +1116,36 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
       const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
       maxres = as.maxres;
+      ++since_grow;
+      if (r < r_t) {
+        // effective-rank block: grow when the sentinel is positive, or when it
+        // will not certify (an eigenvalue at ~0 -- move the sentinel deeper)
+        int np = 0;
+        for (int i = 0; i < b; ++i) np += (s.theta[i] > 0.0) ? 1 : 0;
+        const bool sent_ok = s.theta[r] < 0.0 && s.res[r] <= 0.1 * -s.theta[r];
+        if (s.theta[r] > 0.0 || (!sent_ok && since_grow >= 4)) {
+          const int rn = min(r_t, max(np + 2, r + 4));
+          const int kn = min(rn + 1, n);
+          if (kn > lcap) { grow_err = 1; break; }
+          int bn = choose_block(kn, n);
+          if (bn > lcap) bn = lcap;
+          if (bn < b) bn = b;
+          __syncthreads();
+          for (int it = tid; it < (x.r1 - x.r0) * bn; it += blockDim.x) {
+            const int rho = x.r0 + it / bn, j = it % bn;
+            if (j >= b) d.V[(size_t)rho * ld + j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
+          }
+          for (int i = b + tid; i < bn; i += blockDim.x) { s.theta[i] = 0.0; s.res[i] = 1.0e300; }
+          r = rn; k = kn; b = bn;
+          cert_tol = (r < r_t) ? -1.0 : cert_tol0;
+          theta_valid = false;
+          av_valid = false;
+          since_grow = 0;
+          prev_maxres = 1.0e300;
+          __syncthreads();
+          continue;
+        }
+      }
       // a block that was not filtered in this pass (cold RR) is not trusted
       if (as.last_bad < 0 && !as.cert_bad && !as.tail_bad && (m > 0 || b >= n)) {
         converged = 1;
@@ -1302,6 +1355,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (tid == 0) {
       st->b = b;
       st->rF = rN;
+      st->r_cur = r;
+      int np = 0;
+      for (int i = 0; i < rN; ++i) np += (s.theta[i] > 0.0) ? 1 : 0;
+      st->npos = np;
       st->theta_valid = theta_valid ? 1 : 0;
       // degree hint for the next iteration's first pass: after a single-pass
       // convergence drop the measured slack (less a safety degree), else the
@@ -1325,6 +1382,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       o[O_ED2] = ed2_tot;
       o[O_CORR] = corr_tot;
       o[O_BLK] = b;
+      o[O_ERR] = grow_err;
+      if (grow_err) *d.stopf = 1;
     }
   }
 }

@@ -691,8 +691,12 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     Instance* I = b->inst[k];
     if (rank[a] < 1 || rank[a] > I->n)
       return fail(PDSDP_EINVAL, "rank r=" + std::to_string(rank[a]) + " outside [1, " + std::to_string(I->n) + "]");
-    const int kk = std::min(rank[a] + 1, I->n);
-    if (kk > PDSDP_BMAX) return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + " needs an eigen block above 64");
+    // target ranks above the block limit run as effective-rank blocks (the
+    // positive eigenpairs plus a sentinel); the device reports when those do
+    // not fit either
+    if (flags && (flags[a] & 8) && std::min(rank[a] + 1, I->n) > PDSDP_BMAX)
+      return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + " needs an eigen block above 64");
+    const int kk = std::min(std::min(rank[a] + 1, I->n), PDSDP_BMAX);
     for (int j = 0; j < K; ++j) {
       Ctl& c = b->h_ctl[(size_t)k * PDSDP_KMAX + j];
       c.r = rank[a];
@@ -702,6 +706,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
       c.conv_thr = conv_thr ? conv_thr[a] : -1.0;
       c.stall_thr = stall_thr ? stall_thr[(size_t)a * K + j] : HUGE_VAL;
       b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_DONE] = 0.0;
+      b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_ERR] = 0.0;
     }
     b->h_active[a] = k;
     const int g = std::max(kk / 4, 4);
@@ -738,6 +743,9 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
       const double* src = b->h_out + ((size_t)insts[a] * PDSDP_KMAX + j) * PDSDP_OUT_LEN;
       memcpy(out + ((size_t)a * K + j) * PDSDP_OUT_LEN, src, PDSDP_OUT_LEN * sizeof(double));
       if (src[O_DONE] == 1.0) done = j + 1;
+      if (src[O_ERR] != 0.0)
+        return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + ": S has more positive eigenvalues than an eigen block of " +
+                                     std::to_string(PDSDP_BMAX) + " holds (PDSDP_BMAX)");
     }
     if (steps_done) steps_done[a] = done;
   }

@@ -247,10 +247,34 @@ def test_full_rank_and_tiny_problems():
     assert res.primal_objective == pytest.approx(ref.primal_objective, rel=OBJ_TOL)
 
 
+def test_target_rank_above_block_uses_positive_part():
+    """Target ranks beyond the eigen block (the rank doubling of a stalled
+    run, BASELINE configs[2]): only the positive eigenpairs plus a sentinel
+    are computed; X+, y and the certificate decisions match the oracle, which
+    uses dense eigh there (symmat.py:181-185)."""
+    prob = workloads.equipartition_problem(150, 0.05, 2)
+    for r0, K in ((100, 60), (150, 40), (70, 180)):   # X has 42 positive eigenpairs at k=180
+        cfg = SolverConfig(eps_tol=1e-4, max_iter=K, initial_rank=r0, window_ell=50)
+        res = pk.solve_lr_pd_sdp(prob, cfg)
+        ref = orc.solve_lr(prob, cfg)
+        assert res.iterations == ref.iterations and res.rank_path == ref.rank_path
+        assert rel(res.X.data, ref.X) <= ITER_TOL
+        assert rel(res.y, ref.y) <= ITER_TOL
+        np.testing.assert_allclose(res.final_residuals, ref.final_residuals, rtol=1e-7)
+
+
 def test_rank_above_block_limit_fails_loudly():
+    # S_1 = alpha L / 4 has ~n positive eigenvalues: more than one block holds
     prob = workloads.maxcut_problem(200, 0.1, 0, signed=False)
     with pytest.raises(ValueError, match="eigen block"):
         pk.solve_lr_pd_sdp(prob, SolverConfig(initial_rank=80, max_iter=2))
+    # the same run continued past 62 positive eigenpairs (reference: dense eigh)
+    prob = workloads.equipartition_problem(150, 0.05, 2)
+    with pytest.raises(ValueError, match="eigen block"):
+        pk.solve_lr_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=300, initial_rank=70, window_ell=50))
+    # op level: aproj_psd needs lambda_{r+1} itself, so r + 1 must fit the block
+    with pytest.raises(ValueError, match="eigen block"):
+        pk.aproj_psd(pk.SymMatrix.from_dense(np.eye(100)), 80)
 
 
 def test_time_limit_and_max_iter_status():

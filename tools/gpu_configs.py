@@ -7,12 +7,10 @@ from paper_1810_05231_b200 import workloads
 which = [int(a) for a in sys.argv[1:]] or [1, 4, 3]
 for idx in which:
     prob, cfg = workloads.config(idx)
-    if idx == 2:
-        cfg = pk.SolverConfig(**{**cfg.__dict__, "max_iter": 20})
     st = {}
     hist = []
     t = time.perf_counter()
-    cfg = pk.SolverConfig(**{**cfg.__dict__, "progress_every": 500})
+    cfg = pk.SolverConfig(**{**cfg.__dict__, "progress_every": 5000})
     res = pk.solve_lr_pd_sdp(prob, cfg, callback=lambda i: (hist.append(i), print("   ", i, flush=True)), stats=st)
     dt = time.perf_counter() - t
     print(f"cfg{idx+1}: {res.status} iters={res.iterations} obj={res.primal_objective:.10f} dobj={res.dual_objective:.10f} "
