@@ -64,6 +64,7 @@ struct Sm {
   double* ys;                  // staged operand block (n x ycw)
   double *SF, *SYc, *SYp;      // own rows of F (SYc/SYp unused)
   int* szp;                    // own rows of zptr
+  int* gb;                     // [C+1] first row of each CTA (multicast row groups)
   int own, sld;                // own-row buffers valid; their stride
   int ycap;                    // doubles in the staging buffer
   int ycw;                     // staged column chunk width (even; 0 = gather path)
@@ -451,41 +452,29 @@ __device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s
   else apply_rows(d, x, s, zv, Yin, Yprev, out, c0, bc, rF, nlock, ca, cb, cd);
 }
 
-// Operator step with the CTA's rows resident in shared memory: the Gram
-// partial reads F and Y_j from smem, the operand block is staged for all n
-// rows, and the result is written both to global (for the other CTAs) and
-// into the Y_{j-1} smem slot, which becomes Y_{j+1} (caller swaps SYc/SYp).
 // Operator step of the Chebyshev recurrence.  The operand block Y_j (active
-// columns, compact stride bcp, global buffer Yc[p]) is all-gathered inside the
-// cluster with TMA bulk multicast: every CTA broadcasts its own rows into every
-// CTA's staging buffer (one L2 read per row block), in row groups that fit the
-// buffer; each own row's Z slots of a group form a contiguous sub-range
-// (columns are sorted).  F's own rows stay in shared memory; the CTA's own
-// items of Y_j and Y_{j-1} are prefetched into registers.  Y_{j+1} goes to
+// columns, compact row stride bcp = bc rounded up to 4, global buffer Yc[p])
+// is all-gathered inside the cluster with TMA bulk multicast: every CTA
+// broadcasts its own rows into every CTA's staging buffer (one L2 read per
+// row block), in row groups that fit the buffer.  Work items are (own row,
+// 4-column chunk): each gathered Z slot feeds 4 FMAs from two 16-byte smem
+// loads, and a running slot pointer per item walks the row's (column-sorted)
+// slots group by group.  F's own rows stay in shared memory.  Y_{j+1} goes to
 // global row-major (for Rayleigh-Ritz) and into Yc[p^1] over Y_{j-1}.
+#define PDSDP_OWN_ITEMS 2      // (row, 4-column chunk) items per thread
+__device__ __forceinline__ int own_stride(int bc) { return (bc + 3) & ~3; }
+
 __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
                                                   double* out, int c0, int bc, int rF, int nlock,
                                                   double ca, double cb, double cd, Prof& pf,
                                                   int& ycp, unsigned long long* mbar, unsigned& mphase) {
   prof_mark(pf, 1);
   const int nl = x.r1 - x.r0, sl = s.sld, ld = d.ld, n = d.n, tid = threadIdx.x;
-  const int bcp = (bc + 1) & ~1;
-  const size_t nld = (size_t)n * ld;
+  const int bcp = own_stride(bc), nch = bcp >> 2;
+  const size_t nld = (size_t)n * (ld + 4);
   const double* Ycur = d.Yc + (size_t)ycp * nld;
   double* Ynxt = d.Yc + (size_t)(ycp ^ 1) * nld;
-  const int nitems = nl * bc;
-  double ycur[4], yprv[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int it = tid + u * blockDim.x;
-    ycur[u] = 0.0; yprv[u] = 0.0;
-    if (it < nitems) {
-      const int lr = it / bc, jj = it - lr * bc;
-      const size_t o = (size_t)(x.r0 + lr) * bcp + jj;
-      if (cb != 0.0) ycur[u] = __ldcg(Ycur + o);
-      if (cd != 0.0) yprv[u] = __ldcg(Ynxt + o);
-    }
-  }
+  const int nitems = nl * nch;
   double* slot = red_slot(d, x, x.c);
   gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
   gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
@@ -493,26 +482,36 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   prof_mark(pf, 2);
   cg::this_cluster().sync();                 // publishes Y_j rows and the partials
   const double alpha = d.alpha;
-  double* ys = s.ys;
+  const double* ys = s.ys;
   const int C = x.C;
   const int rows_cap = s.ycap / bcp;
   const unsigned short mask = (unsigned short)((1u << C) - 1u);
-  int g0 = 0;
-  bool first = true;
-  double zacc[4] = {0.0, 0.0, 0.0, 0.0};
   const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
   const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
   const int zoff = s.zstaged ? s.zoff : 0;
+  double zacc[PDSDP_OWN_ITEMS][4];
+  int ep[PDSDP_OWN_ITEMS], ee[PDSDP_OWN_ITEMS];
+#pragma unroll
+  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+    const int it = tid + u * blockDim.x;
+    const int lr = (it < nitems) ? it / nch : 0;
+    ep[u] = s.szp[lr] - zoff;
+    ee[u] = (it < nitems) ? s.szp[lr + 1] - zoff : ep[u];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) zacc[u][v] = 0.0;
+  }
+  int g0 = 0;
+  bool first = true;
   while (g0 < C) {
-    const int R0 = (int)(((long long)n * g0) / C);
+    const int R0 = s.gb[g0];
     int g1 = g0 + 1;
-    while (g1 < C && (int)(((long long)n * (g1 + 1)) / C) - R0 <= rows_cap) ++g1;
-    const int R1 = (int)(((long long)n * g1) / C);
+    while (g1 < C && s.gb[g1 + 1] - R0 <= rows_cap) ++g1;
+    const int R1 = s.gb[g1];
     if (tid == 0) {
       mbar_expect_tx(mbar, (unsigned)((R1 - R0) * bcp * 8));
       if (x.c >= g0 && x.c < g1) {
         const char* src = reinterpret_cast<const char*>(Ycur + (size_t)x.r0 * bcp);
-        char* dst = reinterpret_cast<char*>(ys + (size_t)(x.r0 - R0) * bcp);
+        char* dst = reinterpret_cast<char*>(s.ys + (size_t)(x.r0 - R0) * bcp);
         unsigned left = (unsigned)(nl * bcp * 8), off = 0;
         while (left > 0) {
           const unsigned piece = left > 65536u ? 65536u : left;
@@ -537,60 +536,59 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     mphase ^= 1u;
     __syncthreads();
     prof_mark(pf, 14);
-    const bool all = (R0 == 0 && R1 == n);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
       const int it = tid + u * blockDim.x;
       if (it >= nitems) break;
-      const int lr = it / bc, jj = it - lr * bc;
-      int e = s.szp[lr] - zoff, e1 = s.szp[lr + 1] - zoff;
-      if (!all) {
-        int lo = e, hi = e1;
-        while (lo < hi) { const int md = (lo + hi) >> 1; if (zcol[md] < R0) lo = md + 1; else hi = md; }
-        e = lo;
-        int lo2 = e; hi = e1;
-        while (lo2 < hi) { const int md = (lo2 + hi) >> 1; if (zcol[md] < R1) lo2 = md + 1; else hi = md; }
-        e1 = lo2;
+      const int cq = it % nch;
+      const double* yb = ys + 4 * cq - (size_t)R0 * bcp;
+      int e = ep[u];
+      const int e1 = ee[u];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (; e < e1; ++e) {
+        const int q = zcol[e];
+        if (q >= R1) break;
+        const double zv_ = zval[e];
+        const double2 p0 = *reinterpret_cast<const double2*>(yb + (size_t)q * bcp);
+        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q * bcp + 2);
+        a0 = fma(zv_, p0.x, a0); a1 = fma(zv_, p0.y, a1);
+        a2 = fma(zv_, p1.x, a2); a3 = fma(zv_, p1.y, a3);
       }
-      double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-      for (; e + 4 <= e1; e += 4) {
-        const int q0 = zcol[e] - R0, q1 = zcol[e + 1] - R0, q2 = zcol[e + 2] - R0, q3 = zcol[e + 3] - R0;
-        z0 = fma(zval[e], ys[(size_t)q0 * bcp + jj], z0);
-        z1 = fma(zval[e + 1], ys[(size_t)q1 * bcp + jj], z1);
-        z2 = fma(zval[e + 2], ys[(size_t)q2 * bcp + jj], z2);
-        z3 = fma(zval[e + 3], ys[(size_t)q3 * bcp + jj], z3);
-      }
-      for (; e < e1; ++e) z0 = fma(zval[e], ys[(size_t)(zcol[e] - R0) * bcp + jj], z0);
-      zacc[u] += (z0 + z1) + (z2 + z3);
+      ep[u] = e;
+      zacc[u][0] += a0; zacc[u][1] += a1; zacc[u][2] += a2; zacc[u][3] += a3;
     }
     g0 = g1;
     if (g0 < C) cg::this_cluster().sync();
     prof_mark(pf, 3);
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
     const int it = tid + u * blockDim.x;
     if (it >= nitems) break;
-    const int lr = it / bc, jj = it - lr * bc, j = c0 + jj;
+    const int lr = it / nch, cq = it - lr * nch;
     const double* Fr = s.SF + (size_t)lr * sl;
-    double w0 = 0.0, w1 = 0.0;
-    int l = 0;
-    for (; l + 2 <= rF; l += 2) {
-      w0 = fma(Fr[l], s.T[l * bc + jj], w0);
-      w1 = fma(Fr[l + 1], s.T[(l + 1) * bc + jj], w1);
-    }
-    if (l < rF) w0 = fma(Fr[l], s.T[l * bc + jj], w0);
-    double w = w0 + w1;
-    if (nlock) {
-      const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
+    const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
+    const size_t oc = (size_t)(x.r0 + lr) * bcp + 4 * cq;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int jj = 4 * cq + v;
+      if (jj >= bc) break;
+      double w0 = 0.0, w1 = 0.0;
+      int l = 0;
+      for (; l + 2 <= rF; l += 2) {
+        w0 = fma(Fr[l], s.T[l * bc + jj], w0);
+        w1 = fma(Fr[l + 1], s.T[(l + 1) * bc + jj], w1);
+      }
+      if (l < rF) w0 = fma(Fr[l], s.T[l * bc + jj], w0);
+      double w = w0 + w1;
       for (int t = 0; t < nlock; ++t) w = fma(Vr[t], s.T[(rF + t) * bc + jj], w);
+      w = fma(-alpha, zacc[u][v], w);
+      double o = ca * w;
+      if (cb != 0.0) o = fma(cb, __ldcg(Ycur + oc + v), o);
+      if (cd != 0.0) o = fma(cd, __ldcg(Ynxt + oc + v), o);
+      out[(size_t)(x.r0 + lr) * ld + c0 + jj] = o;
+      Ynxt[oc + v] = o;
     }
-    w = fma(-alpha, zacc[u], w);
-    double o = ca * w;
-    if (cb != 0.0) o = fma(cb, ycur[u], o);
-    if (cd != 0.0) o = fma(cd, yprv[u], o);
-    out[(size_t)(x.r0 + lr) * ld + j] = o;
-    Ynxt[(size_t)(x.r0 + lr) * bcp + jj] = o;
   }
   fence_proxy_async();
   __syncthreads();
@@ -663,7 +661,7 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
 inline size_t iterate_smem_bytes(int lds, int zcap, int ycap, int owncap, int nlmax) {
   return (size_t)(5 * lds * (lds + 1) + PDSDP_NTHR + 13 * PDSDP_BMAX + PDSDP_GRAM_SCR + zcap + ycap + owncap) *
              sizeof(double) +
-         (size_t)(3 * PDSDP_BMAX + 8 + zcap + (owncap ? nlmax + 2 : 0)) * sizeof(int) + 64;
+         (size_t)(3 * PDSDP_BMAX + 8 + 20 + zcap + (owncap ? nlmax + 2 : 0)) * sizeof(int) + 64;
 }
 
 __device__ int choose_block(int k, int n) {
@@ -731,6 +729,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.perm = ip; ip += PDSDP_BMAX; s.pq = ip; ip += 2 * PDSDP_BMAX; s.flag = ip; ip += 8;
     int* zc = ip; ip += zcap;
     s.szp = ip; ip += (owncap ? nlmax + 2 : 0);
+    s.gb = ip; ip += 20;
     s.zc = zc; s.zvs = zvs;
     s.zoff = d.zptr[x.r0];
     s.zstaged = (d.zptr[x.r1] - s.zoff) <= zcap ? 1 : 0;
@@ -740,8 +739,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.ycw = (cw >= 2) ? cw : 0;
     s.sld = lcap;
     s.ycap = ycap;
-    s.own = (owncap > 0 && (x.r1 - x.r0) * lcap <= owncap && (x.r1 - x.r0) <= nlmax &&
-             (x.r1 - x.r0) * lcap <= ycap && (x.r1 - x.r0) * lcap <= 4 * PDSDP_NTHR) ? 1 : 0;
+    {
+      const int nl = x.r1 - x.r0, sp = own_stride(lcap);
+      s.own = (owncap > 0 && nl * lcap <= owncap && nl <= nlmax && nl * sp <= ycap &&
+               nl * (sp / 4) <= PDSDP_OWN_ITEMS * PDSDP_NTHR) ? 1 : 0;
+    }
   }
   __shared__ __align__(8) unsigned long long mbar_sm;   // completion barrier of the operand all-gather
   if (threadIdx.x == 0) mbar_init(&mbar_sm, 1);
@@ -812,8 +814,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       ((double*)s.zvs)[e] = zv[s.zoff + e];
     }
   }
-  if (s.own)
+  if (s.own) {
     for (int lr = tid; lr <= x.r1 - x.r0; lr += blockDim.x) s.szp[lr] = d.zptr[x.r0 + lr];
+    for (int c = tid; c <= x.C; c += blockDim.x) s.gb[c] = (int)(((long long)n * c) / x.C);
+  }
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
     const int rho = x.r0 + it / b, j = it % b;
     double* Vr = d.V + (size_t)rho * ld;
@@ -895,8 +899,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (m > 0 && s.own) {
       // own rows of V (the recurrence's Y_0) into the compact multicast source
       const int nl = x.r1 - x.r0;
-      const int bcp = (bc + 1) & ~1;
-      const size_t nld = (size_t)n * ld;
+      const int bcp = own_stride(bc);
+      const size_t nld = (size_t)n * (ld + 4);
       int ycp = 0;
       for (int it = tid; it < nl * bc; it += blockDim.x) {
         const int lr = it / bc, jj = it - lr * bc;

@@ -343,7 +343,8 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   add(I.trow.size() * 4 + 4); add(I.tcoef.size() * 8 + 8); add(I.nz * 8); add(I.nz * 8);
   add((I.mp + 1) * 4); add(I.ai.size() * 4 + 4); add(I.aj.size() * 4 + 4); add(I.ag.size() * 8 + 8);
   add((C + 1) * 4); add(I.bv.size() * 8 + 8); add(I.hv.size() * 8 + 8);
-  for (int k = 0; k < 8; ++k) add(nld * 8);
+  for (int k = 0; k < 6; ++k) add(nld * 8);
+  add(2 * (size_t)I.n * (I.ld + 4) * 8);
   add(I.mp * 8 + 8); add(I.mp * 8 + 8); add(I.mp * 8 + 8);
   add((size_t)2 * C * PDSDP_RED_MAX * 8);
   add((size_t)I.ntile * 8 + 8); add(64); add(sizeof(State));
@@ -405,7 +406,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   d.bv = bv; d.hv = hv;
   d.V = a.take<double>(nld); d.AV = a.take<double>(nld); d.Y0 = a.take<double>(nld);
   d.Y1 = a.take<double>(nld); d.Y2 = a.take<double>(nld); d.F = a.take<double>(nld);
-  d.Yc = a.take<double>(2 * nld);
+  d.Yc = a.take<double>(2 * (size_t)I.n * (I.ld + 4));
   d.ybuf0 = a.take<double>(I.mp + 1); d.ybuf1 = a.take<double>(I.mp + 1); d.dy = a.take<double>(I.mp + 1);
   d.red = a.take<double>((size_t)2 * C * PDSDP_RED_MAX);
   d.rpart = a.take<double>(I.ntile + 1);
