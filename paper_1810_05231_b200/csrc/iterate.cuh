@@ -467,7 +467,8 @@ __device__ __forceinline__ int own_stride(int bc) { return (bc + 3) & ~3; }
 __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
                                                   double* out, int c0, int bc, int rF, int nlock,
                                                   double ca, double cb, double cd, Prof& pf,
-                                                  int& ycp, unsigned long long* mbar, unsigned& mphase) {
+                                                  int& ycp, unsigned long long* mbar, unsigned& mphase,
+                                                  bool& gram_ready, bool gram_next) {
   prof_mark(pf, 1);
   const int nl = x.r1 - x.r0, sl = s.sld, ld = d.ld, n = d.n, tid = threadIdx.x;
   const int bcp = own_stride(bc), nch = bcp >> 2;
@@ -475,10 +476,13 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const double* Ycur = d.Yc + (size_t)ycp * nld;
   double* Ynxt = d.Yc + (size_t)(ycp ^ 1) * nld;
   const int nitems = nl * nch;
-  double* slot = red_slot(d, x, x.c);
-  gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
-  gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
-            slot + rF * bc, s.gsc);
+  if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
+    double* slot = red_slot(d, x, x.c);
+    gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
+    gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
+              slot + rF * bc, s.gsc);
+  }
+  gram_ready = false;
   prof_mark(pf, 2);
   cg::this_cluster().sync();                 // publishes Y_j rows and the partials
   const double alpha = d.alpha;
@@ -588,10 +592,29 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       if (cd != 0.0) o = fma(cd, __ldcg(Ynxt + oc + v), o);
       out[(size_t)(x.r0 + lr) * ld + c0 + jj] = o;
       Ynxt[oc + v] = o;
+      zacc[u][v] = o;
     }
   }
   fence_proxy_async();
   __syncthreads();
+  if (gram_next) {
+    // the next step's Gram partial from a shared-memory copy of the own rows
+    // of Y_{j+1} (the staging buffer is idle until the next cluster barrier)
+    double* yo = s.ys;
+#pragma unroll
+    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      const int it = tid + u * blockDim.x;
+      if (it >= nitems) break;
+      const int lr = it / nch, cq = it - lr * nch;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) yo[(size_t)lr * bcp + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
+    }
+    __syncthreads();
+    double* slot = red_slot(d, x, x.c);
+    gram_mma2(s.SF, sl, rF, yo, bcp, bc, 0, nl, slot, s.gsc);
+    gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, yo, bcp, bc, 0, nl, slot + rF * bc, s.gsc);
+    gram_ready = true;
+  }
   ycp ^= 1;
 }
 
@@ -716,13 +739,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.lds = lds;
     double* p = smem;
     const int sq = lcap * lds;
-    s.A = p; p += sq; s.Q = p; p += sq; s.L = p; p += sq; s.M = p; p += sq; s.T = p; p += sq;
+    s.T = p; p += sq;
     s.scr = p; p += PDSDP_NTHR;
     s.theta = p; p += PDSDP_BMAX; s.res = p; p += PDSDP_BMAX; s.lamF = p; p += PDSDP_BMAX;
     s.lamN = p; p += PDSDP_BMAX; s.dsc = p; p += PDSDP_BMAX; s.cs = p; p += 4 * PDSDP_BMAX;
     s.red1 = p; p += 4 * PDSDP_BMAX;
     s.gsc = p; p += PDSDP_GRAM_SCR;
-    s.ys = p; p += ycap;
+    // A, Q, L, M are Rayleigh-Ritz workspaces: dead while the filter runs, so
+    // the operand staging buffer starts at A and spans them too
+    s.A = p; p += sq; s.Q = p; p += sq; s.L = p; p += sq; s.M = p; p += sq;
+    s.ys = s.A; p += ycap;
     s.SF = p; p += owncap;
     double* zvs = p; p += zcap;
     int* ip = (int*)p;
@@ -733,15 +759,15 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.zc = zc; s.zvs = zvs;
     s.zoff = d.zptr[x.r0];
     s.zstaged = (d.zptr[x.r1] - s.zoff) <= zcap ? 1 : 0;
-    int cw = ycap / d.n;
+    int cw = (ycap + 4 * sq) / d.n;
     cw &= ~1;
     if (cw > d.ld) cw = d.ld;
     s.ycw = (cw >= 2) ? cw : 0;
     s.sld = lcap;
-    s.ycap = ycap;
+    s.ycap = ycap + 4 * sq;
     {
       const int nl = x.r1 - x.r0, sp = own_stride(lcap);
-      s.own = (owncap > 0 && nl * lcap <= owncap && nl <= nlmax && nl * sp <= ycap &&
+      s.own = (owncap > 0 && nl * lcap <= owncap && nl <= nlmax && nl * sp <= s.ycap &&
                nl * (sp / 4) <= PDSDP_OWN_ITEMS * PDSDP_NTHR) ? 1 : 0;
     }
   }
@@ -902,6 +928,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const int bcp = own_stride(bc);
       const size_t nld = (size_t)n * (ld + 4);
       int ycp = 0;
+      bool gram_ready = false;
       for (int it = tid; it < nl * bc; it += blockDim.x) {
         const int lr = it / bc, jj = it - lr * bc;
         d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = d.V[(size_t)(x.r0 + lr) * ld + c0 + jj];
@@ -925,13 +952,15 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             __syncthreads();
             ycp = 1;
           } else {
-            operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase);
+            operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase,
+                              gram_ready, j < m);
             ++matvecs;
           }
         } else {
           const double sn = 1.0 / (2.0 / sig1 - sg);
           const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
-          operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase);
+          operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase,
+                            gram_ready, j < m);
           ++matvecs;
           sg = sn;
         }
@@ -994,21 +1023,19 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       prof_mark(pf, 1);
       gram_mma(buf(iy), b, buf(iy), b, ld, x.r0, x.r1, slot, s.gsc);
       gram_mma(d.F, rFx, buf(iy), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
-      // reduce into A (G1) and T
+      // reduce T now; G1 after the product (whose staging buffer overlays A)
       cg::this_cluster().sync();
-      const int q = b * b + rFx * b;
-      for (int i = tid; i < q; i += blockDim.x) {
-        const double acc = cluster_sum(d, x, i, false);
-        if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
-        else s.T[i - b * b] = acc;
-      }
-      x.par ^= 1;
+      for (int i = tid; i < rFx * b; i += blockDim.x) s.T[i] = cluster_sum(d, x, b * b + i, false);
       __syncthreads();
     }
     scale_T(s, rFx, 0, b);
     prof_mark(pf, 3);
     if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
     else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
+    __syncthreads();
+    for (int i = tid; i < b * b; i += blockDim.x) s.A[(i / b) * lds + (i % b)] = cluster_sum(d, x, i, false);
+    x.par ^= 1;
+    __syncthreads();
     prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----

@@ -467,7 +467,7 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds, int step) {
   long long want = (long long)b->nmax * std::min(b->ldmax, 16);
   int ycap = (int)std::min<long long>(want, (long long)(avail / 8));
   ycap &= ~1;
-  if (ycap < 2 * b->nmax) { ycap = 0; owncap = 0; }
+  if (ycap + 4LL * lds * (lds + 1) < 2LL * b->nmax) { ycap = 0; owncap = 0; }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nact * b->C);
   cfg.blockDim = dim3(PDSDP_NTHR);
