@@ -1112,7 +1112,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // pairs among the trailing guard columns only need loose accuracy (their
     // Ritz pairs are not used; residuals are recomputed honestly below)
     double *Aj, *Qj;
-    jacobi_eig2(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
+    jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     prof_mark(pf, 12);
     if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];
     sort_desc(Aj, b, lds, s.theta, s.perm);

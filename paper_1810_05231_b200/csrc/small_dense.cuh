@@ -636,6 +636,118 @@ __device__ void jacobi_eig2(double* A, double* A2, double* Q, double* Q2, int b,
 }
 
 
+// Parallel-order cyclic Jacobi for the b x b (b <= 64) projected matrix,
+// block-wide.  Same contract and rotations as jacobi_eig2, restructured for
+// latency: per round, thread p (< b) writes the row coefficients (a0, a1) of
+// index p -- an unpaired index is its own partner with (1, 0) -- so the
+// element update  A' = J^T A J,  Q' = Q J  is branch-free; thread (i, j0)
+// owns row i and columns j0, j0+8, ... (no index division); a sweep starts
+// only if some off-diagonal entry is above its threshold (no trailing no-op
+// sweep).
+__device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
+                            int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double fro_part[32];
+  double f = 0.0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
+    const double v = A[i * lds + j];
+    f = fma(v, v, f);
+  }
+  f = warp_sum(f);
+  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
+  const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
+  for (int e = tid; e < R * bb; e += nt) {
+    const int t = e / bb, j = e % bb;
+    if (j < np) {
+      const int t0 = j, t1 = bb - 1 - j;
+      const int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + t) % R;
+      const int q = 1 + (t1 - 1 + t) % R;
+      tab[t * bb + p] = (q < b) ? q : p;
+      tab[t * bb + q] = (p < b) ? p : q;
+    }
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
+  fro = sqrt(fro);
+  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  double* c0a = cs;                 // a0 per index
+  double* c1a = cs + PDSDP_BMAX;    // a1 per index (signed)
+  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
+  const int ri = tid >> 3, cj = tid & 7;    // row and first column of this thread
+  int sweeps = 0;
+  if (b > 1) {
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      // any off-diagonal entry above its threshold?
+      int need = 0;
+      if (ri < b)
+        for (int j = cj; j < b; j += 8)
+          if (j > ri && fabs(Ac[ri * lds + j]) > ((ri < nimp) ? thr_imp : thr_guard)) need = 1;
+      if (!__syncthreads_or(need)) break;
+      for (int t = 0; t < R; ++t) {
+        const int* pt = tab + t * bb;
+        // (1) rotation of the pair (p, q), p < q, stored per index
+        if (tid < b) {
+          const int p = tid, q = pt[p];
+          double c = 1.0, sn = 0.0;
+          if (q != p) {
+            const int lo_ = min(p, q), hi_ = max(p, q);
+            const double apq = Ac[lo_ * lds + hi_];
+            if (fabs(apq) > ((lo_ < nimp) ? thr_imp : thr_guard)) {
+              const double tau = (Ac[hi_ * lds + hi_] - Ac[lo_ * lds + lo_]) * fast_rcp(2.0 * apq);
+              const double at = fabs(tau);
+              double tt;
+              if (at < 1e150) {
+                const double u = fma(tau, tau, 1.0);
+                tt = fast_rcp(at + u * fast_rsqrt(u));
+              } else {
+                tt = 0.5 * fast_rcp(at);
+              }
+              tt = (tau >= 0.0) ? tt : -tt;
+              if (!isfinite(tau)) tt = 0.0;
+              c = fast_rsqrt(fma(tt, tt, 1.0));
+              sn = tt * c;
+            }
+            // column lo_ -> c*col_lo - s*col_hi ; column hi_ -> s*col_lo + c*col_hi
+            c0a[p] = c;
+            c1a[p] = (p == lo_) ? -sn : sn;
+          } else {
+            c0a[p] = 1.0;
+            c1a[p] = 0.0;
+          }
+        }
+        __syncthreads();
+        // (2) A' = J^T A J and Q' = Q J
+        if (ri < b) {
+          const int pi = pt[ri];
+          const double a0 = c0a[ri], a1 = c1a[ri];
+          const double* Ar = Ac + ri * lds;
+          const double* Apr = Ac + pi * lds;
+          const double* Qr = Qc + ri * lds;
+          for (int j = cj; j < b; j += 8) {
+            const int pj = pt[j];
+            const double b0 = c0a[j], b1 = c1a[j];
+            double v = fma(b1, Ar[pj], b0 * Ar[j]);
+            const double w = fma(b1, Apr[pj], b0 * Apr[j]);
+            v = fma(a1, w, a0 * v);
+            if (pj == ri && pj != j && b1 != 0.0) v = 0.0;      // annihilated pair
+            An[ri * lds + j] = v;
+            Qn[ri * lds + j] = fma(b1, Qr[pj], b0 * Qr[j]);
+          }
+        }
+        __syncthreads();
+        { double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp; }
+      }
+      ++sweeps;
+    }
+  }
+  *Aout = Ac; *Qout = Qc;
+  if (tid == 0) sflag[0] = sweeps;
+  __syncthreads();
+}
+
 // Same as jacobi_eig2, executed by warp 0 alone (warp-synchronous).
 __device__ void jacobi_eig2_warp(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
                             int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
