@@ -425,6 +425,32 @@ __device__ __forceinline__ void rotate_rows(const Inst& d, const Cta& x, const d
   }
 }
 
+// rows [0, nl) of a b-column block, global (stride ld) -> shared (stride b)
+__device__ __forceinline__ void copy_rows_in(const double* __restrict__ src, int ld, double* dst, int nl, int b) {
+  for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
+    const int lr = it / b, j = it - lr * b;
+    dst[it] = src[(size_t)lr * ld + j];
+  }
+}
+
+// out (nl x b, stride ldo) = In (nl x b, stride ldi) * Msm (b x b, stride lds);
+// In in shared memory, out in shared or global memory
+__device__ __forceinline__ void rot_block(const double* In, int ldi, const double* Msm, int lds,
+                                          double* out, int ldo, int nl, int b) {
+  for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
+    const int lr = it / b, j = it - lr * b;
+    const double* row = In + (size_t)lr * ldi;
+    double a0 = 0.0, a1 = 0.0;
+    int t = 0;
+    for (; t + 2 <= b; t += 2) {
+      a0 = fma(row[t], Msm[t * lds + j], a0);
+      a1 = fma(row[t + 1], Msm[(t + 1) * lds + j], a1);
+    }
+    if (t < b) a0 = fma(row[t], Msm[t * lds + j], a0);
+    out[(size_t)lr * ldo + j] = a0 + a1;
+  }
+}
+
 // T (smem, (rF + nlock) x bc) <- [diag(lamF); -diag(theta)] .* T  (in place)
 __device__ void scale_T(const Sm& s, int rF, int nlock, int bc) {
   for (int e = threadIdx.x; e < (rF + nlock) * bc; e += blockDim.x) {
@@ -1054,16 +1080,38 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
     }
     __syncthreads();
-    // Y1 = Y M1 -> buf(iav) ; W1 = W M1 -> buf(iw1)
+    // Y1 = Y M1 ; W1 = W M1 -- in shared memory (own rows) when they fit
+    // after the Rayleigh-Ritz workspaces, else in buf(iav) / buf(iw1)
     prof_mark(pf, 5);
-    rotate_rows(d, x, buf(iy), s.M, lds, buf(iav), b);
-    rotate_rows(d, x, buf(iw), s.M, lds, buf(iw1), b);
+    const int nlr = x.r1 - x.r0;
+    const bool rsm = 3 * nlmax * b <= ycap;
+    double* S0 = s.A + 4 * (size_t)lcap * lds;
+    double* S1 = S0 + (size_t)nlr * b;
+    double* S2 = S1 + (size_t)nlr * b;
+    if (rsm) {
+      copy_rows_in(buf(iy) + (size_t)x.r0 * ld, ld, S0, nlr, b);
+      __syncthreads();
+      rot_block(S0, b, s.M, lds, S1, b, nlr, b);
+      __syncthreads();
+      copy_rows_in(buf(iw) + (size_t)x.r0 * ld, ld, S0, nlr, b);
+      __syncthreads();
+      rot_block(S0, b, s.M, lds, S2, b, nlr, b);
+    } else {
+      rotate_rows(d, x, buf(iy), s.M, lds, buf(iav), b);
+      rotate_rows(d, x, buf(iw), s.M, lds, buf(iw1), b);
+    }
     __syncthreads();
     // ---- R2: G2 = Y1^T Y1, H = Y1^T W1 ----
     {
       double* slot = red_slot(d, x, x.c);
-      gram_mma(buf(iav), b, buf(iav), b, ld, x.r0, x.r1, slot, s.gsc);
-      gram_mma(buf(iav), b, buf(iw1), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
+      if (rsm) {
+        gram_mma2(S1, b, b, S1, b, b, 0, nlr, slot, s.gsc);
+        gram_mma2(S1, b, b, S2, b, b, 0, nlr, slot + b * b, s.gsc);
+      } else {
+        gram_mma(buf(iav), b, buf(iav), b, ld, x.r0, x.r1, slot, s.gsc);
+        gram_mma(buf(iav), b, buf(iw1), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
+      }
+      prof_mark(pf, 4);
       cg::this_cluster().sync();
       const int q = 2 * b * b;
       for (int i = tid; i < q; i += blockDim.x) {
@@ -1128,13 +1176,19 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     __syncthreads();
     // V = Y1 B ; AV = W1 B  (AV goes to buf(iw), which becomes the AV buffer)
     prof_mark(pf, 5);
-    rotate_rows(d, x, buf(iav), Bm, lds, d.V, b);
-    rotate_rows(d, x, buf(iw1), Bm, lds, buf(iw), b);
+    if (rsm) {
+      rot_block(S1, b, Bm, lds, d.V + (size_t)x.r0 * ld, ld, nlr, b);
+      rot_block(S2, b, Bm, lds, buf(iw) + (size_t)x.r0 * ld, ld, nlr, b);
+    } else {
+      rotate_rows(d, x, buf(iav), Bm, lds, d.V, b);
+      rotate_rows(d, x, buf(iw1), Bm, lds, buf(iw), b);
+    }
     iav = iw;
     av_valid = true;
     theta_valid = true;
     __syncthreads();
     // ---- R3: residual norms ----
+    prof_mark(pf, 4);
     colres_partial(buf(iav), d.V, s.theta, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
     cluster_reduce(d, x, b, 0, s.red1);
     ++passes;
@@ -1233,7 +1287,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     __syncthreads();
   }
-  double ed2 = 0.0, fin = 1.0;
+  double ed2 = 0.0, fin = 1.0, dysd = 0.0;   // dysd: <dy, M(X+ - X)> = <M^T dy, dX>
   {
     const int G = d.group;
     const int lane = tid & 31, sub = lane % G;
@@ -1270,30 +1324,34 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         d.dy[i] = dyi;
         const double t = dyi / alpha - sd;
         ed2 = fma(t, t, ed2);
+        dysd = fma(dyi, sd, dysd);
         if (!isfinite(ynew)) fin = 0.0;
       }
     }
   }
-  // block reduce ed2 (sum), fin (min -> use max of negatives)
+  // block reduce ed2, dysd (sums), fin (min -> max of negatives)
   {
     double v = warp_sum(ed2);
+    double v2 = warp_sum(dysd);
     double f = fin;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) f = fmin(f, __shfl_xor_sync(0xffffffffu, f, o));
-    if ((tid & 31) == 0) { s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = f; }
+    if ((tid & 31) == 0) { s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = f; s.scr[64 + (tid >> 5)] = v2; }
     __syncthreads();
     if (tid == 0) {
-      double a = 0.0, ff = 1.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; ff = fmin(ff, s.scr[32 + w]); }
+      double a = 0.0, a2 = 0.0, ff = 1.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; a2 += s.scr[64 + w]; ff = fmin(ff, s.scr[32 + w]); }
       double* slot = red_slot(d, x, x.c);
       slot[0] = a;
-      slot[1] = -ff;   // max of -fin
+      slot[1] = a2;
+      slot[2] = -ff;   // max of -fin
     }
     __syncthreads();
   }
-  cluster_reduce(d, x, 1, 1, s.red1);
+  cluster_reduce(d, x, 2, 1, s.red1);
   const double ed2_tot = s.red1[0];
-  double fin_tot = -s.red1[1];
+  const double dysd_tot = s.red1[1];
+  double fin_tot = -s.red1[2];
   for (int i = 0; i < rN; ++i) if (s.theta[i] > 0.0 && !isfinite(s.theta[i])) fin_tot = 0.0;
 
   prof_mark(pf, 7);
@@ -1313,14 +1371,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       zvn[e] = z;
       const int i = d.zrow[e], j = d.zcol[e];
       if (j >= i) {
-        const double* Vi = d.V + (size_t)i * ld; const double* Vj = d.V + (size_t)j * ld;
-        const double* Fi = d.F + (size_t)i * ld; const double* Fj = d.F + (size_t)j * ld;
-        double xn = 0.0, xo = 0.0;
-        for (int l = 0; l < rN; ++l) if (s.lamN[l] != 0.0) xn = fma(Vi[l] * s.lamN[l], Vj[l], xn);
-        for (int l = 0; l < rF; ++l) if (s.lamF[l] != 0.0) xo = fma(Fi[l] * s.lamF[l], Fj[l], xo);
-        const double v = (xn - xo) / alpha;
         const double w = (i == j) ? 1.0 : 2.0;
-        corr = fma(w * a, a - 2.0 * v, corr);
+        corr = fma(w * a, a, corr);
         for (int q = 0; q < d.nd; ++q) cu[q] = fma(w * a, d.du[(size_t)q * n + i] * d.du[(size_t)q * n + j], cu[q]);
       }
     }
@@ -1359,16 +1411,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     __syncthreads();
   }
   cluster_reduce(d, x, 1 + d.nd, 1, s.red1);
-  // dense rank-one rows: their share of the primal residual and of the
-  // Gershgorin bound.  With A = M^T dy = A_s + sum_q dlt_q u_q u_q^T,
-  // dlt_q = sig_q dy_q and V = dX / alpha:
-  //   ||A||^2 - 2<A, V> = corr_s + sum_q (2 dlt_q <A_s, u_q u_q^T> - 2 dy_q sig_q u_q^T dX u_q / alpha)
-  //                       + sum_{q,l} dlt_q dlt_l (u_q^T u_l)^2
+  // Support correction of the primal residual  eps_p^2 = ||dX/alpha||^2 + corr,
+  // corr = ||A||^2 - 2 <A, dX>/alpha with A = M^T dy; the cross term is
+  // <dy, M(dX)> from the dual step (adjoint identity).  Dense rank-one rows:
+  // A = A_s + sum_q dlt_q u_q u_q^T, dlt_q = sig_q dy_q, so
+  //   ||A||^2 = ||A_s||^2 + 2 sum_q dlt_q <A_s, u_q u_q^T> + sum_{q,l} dlt_q dlt_l (u_q^T u_l)^2,
   // and lambda_max(Z+) <= gersh(Z_s) + sum_q max(0, sig_q y+_q) ||u_q||^2.
-  double corr_tot = s.red1[0], gmax_tot = s.red1[1 + d.nd];
+  double corr_tot = s.red1[0] - 2.0 * dysd_tot / alpha, gmax_tot = s.red1[1 + d.nd];
   for (int q = 0; q < d.nd; ++q) {
     const double dyq = d.dy[d.drow[q]], dlt = d.dsig[q] * dyq;
-    corr_tot += 2.0 * dlt * s.red1[1 + q] - 2.0 * dyq * dsum_sm[2 * q + 1] / alpha;
+    corr_tot += 2.0 * dlt * s.red1[1 + q];
     for (int l = 0; l < d.nd; ++l) corr_tot += dlt * d.dsig[l] * d.dy[d.drow[l]] * d.duu[q * PDSDP_NDMAX + l];
     gmax_tot += fmax(0.0, d.dsig[q] * yn[d.drow[q]]) * d.dun2[q];
   }

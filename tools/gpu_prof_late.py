@@ -24,9 +24,9 @@ dt = time.perf_counter() - t
 kt = b.kernel_times()
 print(f"n={prob.n} r={r} K0={K0} K={K}: loop {1e6*dt/K:.1f} us/iter; iterate kernel {1e3*kt['iterate_ms']/K:.1f} us; "
       f"residual kernel {1e3*kt['residual_ms']/K:.1f} us; matvecs/iter {mv/K:.2f} passes/iter {ps/K:.2f} block {o[11]}")
-names = ["prologue/epilogue", "op gram", "op cluster-reduce", "op apply", "-", "rotate+R2", "R3+conv", "dual+adjoint",
+names = ["prologue/epilogue", "op gram", "op cluster-reduce", "op apply", "R2 reduce, R3+assess+plan", "rotations+R2 gram", "dual step", "adjoint+epilogue",
          "chol", "tri_inv+M1", "DHD+gemms", "jacobi", "sort+B", "apply: staging issue", "apply: staging wait", "jacobi sweeps (count)"]
 tot = pc[:15].sum()
 for nm, c in zip(names[:15], pc[:15]):
-    if nm != "-": print(f"   {nm:22s} {c/K/1.965e3:8.1f} us/iter ({c/tot:.2f})")
+    print(f"   {nm:22s} {c/K/1.965e3:8.1f} us/iter ({c/tot:.2f})")
 print(f"   jacobi sweeps/iter {pc[15]/K:.2f}")
