@@ -909,7 +909,20 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const bool stale = (pass == 0 && !rerun);   // residuals belong to the previous S
       const double eps_rel = fmax(as.maxres, stale ? 1e-3 : 0.0);
       int mcap = PDSDP_MMAX;
-      if (as.last_bad >= 0 || stale || (!as.cert_bad && !as.tail_bad)) {
+      // leading pairs already converged to the kept tolerance: deflate them
+      // and filter the rest of the block (a small spread admits the degree the
+      // slow column needs, and the trailing columns track the eigenvalues
+      // just below the cut instead of riding along unfiltered)
+      int nconv = 0;
+      if (!stale && as.last_bad >= 0)
+        while (nconv < as.last_bad && col_ok(nconv, s.res[nconv], s.theta, r, b, scale, xnorm, cert_tol)) ++nconv;
+      if (nconv >= 1) {
+        nlock = nconv; c0 = nconv; bc = b - nconv;
+        mcap = cheb_plan(s.theta, b, lo, s.theta[nconv], s.theta[b - 1], s.theta[as.last_bad], as.rho_k, scale,
+                         eps_rel, m, fe, fc, sig1);
+        if (m < 2) m = 2;
+        if (m > mcap) m = mcap;
+      } else if (as.last_bad >= 0 || stale || (!as.cert_bad && !as.tail_bad)) {
         // kept columns; guards filtered too unless that would collapse the block
         int a1 = (as.last_bad >= 0) ? as.last_bad + 1 : r;
         if (a1 > b - 1) a1 = b - 1;
