@@ -124,9 +124,15 @@ int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_pack
 
 /* Per-kernel CUDA-event timing of pdsdp_iterate (for the roofline report):
  * out[0] iterate-kernel ms total, out[1] launches, out[2] residual-kernel ms
- * total, out[3] launches.  enable != 0 switches recording on and clears. */
+ * total (verification mode only), out[3] launches.  enable != 0 switches recording on and clears. */
 int pdsdp_set_timing(pdsdp_batch* b, int enable);
 int pdsdp_kernel_times(pdsdp_batch* b, double* out /* [4] */);
+
+/* Verification mode: after every iteration also evaluate the dense part
+ * ||dX/alpha||_F^2 of the primal residual (reference pdhg.py:198-208) entry by
+ * entry over the upper triangle on the whole GPU (DMMA), into output slot 14,
+ * next to the factored form the iteration uses (slot 8).  Off by default. */
+int pdsdp_set_verify_residual(pdsdp_batch* b, int enable);
 
 /* Eigensolver diagnostics of the last iteration of one instance:
  * out[0..256) per pass (m, worst rel residual, slow column, theta, t, lo, cut, ||X+||),

@@ -125,7 +125,7 @@ struct Ctl {
 
 // output slots
 enum { O_EPS_P = 0, O_EPS_D, O_LAM, O_FIN, O_PASSES, O_MATVECS, O_EIGCONV, O_EIGRES,
-       O_DENSE, O_CORR, O_ED2, O_BLK, O_DONE, O_ERR };
+       O_DENSE, O_CORR, O_ED2, O_BLK, O_DONE, O_ERR, O_DENSE_EXACT };
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -489,6 +489,9 @@ __device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s
 // global row-major (for Rayleigh-Ritz) and into Yc[p^1] over Y_{j-1}.
 #define PDSDP_OWN_ITEMS 2      // (row, 4-column chunk) items per thread
 __device__ __forceinline__ int own_stride(int bc) { return (bc + 3) & ~3; }
+// the locked pairs' own rows are copied next to F's in shared memory when
+// they fit the row stride of SF
+__device__ __forceinline__ bool own_lock_sm(int rFx, int nlock, int sl) { return nlock > 0 && rFx + nlock <= sl; }
 
 __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
                                                   double* out, int c0, int bc, int rF, int nlock,
@@ -504,9 +507,13 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const int nitems = nl * nch;
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
     double* slot = red_slot(d, x, x.c);
-    gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
-    gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
-              slot + rF * bc, s.gsc);
+    if (own_lock_sm(rF, nlock, sl)) {
+      gram_mma2(s.SF, sl, rF + nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
+    } else {
+      gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
+      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
+                slot + rF * bc, s.gsc);
+    }
   }
   gram_ready = false;
   prof_mark(pf, 2);
@@ -591,6 +598,12 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     if (g0 < C) cg::this_cluster().sync();
     prof_mark(pf, 3);
   }
+#ifdef PDSDP_PROF_EPI
+  prof_mark(pf, 10);
+#endif
+  // locked pairs' own rows sit after F's in SF when they fit (own_lock_sm)
+  const int nsf = own_lock_sm(rF, nlock, sl) ? rF + nlock : rF;
+  const int nglb = nsf == rF ? nlock : 0;
 #pragma unroll
   for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
     const int it = tid + u * blockDim.x;
@@ -599,30 +612,50 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     const double* Fr = s.SF + (size_t)lr * sl;
     const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
     const size_t oc = (size_t)(x.r0 + lr) * bcp + 4 * cq;
+    // recurrence terms Y_j, Y_{j-1} of the item, loaded before its stores
+    // (which may alias them as far as the compiler knows: one L2 round trip
+    // per item instead of one per element)
+    double yc[4], yp[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const bool ok = 4 * cq + v < bc;
+      yc[v] = (ok && cb != 0.0) ? __ldcg(Ycur + oc + v) : 0.0;
+      yp[v] = (ok && cd != 0.0) ? __ldcg(Ynxt + oc + v) : 0.0;
+    }
+    double w[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < nsf; ++l) {
+      const double f = Fr[l];
+      const double* Tl = s.T + l * bc + 4 * cq;   // entries past bc are never used
+#pragma unroll
+      for (int v = 0; v < 4; ++v) w[v] = fma(f, Tl[v], w[v]);
+    }
+    for (int t = 0; t < nglb; ++t) {
+      const double f = __ldcg(Vr + t);
+      const double* Tl = s.T + (rF + t) * bc + 4 * cq;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) w[v] = fma(f, Tl[v], w[v]);
+    }
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int jj = 4 * cq + v;
       if (jj >= bc) break;
-      double w0 = 0.0, w1 = 0.0;
-      int l = 0;
-      for (; l + 2 <= rF; l += 2) {
-        w0 = fma(Fr[l], s.T[l * bc + jj], w0);
-        w1 = fma(Fr[l + 1], s.T[(l + 1) * bc + jj], w1);
-      }
-      if (l < rF) w0 = fma(Fr[l], s.T[l * bc + jj], w0);
-      double w = w0 + w1;
-      for (int t = 0; t < nlock; ++t) w = fma(Vr[t], s.T[(rF + t) * bc + jj], w);
-      w = fma(-alpha, zacc[u][v], w);
-      double o = ca * w;
-      if (cb != 0.0) o = fma(cb, __ldcg(Ycur + oc + v), o);
-      if (cd != 0.0) o = fma(cd, __ldcg(Ynxt + oc + v), o);
+      const double wv = fma(-alpha, zacc[u][v], w[v]);
+      double o = ca * wv;
+      if (cb != 0.0) o = fma(cb, yc[v], o);
+      if (cd != 0.0) o = fma(cd, yp[v], o);
       out[(size_t)(x.r0 + lr) * ld + c0 + jj] = o;
       Ynxt[oc + v] = o;
       zacc[u][v] = o;
     }
   }
+#ifdef PDSDP_PROF_EPI
+  prof_mark(pf, 12);
+#endif
   fence_proxy_async();
   __syncthreads();
+#ifdef PDSDP_PROF_EPI
+  prof_mark(pf, 3);
+#endif
   if (gram_next) {
     // the next step's Gram partial from a shared-memory copy of the own rows
     // of Y_{j+1} (the staging buffer is idle until the next cluster barrier)
@@ -637,8 +670,12 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     __syncthreads();
     double* slot = red_slot(d, x, x.c);
-    gram_mma2(s.SF, sl, rF, yo, bcp, bc, 0, nl, slot, s.gsc);
-    gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, yo, bcp, bc, 0, nl, slot + rF * bc, s.gsc);
+    if (own_lock_sm(rF, nlock, sl)) {
+      gram_mma2(s.SF, sl, rF + nlock, yo, bcp, bc, 0, nl, slot, s.gsc);
+    } else {
+      gram_mma2(s.SF, sl, rF, yo, bcp, bc, 0, nl, slot, s.gsc);
+      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, yo, bcp, bc, 0, nl, slot + rF * bc, s.gsc);
+    }
     gram_ready = true;
   }
   ycp ^= 1;
@@ -704,6 +741,56 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
   if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(1e4 / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
   if (mcap < 2) mcap = 2;
   return mcap;
+}
+
+// ||dX||_F^2 for dX = V diag(lamN) V^T - F diag(lamF) F^T with orthonormal V
+// (n x rN) and F (n x rF), from P = V^T F and G = F_perp^T F_perp, F_perp =
+// F - V P:
+//   dX = V A0 V^T - V B F_perp^T - F_perp B^T V^T - F_perp diag(lamF) F_perp^T,
+//   A0 = diag(lamN) - P diag(lamF) P^T,  B = P diag(lamF),
+// whose four blocks are mutually orthogonal (V^T F_perp = 0), so
+//   ||dX||^2 = ||A0||^2 + 2 tr(B G B^T) + sum_jl lamF_j lamF_l G_jl^2.
+// Every term is a sum of squares of small quantities: no cancellation against
+// ||X||^2 (the expanded square ||X+||^2 - 2<X+, X> + ||X||^2 loses ~10 digits
+// near the stopping tolerance).  Block-wide; deterministic fixed-order sums.
+__device__ double dense_residual_lowrank(const double* P, const double* G, const double* lamN, const double* lamF,
+                                         int rN, int rF, double* scr) {
+  const int tid = threadIdx.x;
+  double acc = 0.0;
+  // ||A0||^2 : one entry (i, l) per work item
+  for (int e = tid; e < rN * rN; e += blockDim.x) {
+    const int i = e / rN, l = e - i * rN;
+    double a = (i == l) ? lamN[i] : 0.0;
+    for (int j = 0; j < rF; ++j) a = fma(-P[i * rF + j] * lamF[j], P[l * rF + j], a);
+    acc = fma(a, a, acc);
+  }
+  // 2 tr(B G B^T) = 2 sum_i sum_{j,l} B_ij G_jl B_il : one (i, j) per work item
+  for (int e = tid; e < rN * rF; e += blockDim.x) {
+    const int i = e / rF, j = e - i * rF;
+    const double bij = P[i * rF + j] * lamF[j];
+    double t = 0.0;
+    for (int l = 0; l < rF; ++l) t = fma(G[j * rF + l], P[i * rF + l] * lamF[l], t);
+    acc = fma(2.0 * bij, t, acc);
+  }
+  // sum_jl lamF_j lamF_l G_jl^2
+  for (int e = tid; e < rF * rF; e += blockDim.x) {
+    const int j = e / rF, l = e - j * rF;
+    const double g = G[e];
+    acc = fma(lamF[j] * lamF[l] * g, g, acc);
+  }
+  acc = warp_sum(acc);
+  __syncthreads();
+  if ((tid & 31) == 0) scr[tid >> 5] = acc;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += scr[w];
+  __syncthreads();
+  return tot;
+}
+
+// a ring buffer free once the eigensolver passes are done (not V, F, AV)
+__device__ __forceinline__ double* buf_free_after_passes(const Inst& d, int iav) {
+  return iav == 2 ? d.Y1 : d.Y0;
 }
 
 // dynamic shared memory of lrpdhg_iterate_kernel (must match the carve-up below)
@@ -972,6 +1059,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         const int lr = it / bc, jj = it - lr * bc;
         d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = d.V[(size_t)(x.r0 + lr) * ld + c0 + jj];
       }
+      if (own_lock_sm(rFx, nlock, s.sld))
+        for (int it = tid; it < nl * nlock; it += blockDim.x) {
+          const int lr = it / nlock, t = it - lr * nlock;
+          s.SF[(size_t)lr * s.sld + rFx + t] = d.V[(size_t)(x.r0 + lr) * ld + t];
+        }
       fence_proxy_async();
       __syncthreads();
       double sg = sig1;
@@ -1351,20 +1443,37 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     for (int o = 16; o > 0; o >>= 1) f = fmin(f, __shfl_xor_sync(0xffffffffu, f, o));
     if ((tid & 31) == 0) { s.scr[tid >> 5] = v; s.scr[32 + (tid >> 5)] = f; s.scr[64 + (tid >> 5)] = v2; }
     __syncthreads();
+    // P = V^T F (own rows) rides along: the dense part of the primal residual
+    // is evaluated in factored form (see dense_residual_lowrank)
+    gram_mma(d.V, rN, d.F, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 2, s.gsc);
     if (tid == 0) {
       double a = 0.0, a2 = 0.0, ff = 1.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; a2 += s.scr[64 + w]; ff = fmin(ff, s.scr[32 + w]); }
       double* slot = red_slot(d, x, x.c);
       slot[0] = a;
       slot[1] = a2;
-      slot[2] = -ff;   // max of -fin
+      slot[2 + rN * rF] = -ff;   // max of -fin
     }
     __syncthreads();
   }
-  cluster_reduce(d, x, 2, 1, s.red1);
+  cluster_reduce(d, x, 2 + rN * rF, 1, s.red1);
   const double ed2_tot = s.red1[0];
   const double dysd_tot = s.red1[1];
-  double fin_tot = -s.red1[2];
+  double fin_tot = -s.red1[2 + rN * rF];
+  // keep P (rN x rF, row-major) and form the own rows of F_perp = F - V P
+  // in a free ring buffer
+  double* Pm = s.T;
+  for (int i = tid; i < rN * rF; i += blockDim.x) Pm[i] = s.red1[2 + i];
+  double* Fp = buf_free_after_passes(d, iav);
+  __syncthreads();
+  for (int it = tid; it < (x.r1 - x.r0) * rF; it += blockDim.x) {
+    const int rho = x.r0 + it / rF, j = it % rF;
+    const double* Vr = d.V + (size_t)rho * ld;
+    double a = d.F[(size_t)rho * ld + j];
+    for (int l = 0; l < rN; ++l) a = fma(-Vr[l], Pm[l * rF + j], a);
+    Fp[(size_t)rho * ld + j] = a;
+  }
+  __syncthreads();
   for (int i = 0; i < rN; ++i) if (s.theta[i] > 0.0 && !isfinite(s.theta[i])) fin_tot = 0.0;
 
   prof_mark(pf, 7);
@@ -1409,6 +1518,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       for (int q = 0; q < d.nd; ++q) s.scr[64 + 32 * q + (tid >> 5)] = cw[q];
     }
     __syncthreads();
+    gram_mma(Fp, rF, Fp, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 1 + d.nd, s.gsc);
     if (tid == 0) {
       double a = 0.0, gg = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; gg = fmax(gg, s.scr[32 + w]); }
@@ -1419,18 +1529,21 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += s.scr[64 + 32 * q + w];
         slot[1 + q] = c;
       }
-      slot[1 + d.nd] = gg;
+      slot[1 + d.nd + rF * rF] = gg;
     }
     __syncthreads();
   }
-  cluster_reduce(d, x, 1 + d.nd, 1, s.red1);
+  cluster_reduce(d, x, 1 + d.nd + rF * rF, 1, s.red1);
+  // dense part ||dX||_F^2 of the primal residual from P and G (CTA 0 reports)
+  const double dense_a2 = (x.c == 0) ? dense_residual_lowrank(Pm, s.red1 + 1 + d.nd, s.lamN, s.lamF, rN, rF, s.scr)
+                                     : 0.0;
   // Support correction of the primal residual  eps_p^2 = ||dX/alpha||^2 + corr,
   // corr = ||A||^2 - 2 <A, dX>/alpha with A = M^T dy; the cross term is
   // <dy, M(dX)> from the dual step (adjoint identity).  Dense rank-one rows:
   // A = A_s + sum_q dlt_q u_q u_q^T, dlt_q = sig_q dy_q, so
   //   ||A||^2 = ||A_s||^2 + 2 sum_q dlt_q <A_s, u_q u_q^T> + sum_{q,l} dlt_q dlt_l (u_q^T u_l)^2,
   // and lambda_max(Z+) <= gersh(Z_s) + sum_q max(0, sig_q y+_q) ||u_q||^2.
-  double corr_tot = s.red1[0] - 2.0 * dysd_tot / alpha, gmax_tot = s.red1[1 + d.nd];
+  double corr_tot = s.red1[0] - 2.0 * dysd_tot / alpha, gmax_tot = s.red1[1 + d.nd + rF * rF];
   for (int q = 0; q < d.nd; ++q) {
     const double dyq = d.dy[d.drow[q]], dlt = d.dsig[q] * dyq;
     corr_tot += 2.0 * dlt * s.red1[1 + q];
@@ -1479,7 +1592,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       o[O_CORR] = corr_tot;
       o[O_BLK] = b;
       o[O_ERR] = grow_err;
-      if (grow_err) *d.stopf = 1;
+      // primal / dual residuals (reference pdhg.py:198-208)
+      const double dense = dense_a2 / (alpha * alpha);
+      const double ep = sqrt(fmax(dense + corr_tot, 0.0)), ed = sqrt(fmax(ed2_tot, 0.0));
+      o[O_DENSE] = dense;
+      o[O_EPS_P] = ep;
+      o[O_EPS_D] = ed;
+      o[O_DONE] = 1.0;
+      // pause the chunk where the host's control logic may act (lowrank.py:145-185)
+      const double ec = ep + ed;
+      if (grow_err || fin_tot != 1.0 || ec <= ctl.conv_thr || ec >= ctl.stall_thr) *d.stopf = 1;
     }
   }
 }

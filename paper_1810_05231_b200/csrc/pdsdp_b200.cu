@@ -100,6 +100,7 @@ struct pdsdp_batch {
   long long zmax = 0;    // largest per-CTA slice of Z rows over the batch
   int nmax = 0, ldmax = 0;
   int timing = 0;
+  int verify_residual = 0;   // also run residual_kernel (exact dense term) after each step
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0;
 };
@@ -707,6 +708,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
       c.conv_thr = conv_thr ? conv_thr[a] : -1.0;
       c.stall_thr = stall_thr ? stall_thr[(size_t)a * K + j] : HUGE_VAL;
       b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_DONE] = 0.0;
+      b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_DENSE_EXACT] = NAN;
       b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_ERR] = 0.0;
     }
     b->h_active[a] = k;
@@ -727,8 +729,10 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     int rc = launch_iterate(b, nact, lds, j);
     if (rc) return rc;
     if (tm) CK(cudaEventRecord(b->ev[1], b->stream));
-    residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_ctl, b->d_active, j);
-    CK(cudaGetLastError());
+    if (b->verify_residual) {
+      residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_ctl, b->d_active, j);
+      CK(cudaGetLastError());
+    }
     if (tm) CK(cudaEventRecord(b->ev[2], b->stream));
   }
   CK(cudaStreamSynchronize(b->stream));
@@ -764,6 +768,12 @@ int pdsdp_set_timing(pdsdp_batch* b, int enable) {
     if (!b->ev[k]) CK(cudaEventCreate(&b->ev[k]));
   b->timing = enable ? 1 : 0;
   b->t_iter = b->n_iter = b->t_res = b->n_res = 0.0;
+  return PDSDP_OK;
+}
+
+int pdsdp_set_verify_residual(pdsdp_batch* b, int enable) {
+  if (!b) return fail(PDSDP_EINVAL, "batch is NULL");
+  b->verify_residual = enable ? 1 : 0;
   return PDSDP_OK;
 }
 

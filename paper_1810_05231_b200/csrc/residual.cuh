@@ -1,7 +1,9 @@
 // Whole-GPU kernels around the cluster iteration:
-//   residual_kernel   dense part of the primal fixed-point residual
-//                     eps_p^2 = || dX/alpha - M^T dy ||^2  (reference pdhg.py:198-208)
-//                     on FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64):
+//   residual_kernel   verification mode only (pdsdp_set_verify_residual): the
+//                     dense part ||dX/alpha||_F^2 of the primal residual
+//                     (reference pdhg.py:198-208) evaluated entry by entry on
+//                     FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64), next to
+//                     the factored form the iteration kernel uses:
 //                     dX/alpha = [V | F] diag(lamN, -lamF)/alpha [V | F]^T is a
 //                     rank-(r + rF) SYRK evaluated tile by tile over the upper
 //                     triangle and reduced to one scalar; nothing n x n is stored.
@@ -128,19 +130,9 @@ residual_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls, co
   __syncthreads();
   if (threadIdx.x == 0) {
     double dense = 0.0;
-    for (int w = 0; w < RES_THREADS / 32; ++w) dense += wsum[w];
-    const double ep2 = dense + st->corr;
-    double* o = d.out + step * PDSDP_OUT_LEN;
-    const double ep = sqrt(fmax(ep2, 0.0)), ed = sqrt(fmax(st->ed2, 0.0));
-    o[O_DENSE] = dense;
-    o[O_EPS_P] = ep;
-    o[O_EPS_D] = ed;
-    o[O_DONE] = 1.0;
+    for (int w = 0; w < (int)(RES_THREADS / 32); ++w) dense += wsum[w];
+    d.out[step * PDSDP_OUT_LEN + O_DENSE_EXACT] = dense;
     *d.rcount = 0u;
-    // pause the chunk where the host's control logic may act (lowrank.py:145-185)
-    const Ctl c = ctls[inst_id * PDSDP_KMAX + step];
-    const double ec = ep + ed;
-    if (st->finite != 1.0 || ec <= c.conv_thr || ec >= c.stall_thr) *d.stopf = 1;
   }
 }
 

@@ -23,6 +23,8 @@ OUT_EPS_P, OUT_EPS_D, OUT_LAMBDA, OUT_FINITE = 0, 1, 2, 3
 OUT_PASSES, OUT_MATVECS, OUT_EIGCONV, OUT_EIGRES = 4, 5, 6, 7
 OUT_BLOCK = 11
 OUT_DONE = 12
+OUT_DENSE = 8
+OUT_DENSE_EXACT = 14
 BLOCK_MAX = 64
 KMAX = 64
 
@@ -34,7 +36,7 @@ EXPORTED = (
     "pdsdp_iterate", "pdsdp_objective", "pdsdp_download_x", "pdsdp_download_y",
     "pdsdp_apply_M", "pdsdp_apply_M_adjoint", "pdsdp_aproj_psd", "pdsdp_strerror",
     "pdsdp_last_error", "pdsdp_version", "pdsdp_set_timing", "pdsdp_kernel_times",
-    "pdsdp_debug", "pdsdp_iterate_many",
+    "pdsdp_debug", "pdsdp_iterate_many", "pdsdp_set_verify_residual",
 )
 
 
@@ -83,6 +85,7 @@ def load_library(path: str = LIB_PATH):
             "pdsdp_version": (ct.c_int, []),
             "pdsdp_set_timing": (ct.c_int, [P, ct.c_int]),
             "pdsdp_kernel_times": (ct.c_int, [P, P]),
+            "pdsdp_set_verify_residual": (ct.c_int, [P, ct.c_int]),
             "pdsdp_debug": (ct.c_int, [P, ct.c_int, P]),
             "pdsdp_iterate_many": (ct.c_int, [P, ct.c_int, P, P, P, P, I32, I32, P, P, P, P]),
         }
@@ -157,6 +160,11 @@ class DeviceBatch:
 
     def set_timing(self, enable: bool):
         _check(self.lib.pdsdp_set_timing(self.h, 1 if enable else 0))
+
+    def set_verify_residual(self, enable: bool):
+        """Also evaluate ||dX/alpha||_F^2 entry by entry after each step
+        (output slot OUT_DENSE_EXACT) next to the factored form (OUT_DENSE)."""
+        _check(self.lib.pdsdp_set_verify_residual(self.h, 1 if enable else 0))
 
     def kernel_times(self) -> dict:
         out = np.zeros(4)

@@ -298,3 +298,32 @@ def test_batched_solve_matches_single_instance_solves():
         assert rb.rank_path == rs.rank_path == ro.rank_path
         assert rel(rb.X.data, rs.X.data) <= 1e-12
         assert rel(rb.X.data, ro.X) <= ITER_TOL
+
+
+# ------------------------------------------- factored vs entrywise residual
+
+@pytest.mark.parametrize("ci,K,r", [(0, 300, 5), (1, 40, 10), (3, 30, 1), (4, 40, 1)])
+def test_dense_residual_factored_matches_entrywise(ci, K, r):
+    """The iteration kernel evaluates ||dX/alpha||_F^2 (reference
+    pdhg.py:198-208) in factored form from V^T F and F_perp^T F_perp; the
+    verification kernel evaluates it entry by entry over the upper triangle.
+    They must agree to rounding at every step (1e-9 relative)."""
+    from paper_1810_05231_b200.device import DeviceBatch, OUT_DENSE, OUT_DENSE_EXACT, OUT_DONE
+    from paper_1810_05231_b200.solver import operator_norm_on_device
+    prob, cfg = workloads.config(ci)
+    b = DeviceBatch([prob])
+    alpha = cfg.alpha_safety / operator_norm_on_device(b, 0, 0)
+    b.set_alpha(0, alpha)
+    b.reset(0, 0.0)
+    b.set_verify_residual(True)
+    ypar, checked = 0, 0
+    for k in range(K):
+        o = b.iterate([0], [r], [ypar])[0]
+        ypar ^= 1
+        assert o[OUT_DONE] == 1.0
+        ex, fa = o[OUT_DENSE_EXACT], o[OUT_DENSE]
+        assert np.isfinite(ex)
+        assert abs(fa - ex) <= 1e-9 * max(abs(ex), 1e-300) + 1e-24, (k, fa, ex)
+        checked += 1
+    b.close()
+    assert checked == K
