@@ -138,7 +138,9 @@ int pdsdp_set_verify_residual(pdsdp_batch* b, int enable);
  * out[0..256) per pass (m, worst rel residual, slow column, theta, t, lo, cut, ||X+||),
  * out[256..320) Ritz values, out[320..384) Ritz residual norms,
  * out[384..400) SM cycles per kernel phase (CTA 0), out[400..4504) the last
- * projected Rayleigh-Ritz matrix when flag bit 4 was set (b x b, b at 4496). */
+ * projected Rayleigh-Ritz matrix when flag bit 4 was set (b x b, b at 4496),
+ * out[4504..4504 + 16*2048) per-CTA (label, SM cycle) traces of the last
+ * launch with flag bit 6 (count at the last slot of each CTA's 2048). */
 int pdsdp_debug(pdsdp_batch* b, int inst, double* out /* [4504] */);
 
 const char* pdsdp_strerror(int code);

@@ -17,7 +17,9 @@
 #include <cuda_runtime.h>
 
 #define PDSDP_BMAX 64          // largest eigen block (k = r+1 plus guard vectors)
-#define PDSDP_NTHR 512         // threads per CTA of the cluster kernel
+#ifndef PDSDP_NTHR
+#define PDSDP_NTHR 384         // threads per CTA of the cluster kernel (168 registers each)
+#endif
 #define PDSDP_RED_MAX (2 * PDSDP_BMAX * PDSDP_BMAX + 64)
 #define PDSDP_OUT_LEN 16       // doubles per instance and step in the host-mapped output
 #define PDSDP_KMAX 64          // iterations per pdsdp_iterate_many call
@@ -49,19 +51,37 @@ struct State {
   double hdump[PDSDP_BMAX * PDSDP_BMAX + 8];  // diagnostic: last projected matrix H' (flag bit4)
 };
 
-// thread-0 phase timer (clock64 deltas; diagnostic only)
+// thread-0 phase timer (clock64 deltas; diagnostic only).  With a trace
+// buffer (flag bit 5, CTA 0) every mark / tick is also logged as
+// (label, cycle) pairs for a per-step timeline.
+#define PDSDP_TRACE_CAP 2040
+#define PDSDP_TRACE_CTA 1024
 struct Prof {
   long long last;
   long long acc[16];
   int cur;
+  int ntr;
+  int cap;
+  double* trace;
 };
+__device__ __forceinline__ void prof_log(Prof& p, int label, long long now) {
+  if (p.trace && p.ntr < p.cap) {
+    p.trace[2 * p.ntr] = label;
+    p.trace[2 * p.ntr + 1] = (double)now;
+    ++p.ntr;
+  }
+}
 __device__ __forceinline__ void prof_mark(Prof& p, int phase) {
   if (threadIdx.x == 0) {
     const long long now = clock64();
     p.acc[p.cur] += now - p.last;
     p.last = now;
     p.cur = phase;
+    prof_log(p, phase, now);
   }
+}
+__device__ __forceinline__ void prof_tick(Prof& p, int label) {
+  if (threadIdx.x == 0) prof_log(p, label, clock64());
 }
 
 // Per-instance descriptor (device resident).  Sizes and pointers only.
@@ -109,6 +129,7 @@ struct Inst {
   State* st;
   double* out;         // host-mapped [KMAX][OUT_LEN]
   int* stopf;          // device flag: an event may fire, skip the remaining steps
+  double* trace;       // [C][2 * PDSDP_TRACE_CTA] per-CTA (label, cycle) log (flag bit 6)
 };
 
 static_assert(sizeof(Inst) % 8 == 0, "Inst is copied as 8-byte words");

@@ -487,7 +487,9 @@ __device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s
 // loads, and a running slot pointer per item walks the row's (column-sorted)
 // slots group by group.  F's own rows stay in shared memory.  Y_{j+1} goes to
 // global row-major (for Rayleigh-Ritz) and into Yc[p^1] over Y_{j-1}.
-#define PDSDP_OWN_ITEMS 2      // (row, 4-column chunk) items per thread
+#ifndef PDSDP_OWN_ITEMS
+#define PDSDP_OWN_ITEMS 3      // (row, 4-column chunk) items per thread
+#endif
 __device__ __forceinline__ int own_stride(int bc) { return (bc + 3) & ~3; }
 // the locked pairs' own rows are copied next to F's in shared memory when
 // they fit the row stride of SF
@@ -518,6 +520,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   gram_ready = false;
   prof_mark(pf, 2);
   cg::this_cluster().sync();                 // publishes Y_j rows and the partials
+  prof_tick(pf, 20);
   const double alpha = d.alpha;
   const double* ys = s.ys;
   const int C = x.C;
@@ -557,6 +560,11 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
         }
       }
     }
+    prof_mark(pf, 13);
+    mbar_wait(mbar, mphase);
+    mphase ^= 1u;
+    // reduce T once the first operand group has landed (its L2 reads would
+    // otherwise queue behind the multicast traffic into this SM)
     if (first) {
       const int q = (rF + nlock) * bc;
       for (int i = tid; i < q; i += blockDim.x) {
@@ -567,10 +575,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       }
       x.par ^= 1;
       first = false;
+      prof_tick(pf, 21);
     }
-    prof_mark(pf, 13);
-    mbar_wait(mbar, mphase);
-    mphase ^= 1u;
     __syncthreads();
     prof_mark(pf, 14);
 #pragma unroll
@@ -595,6 +601,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       zacc[u][0] += a0; zacc[u][1] += a1; zacc[u][2] += a2; zacc[u][3] += a3;
     }
     g0 = g1;
+    prof_tick(pf, 22);
     if (g0 < C) cg::this_cluster().sync();
     prof_mark(pf, 3);
   }
@@ -651,8 +658,10 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
 #ifdef PDSDP_PROF_EPI
   prof_mark(pf, 12);
 #endif
+  prof_tick(pf, 24);
   fence_proxy_async();
   __syncthreads();
+  prof_tick(pf, 25);
 #ifdef PDSDP_PROF_EPI
   prof_mark(pf, 3);
 #endif
@@ -678,6 +687,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     gram_ready = true;
   }
+  prof_tick(pf, 26);
   ycp ^= 1;
 }
 
@@ -845,6 +855,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   if (threadIdx.x == 0) {
     pf.last = clock64(); pf.cur = 0;
     for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
+    pf.ntr = 0;
+    pf.cap = PDSDP_TRACE_CAP;
+    pf.trace = ((ctl.flags & 32) && x.c == 0) ? d.st->hdump : nullptr;
+    if (ctl.flags & 64) { pf.trace = d.trace + (size_t)x.c * 2 * PDSDP_TRACE_CTA; pf.cap = PDSDP_TRACE_CTA - 1; }
   }
   __shared__ Sm s_sm;
   Sm& s = s_sm;
@@ -1043,6 +1057,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       }
     }
     force_m = -1;
+    prof_tick(pf, 31);
     // ---- Chebyshev filter on the active columns:  Y_m = p_m(S_d) V ----
     int iy = 0;                       // buffer index holding Y_j (0 == V)
     int iyp = -1;                     // buffer holding Y_{j-1}
@@ -1265,7 +1280,12 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // pairs among the trailing guard columns only need loose accuracy (their
     // Ritz pairs are not used; residuals are recomputed honestly below)
     double *Aj, *Qj;
-    jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
+    // block-pair updates pay off once the per-element traffic dominates the
+    // per-round latency (tools/microbench/small_dense_probe.cu: 1.4x at b = 28)
+    if (b >= 24)
+      jacobi_eig4(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
+    else
+      jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     prof_mark(pf, 12);
     if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];
     sort_desc(Aj, b, lds, s.theta, s.perm);
@@ -1445,7 +1465,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     __syncthreads();
     // P = V^T F (own rows) rides along: the dense part of the primal residual
     // is evaluated in factored form (see dense_residual_lowrank)
+    prof_tick(pf, 50);
     gram_mma(d.V, rN, d.F, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 2, s.gsc);
+    prof_tick(pf, 51);
     if (tid == 0) {
       double a = 0.0, a2 = 0.0, ff = 1.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; a2 += s.scr[64 + w]; ff = fmin(ff, s.scr[32 + w]); }
@@ -1474,6 +1496,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     Fp[(size_t)rho * ld + j] = a;
   }
   __syncthreads();
+  prof_tick(pf, 53);
   for (int i = 0; i < rN; ++i) if (s.theta[i] > 0.0 && !isfinite(s.theta[i])) fin_tot = 0.0;
 
   prof_mark(pf, 7);
@@ -1518,7 +1541,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       for (int q = 0; q < d.nd; ++q) s.scr[64 + 32 * q + (tid >> 5)] = cw[q];
     }
     __syncthreads();
+    prof_tick(pf, 54);
     gram_mma(Fp, rF, Fp, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 1 + d.nd, s.gsc);
+    prof_tick(pf, 55);
     if (tid == 0) {
       double a = 0.0, gg = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s.scr[w]; gg = fmax(gg, s.scr[32 + w]); }
@@ -1537,6 +1562,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   // dense part ||dX||_F^2 of the primal residual from P and G (CTA 0 reports)
   const double dense_a2 = (x.c == 0) ? dense_residual_lowrank(Pm, s.red1 + 1 + d.nd, s.lamN, s.lamF, rN, rF, s.scr)
                                      : 0.0;
+  prof_tick(pf, 57);
   // Support correction of the primal residual  eps_p^2 = ||dX/alpha||^2 + corr,
   // corr = ||A||^2 - 2 <A, dX>/alpha with A = M^T dy; the cross term is
   // <dy, M(dX)> from the dual step (adjoint identity).  Dense rank-one rows:
@@ -1553,8 +1579,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
 
   // ---------------- epilogue: state for the next iteration + scalars ----------------
   prof_mark(pf, 0);
-  if (x.c == 0 && tid == 0)
+  if (x.c == 0 && tid == 0) {
     for (int q = 0; q < 15; ++q) st->prof[q] = (double)pf.acc[q];
+    if (pf.trace && !(ctl.flags & 64)) { prof_tick(pf, 99); st->hdump[PDSDP_BMAX * PDSDP_BMAX + 7] = pf.ntr; }
+  }
+  if (tid == 0 && (ctl.flags & 64)) {
+    prof_tick(pf, 99);
+    pf.trace[2 * PDSDP_TRACE_CTA - 1] = pf.ntr;
+  }
   if (x.c == 0) {
     for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
       st->theta[i] = (i < b) ? s.theta[i] : 0.0;

@@ -356,6 +356,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   add(NORM_BLOCKS * 8); add(64); add(4096 * 8);
   add((size_t)I.P * 8);
   add(I.du.size() * 8 + 8);
+  add((size_t)C * 2 * PDSDP_TRACE_CTA * 8);
   bytes += 4096;
   CK(cudaMalloc(&I.dmem, bytes));
   I.dbytes = bytes;
@@ -413,6 +414,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   d.rpart = a.take<double>(I.ntile + 1);
   d.rcount = a.take<unsigned>(16);
   d.st = a.take<State>(1);
+  d.trace = a.take<double>((size_t)C * 2 * PDSDP_TRACE_CTA);
   d.out = out_dev;
   d.alpha = 1.0;
   // opnorm
@@ -788,6 +790,9 @@ int pdsdp_debug(pdsdp_batch* b, int inst, double* out) {
   memcpy(out + 320, h.res, sizeof(h.res));
   memcpy(out + 384, h.prof, sizeof(h.prof));
   memcpy(out + 400, h.hdump, sizeof(h.hdump));
+  // per-CTA trace of the last flag-bit-6 launch
+  CK(cudaMemcpy(out + 4504, b->inst[inst]->desc.trace, (size_t)b->C * 2 * PDSDP_TRACE_CTA * sizeof(double),
+                cudaMemcpyDeviceToHost));
   // reset the per-launch accumulators that the kernel adds into
   State* dst = b->inst[inst]->desc.st;
   CK(cudaMemset(&dst->prof[15], 0, sizeof(double)));

@@ -676,15 +676,16 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
   double* c0a = cs;                 // a0 per index
   double* c1a = cs + PDSDP_BMAX;    // a1 per index (signed)
   double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
-  const int ri = tid >> 3, cj = tid & 7;    // row and first column of this thread
+  const int ri = tid >> 3, cj = tid & 7;    // first row and first column of this thread
+  const int rstep = nt >> 3;
   int sweeps = 0;
   if (b > 1) {
     for (int sweep = 0; sweep < 40; ++sweep) {
       // any off-diagonal entry above its threshold?
       int need = 0;
-      if (ri < b)
+      for (int i = ri; i < b; i += rstep)
         for (int j = cj; j < b; j += 8)
-          if (j > ri && fabs(Ac[ri * lds + j]) > ((ri < nimp) ? thr_imp : thr_guard)) need = 1;
+          if (j > i && fabs(Ac[i * lds + j]) > ((i < nimp) ? thr_imp : thr_guard)) need = 1;
       if (!__syncthreads_or(need)) break;
       for (int t = 0; t < R; ++t) {
         const int* pt = tab + t * bb;
@@ -720,21 +721,153 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
         }
         __syncthreads();
         // (2) A' = J^T A J and Q' = Q J
-        if (ri < b) {
-          const int pi = pt[ri];
-          const double a0 = c0a[ri], a1 = c1a[ri];
-          const double* Ar = Ac + ri * lds;
+        for (int i = ri; i < b; i += rstep) {
+          const int pi = pt[i];
+          const double a0 = c0a[i], a1 = c1a[i];
+          const double* Ar = Ac + i * lds;
           const double* Apr = Ac + pi * lds;
-          const double* Qr = Qc + ri * lds;
+          const double* Qr = Qc + i * lds;
           for (int j = cj; j < b; j += 8) {
             const int pj = pt[j];
             const double b0 = c0a[j], b1 = c1a[j];
             double v = fma(b1, Ar[pj], b0 * Ar[j]);
             const double w = fma(b1, Apr[pj], b0 * Apr[j]);
             v = fma(a1, w, a0 * v);
-            if (pj == ri && pj != j && b1 != 0.0) v = 0.0;      // annihilated pair
-            An[ri * lds + j] = v;
-            Qn[ri * lds + j] = fma(b1, Qr[pj], b0 * Qr[j]);
+            if (pj == i && pj != j && b1 != 0.0) v = 0.0;      // annihilated pair
+            An[i * lds + j] = v;
+            Qn[i * lds + j] = fma(b1, Qr[pj], b0 * Qr[j]);
+          }
+        }
+        __syncthreads();
+        { double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp; }
+      }
+      ++sweeps;
+    }
+  }
+  *Aout = Ac; *Qout = Qc;
+  if (tid == 0) sflag[0] = sweeps;
+  __syncthreads();
+}
+
+// Cyclic parallel Jacobi with (pair, pair) block updates.  Same round-robin
+// order, rotations and thresholds as jacobi_eig3, but each work item updates
+// a whole 2x2 block of A (rows of pair a, columns of pair b; a <= b, the
+// mirror block written too) from four loads, and each Q item one row of a
+// column pair: a quarter of the shared-memory traffic of the per-element
+// form and no per-element partner lookups.  Per round: thread k < np forms
+// the rotation of pair k; one barrier; block updates; one barrier.
+// scratch: cs >= 4 * PDSDP_BMAX doubles; tab >= PDSDP_BMAX * (PDSDP_BMAX + 2) / 8 + 2 * PDSDP_BMAX ints.
+__device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
+                            int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double fro_part[32];
+  double f = 0.0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
+    const double v = A[i * lds + j];
+    f = fma(v, v, f);
+  }
+  f = warp_sum(f);
+  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
+  const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
+  const int nA = np * (np + 1) / 2, nQ = b * np;
+  // upper-triangular (a, b) decode of block items
+  int* tri = tab;                       // [nA]
+  int* plo = tab + PDSDP_BMAX * (PDSDP_BMAX / 2 + 1) / 2 + 8;   // [np] pair lower index
+  int* phi = plo + PDSDP_BMAX / 2 + 1;  // [np] pair upper index (-1: none)
+  double* pc = cs;                      // [np] cosine
+  double* ps = cs + PDSDP_BMAX;         // [np] sine
+  for (int a = tid; a < np; a += nt) {
+    int base = a * np - a * (a - 1) / 2;
+    for (int c = a; c < np; ++c) tri[base + (c - a)] = (a << 8) | c;
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
+  fro = sqrt(fro);
+  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
+  const int ri = tid >> 3, cj = tid & 7, rstep = nt >> 3;
+  int sweeps = 0;
+  if (b > 1) {
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      int need = 0;
+      for (int i = ri; i < b; i += rstep)
+        for (int j = cj; j < b; j += 8)
+          if (j > i && fabs(Ac[i * lds + j]) > ((i < nimp) ? thr_imp : thr_guard)) need = 1;
+      if (!__syncthreads_or(need)) break;
+      for (int t = 0; t < R; ++t) {
+        // (1) rotation of pair k (round-robin order of jacobi_eig3)
+        for (int k = tid; k < np; k += nt) {
+          const int p = (k == 0) ? 0 : 1 + (k - 1 + t) % R;
+          const int q = 1 + (bb - 2 - k + t) % R;
+          const int lo_ = min(p, q), hi_ = max(p, q);
+          double c = 1.0, sn = 0.0;
+          if (hi_ < b) {
+            const double apq = Ac[lo_ * lds + hi_];
+            if (fabs(apq) > ((lo_ < nimp) ? thr_imp : thr_guard)) {
+              const double tau = (Ac[hi_ * lds + hi_] - Ac[lo_ * lds + lo_]) * fast_rcp(2.0 * apq);
+              const double at = fabs(tau);
+              double tt;
+              if (at < 1e150) {
+                const double u = fma(tau, tau, 1.0);
+                tt = fast_rcp(at + u * fast_rsqrt(u));
+              } else {
+                tt = 0.5 * fast_rcp(at);
+              }
+              tt = (tau >= 0.0) ? tt : -tt;
+              if (!isfinite(tau)) tt = 0.0;
+              c = fast_rsqrt(fma(tt, tt, 1.0));
+              sn = tt * c;
+            }
+          }
+          plo[k] = lo_;
+          phi[k] = (hi_ < b) ? hi_ : -1;
+          pc[k] = c;
+          ps[k] = sn;
+        }
+        __syncthreads();
+        // (2) A' = J^T A J by 2x2 blocks, Q' = Q J by row / column pair
+        for (int it = tid; it < nA + nQ; it += nt) {
+          if (it < nA) {
+            const int ab = tri[it], a = ab >> 8, bq = ab & 255;
+            const int pa = plo[a], qa = phi[a], pb = plo[bq], qb = phi[bq];
+            const double ca = pc[a], sa = ps[a], cb = pc[bq], sb = ps[bq];
+            const double a00 = Ac[pa * lds + pb];
+            const double a01 = (qb >= 0) ? Ac[pa * lds + qb] : 0.0;
+            const double a10 = (qa >= 0) ? Ac[qa * lds + pb] : 0.0;
+            const double a11 = (qa >= 0 && qb >= 0) ? Ac[qa * lds + qb] : 0.0;
+            // columns: (p, q) -> (c p - s q, s p + c q)
+            const double x00 = fma(-sb, a01, cb * a00), x01 = fma(sb, a00, cb * a01);
+            const double x10 = fma(-sb, a11, cb * a10), x11 = fma(sb, a10, cb * a11);
+            // rows
+            const double y00 = fma(-sa, x10, ca * x00), y10 = fma(sa, x00, ca * x10);
+            const double y01 = fma(-sa, x11, ca * x01);
+            double y11 = fma(sa, x01, ca * x11);
+            if (a == bq) {
+              // diagonal block: the pair's off-diagonal is annihilated
+              An[pa * lds + pa] = y00;
+              if (qa >= 0) {
+                const double off = (sa != 0.0) ? 0.0 : y01;
+                An[pa * lds + qa] = off;
+                An[qa * lds + pa] = off;
+                An[qa * lds + qa] = y11;
+              }
+            } else {
+              An[pa * lds + pb] = y00; An[pb * lds + pa] = y00;
+              if (qb >= 0) { An[pa * lds + qb] = y01; An[qb * lds + pa] = y01; }
+              if (qa >= 0) { An[qa * lds + pb] = y10; An[pb * lds + qa] = y10; }
+              if (qa >= 0 && qb >= 0) { An[qa * lds + qb] = y11; An[qb * lds + qa] = y11; }
+            }
+          } else {
+            const int e = it - nA, i = e / np, bq = e - i * np;
+            const int pb = plo[bq], qb = phi[bq];
+            const double cb = pc[bq], sb = ps[bq];
+            const double q0 = Qc[i * lds + pb];
+            const double q1 = (qb >= 0) ? Qc[i * lds + qb] : 0.0;
+            Qn[i * lds + pb] = fma(-sb, q1, cb * q0);
+            if (qb >= 0) Qn[i * lds + qb] = fma(sb, q0, cb * q1);
           }
         }
         __syncthreads();

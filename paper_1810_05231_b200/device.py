@@ -173,11 +173,11 @@ class DeviceBatch:
                 "residual_ms": out[2], "residual_launches": int(out[3])}
 
     def debug(self, inst: int = 0) -> dict:
-        out = np.zeros(4504)
+        out = np.zeros(4504 + 16 * 2048)
         _check(self.lib.pdsdp_debug(self.h, inst, _ptr(out)))
         bh = int(out[400 + 4096])
         return {"passes": out[:256].reshape(32, 8), "theta": out[256:320], "res": out[320:384],
-                "prof_cycles": out[384:400],
+                "prof_cycles": out[384:400], "raw": out,
                 "H": out[400:400 + bh * bh].reshape(bh, bh) if bh > 0 else None}
 
     # ---- operator norm (problem.py:157-185) ----

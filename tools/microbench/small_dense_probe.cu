@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <cmath>
 #include "small_dense.cuh"
 
 using namespace pdsdp;
@@ -23,8 +24,8 @@ __global__ void __launch_bounds__(512, 1) probe(const double* Gin, const double*
   int* tab = (int*)(theta + 64);
   int* perm = tab + 64 * 64;
   int* flag = perm + 64;
-  long long t_chol = 0, t_tri = 0, t_jac = 0, t_sort = 0, t_gemm = 0;
-  int sweeps = 0;
+  long long t_chol = 0, t_tri = 0, t_jac = 0, t_sort = 0, t_gemm = 0, t_j4 = 0;
+  int sweeps = 0, sweeps4 = 0;
   for (int rep = 0; rep < reps; ++rep) {
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[(e / b) * lds + e % b] = Gin[e];
     __syncthreads();
@@ -43,6 +44,16 @@ __global__ void __launch_bounds__(512, 1) probe(const double* Gin, const double*
     long long t5 = clock64();
     sort_desc(Aj, b, lds, theta, perm);
     long long t6 = clock64();
+    if (threadIdx.x < b) out[100 + threadIdx.x] = theta[threadIdx.x];
+    __syncthreads();
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[(e / b) * lds + e % b] = Hin[e];
+    __syncthreads();
+    long long t7 = clock64();
+    jacobi_eig4(A, M, Q, T, b, lds, cs, tab, flag + 1, b, &Aj, &Qj);
+    long long t8 = clock64();
+    sort_desc(Aj, b, lds, theta, perm);
+    if (threadIdx.x < b) out[200 + threadIdx.x] = theta[threadIdx.x] - out[100 + threadIdx.x];
+    t_j4 += t8 - t7; sweeps4 += flag[1];
     t_chol += t1 - t0; t_tri += t2 - t1; t_gemm += t3 - t2; t_jac += t5 - t4; t_sort += t6 - t5;
     sweeps += flag[0];
     if (!ok && threadIdx.x == 0) out[0] = -1;
@@ -51,7 +62,7 @@ __global__ void __launch_bounds__(512, 1) probe(const double* Gin, const double*
   }
   if (threadIdx.x == 0) {
     cyc[0] = t_chol / reps; cyc[1] = t_tri / reps; cyc[2] = t_gemm / reps; cyc[3] = t_jac / reps;
-    cyc[4] = t_sort / reps; cyc[5] = sweeps;
+    cyc[4] = t_sort / reps; cyc[5] = sweeps; cyc[6] = t_j4 / reps; cyc[7] = sweeps4;
   }
 }
 
@@ -59,7 +70,7 @@ int main() {
   const int reps = 50;
   long long* cyc; cudaMalloc(&cyc, 64 * 8);
   double *G, *H, *out;
-  cudaMalloc(&G, 64 * 64 * 8); cudaMalloc(&H, 64 * 64 * 8); cudaMalloc(&out, 128 * 8);
+  cudaMalloc(&G, 64 * 64 * 8); cudaMalloc(&H, 64 * 64 * 8); cudaMalloc(&out, 512 * 8);
   const size_t smem = 5 * 64 * 65 * 8 + (4 * 64 + 64 + 64) * 8 + (64 * 64 + 64 + 8) * 4;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   srand(1);
@@ -77,9 +88,13 @@ int main() {
       cudaMemcpy(H, h.data(), b * b * 8, cudaMemcpyHostToDevice);
       probe<<<1, 512, smem>>>(G, H, b, reps, cyc, out);
       cudaError_t e = cudaDeviceSynchronize();
-      long long c[8]; cudaMemcpy(c, cyc, 6 * 8, cudaMemcpyDeviceToHost);
+      long long c[8]; cudaMemcpy(c, cyc, 8 * 8, cudaMemcpyDeviceToHost);
+      double dv[64]; cudaMemcpy(dv, out + 200, 64 * 8, cudaMemcpyDeviceToHost);
+      double mx = 0; for (int i = 0; i < b; ++i) mx = fmax(mx, fabs(dv[i]));
       printf("b=%2d off=%.0e: chol %6lld  tri_inv %6lld  gemm %6lld  jacobi %7lld (%.2f sweeps, %5.0f cyc/sweep)  sort %5lld  [%s]\n",
              b, off, c[0], c[1], c[2], c[3], c[5] / (double)reps, c[3] / (c[5] / (double)reps), c[4], cudaGetErrorString(e));
+      printf("        jacobi_eig4 %7lld (%.2f sweeps, %5.0f cyc/sweep)  max |dtheta| vs eig3 %.2e\n", c[6], c[7] / (double)reps,
+             c[6] / (c[7] / (double)reps), mx);
     }
   }
   return 0;
