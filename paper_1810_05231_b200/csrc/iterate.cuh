@@ -28,6 +28,12 @@ namespace pdsdp {
 #define PDSDP_TOL_CERT 1e-8
 #define PDSDP_TOL_CLIP 1e-6
 #define PDSDP_MMAX 24
+// largest amplification of a column's contamination the filter may cause:
+// CholQR2 re-orthonormalises blocks with condition up to ~1e8, so 1e6 keeps
+// a 100x margin (was 1e4)
+#ifndef PDSDP_SPREAD_CAP
+#define PDSDP_SPREAD_CAP 1e6
+#endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
 #endif
@@ -748,7 +754,7 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
   const double tb = (theta[a1 - 1] - c_) / e_;
   const double spread = acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? acosh(tb) : 0.0);
   int mcap = PDSDP_MMAX;
-  if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(1e4 / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
+  if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(PDSDP_SPREAD_CAP / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
   if (mcap < 2) mcap = 2;
   return mcap;
 }
