@@ -123,10 +123,12 @@ int pdsdp_apply_M_adjoint(pdsdp_batch* b, int inst, const double* y, double* out
 int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_packed_out, double* lambda_out);
 
 /* Per-kernel CUDA-event timing of pdsdp_iterate (for the roofline report):
- * out[0] iterate-kernel ms total, out[1] launches, out[2] residual-kernel ms
- * total (verification mode only), out[3] launches.  enable != 0 switches recording on and clears. */
+ * out[0] ms spanned by the executed iteration-kernel launches (CUDA events on
+ * the library stream, one per launch), out[1] iterations executed, out[2]
+ * residual-kernel ms (verification mode only), out[3] its launches, out[4]
+ * iteration-kernel launches issued.  enable != 0 switches recording on and clears. */
 int pdsdp_set_timing(pdsdp_batch* b, int enable);
-int pdsdp_kernel_times(pdsdp_batch* b, double* out /* [4] */);
+int pdsdp_kernel_times(pdsdp_batch* b, double* out /* [5] */);
 
 /* Verification mode: after every iteration also evaluate the dense part
  * ||dX/alpha||_F^2 of the primal residual (reference pdhg.py:198-208) entry by

@@ -439,6 +439,94 @@ __device__ __forceinline__ void copy_rows_in(const double* __restrict__ src, int
   }
 }
 
+// out (nl x b) = In (nl x b, shared memory) * Msm (b x b, shared memory) on
+// FP64 tensor cores (mma.sync.m8n8k4.f64): one warp per 8-row tile, all
+// 8-column tiles of the row tile at once (the A fragment is loaded once per
+// k-step).  A scalar product reads 16 bytes of shared memory per FMA; this
+// reads ~2 (the b x b rotations of a Rayleigh-Ritz pass were bound by it).
+// With In2 / out2 a second block sharing Msm is rotated in the same sweep;
+// with th != nullptr the column sums of (out2 - th .* out)^2 over the rows
+// are accumulated (Ritz residual norms, fixed-order reduction) into gout[b].
+__device__ void rot_mma(const double* __restrict__ In, int ldi, const double* __restrict__ In2, int ldi2,
+                        const double* __restrict__ Msm, int lds, double* __restrict__ out, int ldo,
+                        double* __restrict__ out2, int ldo2, int nl, int b, const double* __restrict__ th,
+                        double* __restrict__ gout, double* __restrict__ scr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int nw = blockDim.x >> 5;
+  const int mt = (nl + 7) >> 3, ntl = (b + 7) >> 3;   // ntl <= 8
+  double cres[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { cres[q][0] = 0.0; cres[q][1] = 0.0; }
+  for (int tm = warp; tm < mt; tm += nw) {
+    const int row = tm * 8 + g;
+    const bool rv = row < nl;
+    double acc[8][2], acc2[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { acc[q][0] = acc[q][1] = 0.0; acc2[q][0] = acc2[q][1] = 0.0; }
+    for (int t0 = 0; t0 < b; t0 += 4) {
+      const int t = t0 + tq;
+      const bool tv = t < b;
+      const double a = (rv && tv) ? In[(size_t)row * ldi + t] : 0.0;
+      const double a2 = (In2 && rv && tv) ? In2[(size_t)row * ldi2 + t] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < ntl) {
+          const int col = q * 8 + g;
+          const double bm = (tv && col < b) ? Msm[t * lds + col] : 0.0;
+          dmma884(acc[q][0], acc[q][1], a, bm);
+          if (In2) dmma884(acc2[q][0], acc2[q][1], a2, bm);
+        }
+      }
+    }
+    // D fragment: row tm*8+g, columns q*8 + 2tq + h
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < ntl && rv) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = q * 8 + 2 * tq + h;
+          if (col < b) {
+            out[(size_t)row * ldo + col] = acc[q][h];
+            if (out2) out2[(size_t)row * ldo2 + col] = acc2[q][h];
+            if (th) {
+              const double rr = acc2[q][h] - th[col] * acc[q][h];
+              cres[q][h] = fma(rr, rr, cres[q][h]);
+            }
+          }
+        }
+      }
+    }
+  }
+  if (th) {
+    // lanes with the same tq hold the same columns: reduce over g (xor 4, 8, 16)
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = cres[q][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        cres[q][h] = v;
+      }
+    if (g == 0)
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = q * 8 + 2 * tq + h;
+          if (col < b) scr[warp * PDSDP_BMAX + col] = cres[q][h];
+        }
+    __syncthreads();
+    if ((int)threadIdx.x < b) {
+      double tsum = 0.0;
+      for (int w = 0; w < nw; ++w) tsum += scr[w * PDSDP_BMAX + threadIdx.x];
+      gout[threadIdx.x] = tsum;
+    }
+  }
+  __syncthreads();
+}
+
 // out (nl x b, stride ldo) = In (nl x b, stride ldi) * Msm (b x b, stride lds);
 // In in shared memory, out in shared or global memory
 __device__ __forceinline__ void rot_block(const double* In, int ldi, const double* Msm, int lds,
@@ -735,6 +823,87 @@ __device__ Assess assess(const double* theta, const double* res, int r, int b, i
   return a;
 }
 
+// Warp-parallel forms of the per-column scans above: every warp evaluates
+// them independently (lanes stride the columns, fixed xor-shuffle trees), so
+// all threads of all CTAs hold identical results without a barrier.  A
+// sequential scan over up to 64 columns with FP64 divisions was several
+// microseconds on the critical path of every pass.
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_maxi(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_mini(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// ||X+||_F estimate sqrt(sum_{i<min(r,b)} max(theta_i, 0)^2)
+__device__ __forceinline__ double kept_norm_w(const double* theta, int r, int b) {
+  const int lane = threadIdx.x & 31, nk = min(r, b);
+  double acc = 0.0;
+  for (int i = lane; i < nk; i += 32) { const double t = fmax(theta[i], 0.0); acc = fma(t, t, acc); }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return sqrt(acc);
+}
+__device__ Assess assess_w(const double* theta, const double* res, int r, int b, int k, double scale,
+                           double xnorm, double cert_tol) {
+  Assess a{-1, false, false, 1.0, 0.0};
+  const int lane = threadIdx.x & 31;
+  const double inv_scale = 1.0 / scale;
+  const double inv_tk = 1.0 / fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
+  int last = -1, cert = 0;
+  double mr = 0.0, rk = 1.0;
+  for (int i = lane; i < k; i += 32) {
+    const double ri = res[i];
+    if (col_ok(i, ri, theta, r, b, scale, xnorm, cert_tol)) continue;
+    mr = fmax(mr, ri * inv_scale);
+    if (i < r) { last = max(last, i); rk = fmax(rk, ri * inv_tk); }
+    else cert = 1;
+  }
+  a.last_bad = warp_maxi(last);
+  a.cert_bad = warp_maxi(cert) != 0;
+  a.maxres = warp_max(mr);
+  a.rho_k = warp_max(rk);
+  if (r < b && r < k + 1 && r >= 1) {
+    const double lo_k = theta[r - 1] - 2.0 * res[r - 1];
+    const double hi_t = theta[r] + 2.0 * res[r];
+    if (!(hi_t < lo_k) && res[r] > PDSDP_TOL_CERT * scale &&
+        !(theta[r] + res[r] < 0.0 && res[r] <= PDSDP_TOL_CLIP * scale) &&
+        !(cert_tol < 0.0 && theta[r] < 0.0 && res[r] <= 0.1 * -theta[r])) {
+      a.tail_bad = true;
+      a.maxres = fmax(a.maxres, res[r] * inv_scale);
+    }
+  }
+  return a;
+}
+// leading columns [0, n) that are col_ok, n <= lim
+__device__ __forceinline__ int leading_ok_w(const double* theta, const double* res, int r, int b, int lim,
+                                            double scale, double xnorm, double cert_tol) {
+  const int lane = threadIdx.x & 31;
+  int first_bad = lim;
+  for (int i = lane; i < lim; i += 32)
+    if (!col_ok(i, res[i], theta, r, b, scale, xnorm, cert_tol)) first_bad = min(first_bad, i);
+  return warp_mini(first_bad);
+}
+
+// Filter-planning heuristics (degrees, caps, slack) need ~3 digits: FP32
+// hardware approximations instead of the FP64 software log / acosh (each a
+// few hundred dependent cycles, on the critical path of every pass).
+__device__ __forceinline__ double plan_log(double x) {
+  return (double)__logf((float)fmin(fmax(x, 1e-37), 1e37));
+}
+__device__ __forceinline__ double plan_acosh(double x) {   // x >= 1
+  const float xf = (float)fmin(fmax(x, 1.0), 1e18);
+  return (double)__logf(xf + sqrtf((xf - 1.0f) * (xf + 1.0f)));
+}
+
 // Chebyshev filter for columns [a0, a1): damp [lo, cut], scale at `top`;
 // degree to reduce a column at `slow` by `rho`, and a cap keeping the
 // amplification spread across the active columns below ~1e4/eps_rel
@@ -749,12 +918,12 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
   if (top - c_ <= e_) top = c_ + 1.0001 * e_;
   s_ = e_ / (top - c_);
   const double ts = (slow - c_) / e_;
-  const double at = (ts > 1.0 + 1e-6) ? acosh(ts) : 0.0;
-  mm = (at > 0.0) ? (int)ceil(acosh(fmax(rho, 1.0)) / at) + 1 : 8;
+  const double at = (ts > 1.0 + 1e-6) ? plan_acosh(ts) : 0.0;
+  mm = (at > 0.0) ? (int)ceil(plan_acosh(fmax(rho, 1.0)) / at) + 1 : 8;
   const double tb = (theta[a1 - 1] - c_) / e_;
-  const double spread = acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? acosh(tb) : 0.0);
+  const double spread = plan_acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? plan_acosh(tb) : 0.0);
   int mcap = PDSDP_MMAX;
-  if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(log(PDSDP_SPREAD_CAP / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
+  if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(plan_log(PDSDP_SPREAD_CAP / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
   if (mcap < 2) mcap = 2;
   return mcap;
 }
@@ -1009,10 +1178,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     double fe = 1.0, fc = 0.0, sig1 = 1.0;
     if (theta_valid && b < n) {
       const double scale = fmax(fmax(fabs(s.theta[0]), fabs(lo)), 1e-300);
-      double xnorm = 0.0;
-      for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
-      xnorm = sqrt(xnorm);
-      const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
+      const double xnorm = kept_norm_w(s.theta, r, b);
+      const Assess as = assess_w(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
       const bool stale = (pass == 0 && !rerun);   // residuals belong to the previous S
       const double eps_rel = fmax(as.maxres, stale ? 1e-3 : 0.0);
       int mcap = PDSDP_MMAX;
@@ -1022,7 +1189,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       // just below the cut instead of riding along unfiltered)
       int nconv = 0;
       if (!stale && as.last_bad >= 0)
-        while (nconv < as.last_bad && col_ok(nconv, s.res[nconv], s.theta, r, b, scale, xnorm, cert_tol)) ++nconv;
+        nconv = leading_ok_w(s.theta, s.res, r, b, as.last_bad, scale, xnorm, cert_tol);
       if (nconv >= 1) {
         nlock = nconv; c0 = nconv; bc = b - nconv;
         mcap = cheb_plan(s.theta, b, lo, s.theta[nconv], s.theta[b - 1], s.theta[as.last_bad], as.rho_k, scale,
@@ -1217,11 +1384,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (rsm) {
       copy_rows_in(buf(iy) + (size_t)x.r0 * ld, ld, S0, nlr, b);
       __syncthreads();
-      rot_block(S0, b, s.M, lds, S1, b, nlr, b);
-      __syncthreads();
+      rot_mma(S0, b, nullptr, 0, s.M, lds, S1, b, nullptr, 0, nlr, b, nullptr, nullptr, nullptr);
       copy_rows_in(buf(iw) + (size_t)x.r0 * ld, ld, S0, nlr, b);
       __syncthreads();
-      rot_block(S0, b, s.M, lds, S2, b, nlr, b);
+      rot_mma(S0, b, nullptr, 0, s.M, lds, S2, b, nullptr, 0, nlr, b, nullptr, nullptr, nullptr);
     } else {
       rotate_rows(d, x, buf(iy), s.M, lds, buf(iav), b);
       rotate_rows(d, x, buf(iw), s.M, lds, buf(iw1), b);
@@ -1308,29 +1474,31 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // V = Y1 B ; AV = W1 B  (AV goes to buf(iw), which becomes the AV buffer)
     prof_mark(pf, 5);
     if (rsm) {
-      rot_block(S1, b, Bm, lds, d.V + (size_t)x.r0 * ld, ld, nlr, b);
-      rot_block(S2, b, Bm, lds, buf(iw) + (size_t)x.r0 * ld, ld, nlr, b);
+      // V = Y1 B, AV = W1 B and the Ritz residual partials in one DMMA sweep
+      rot_mma(S1, b, S2, b, Bm, lds, d.V + (size_t)x.r0 * ld, ld, buf(iw) + (size_t)x.r0 * ld, ld, nlr, b,
+              s.theta, red_slot(d, x, x.c), s.gsc);
+      prof_mark(pf, 4);
     } else {
       rotate_rows(d, x, buf(iav), Bm, lds, d.V, b);
       rotate_rows(d, x, buf(iw1), Bm, lds, buf(iw), b);
+      __syncthreads();
+      prof_mark(pf, 4);
+      colres_partial(buf(iw), d.V, s.theta, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
     }
     iav = iw;
     av_valid = true;
     theta_valid = true;
-    __syncthreads();
     // ---- R3: residual norms ----
-    prof_mark(pf, 4);
-    colres_partial(buf(iav), d.V, s.theta, b, ld, x.r0, x.r1, red_slot(d, x, x.c), s.scr);
     cluster_reduce(d, x, b, 0, s.red1);
+    prof_tick(pf, 70);
     ++passes;
     {
       double scale = fmax(fmax(fabs(s.theta[0]), fabs(lo)), 1e-300);
-      double xnorm = 0.0;
-      for (int i = 0; i < r && i < b; ++i) xnorm += fmax(s.theta[i], 0.0) * fmax(s.theta[i], 0.0);
-      xnorm = sqrt(xnorm);
+      const double xnorm = kept_norm_w(s.theta, r, b);
       for (int i = tid; i < b; i += blockDim.x) s.res[i] = sqrt(fmax(s.red1[i], 0.0));
       __syncthreads();
-      const Assess as = assess(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
+      const Assess as = assess_w(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
+      prof_tick(pf, 71);
       maxres = as.maxres;
       ++since_grow;
       if (r < r_t) {
@@ -1369,12 +1537,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         // each kept column's tolerance (Chebyshev gain acosh(t) per degree)
         if (m > 0 && pass == 0) {
           double sl = 1.0e300;
-          for (int i = 0; i < r && i < b; ++i) {
-            const double t = (s.theta[i] - fc) / fe;
-            if (t <= 1.0 + 1e-6) { sl = 0.0; break; }
-            const double tol = fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
-            sl = fmin(sl, log(tol / fmax(s.res[i], 1e-300)) / acosh(t));
+          const double tol = fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
+          const double ife = 1.0 / fe;
+          for (int i = (tid & 31); i < r && i < b; i += 32) {
+            const double t = (s.theta[i] - fc) * ife;
+            if (t <= 1.0 + 1e-6) { sl = 0.0; continue; }
+            sl = fmin(sl, plan_log(tol / fmax(s.res[i], 1e-300)) / plan_acosh(t));
           }
+          sl = -warp_max(-sl);
           slack = (sl > 0.0 && sl < 64.0) ? (int)floor(sl) : (sl >= 64.0 ? 64 : 0);
         }
         break;
@@ -1384,6 +1554,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       prev_maxres = maxres;
     }
   }
+  prof_tick(pf, 72);
   for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) s.lamN[i] = (i < r && i < b && s.theta[i] > 0.0) ? s.theta[i] : 0.0;
   __syncthreads();
 
@@ -1419,6 +1590,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     __syncthreads();
   }
   double ed2 = 0.0, fin = 1.0, dysd = 0.0;   // dysd: <dy, M(X+ - X)> = <M^T dy, dX>
+  prof_tick(pf, 60);
   {
     const int G = d.group;
     const int lane = tid & 31, sub = lane % G;
@@ -1460,6 +1632,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       }
     }
   }
+  prof_tick(pf, 61);
   // block reduce ed2, dysd (sums), fin (min -> max of negatives)
   {
     double v = warp_sum(ed2);

@@ -102,7 +102,8 @@ struct pdsdp_batch {
   int timing = 0;
   int verify_residual = 0;   // also run residual_kernel (exact dense term) after each step
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0;
+  double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0, n_launch = 0.0;
+  cudaEvent_t tev[PDSDP_KMAX + 1] = {};
 };
 
 namespace {
@@ -591,6 +592,7 @@ int pdsdp_batch_destroy(pdsdp_batch* b) {
   if (b->d_objres) cudaFree(b->d_objres);
   if (b->d_stop) cudaFree(b->d_stop);
   for (int k = 0; k < 3; ++k) if (b->ev[k]) cudaEventDestroy(b->ev[k]);
+  for (int k = 0; k <= PDSDP_KMAX; ++k) if (b->tev[k]) cudaEventDestroy(b->tev[k]);
   if (b->stream) cudaStreamDestroy(b->stream);
   delete b;
   return PDSDP_OK;
@@ -725,25 +727,21 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
   CK(cudaMemsetAsync(b->d_stop, 0, (size_t)N * sizeof(int), b->stream));
   const int kp = std::min(RES_KMAX, (2 * std::min(maxr, PDSDP_BMAX) + 3) & ~3);
   const size_t rsm = (size_t)2 * RES_TILE * (kp + 1) * sizeof(double);
+  // timing: one event before the chunk and one after every iteration launch,
+  // so the span of exactly the executed iterations is known after the sync
+  if (b->timing) CK(cudaEventRecord(b->tev[0], b->stream));
   for (int j = 0; j < K; ++j) {
-    const bool tm = b->timing && j == 0;
-    if (tm) CK(cudaEventRecord(b->ev[0], b->stream));
     int rc = launch_iterate(b, nact, lds, j);
     if (rc) return rc;
-    if (tm) CK(cudaEventRecord(b->ev[1], b->stream));
     if (b->verify_residual) {
       residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_ctl, b->d_active, j);
       CK(cudaGetLastError());
     }
-    if (tm) CK(cudaEventRecord(b->ev[2], b->stream));
+    if (b->timing) CK(cudaEventRecord(b->tev[j + 1], b->stream));
   }
   CK(cudaStreamSynchronize(b->stream));
-  if (b->timing) {
-    float t1 = 0.f, t2 = 0.f;
-    CK(cudaEventElapsedTime(&t1, b->ev[0], b->ev[1]));
-    CK(cudaEventElapsedTime(&t2, b->ev[1], b->ev[2]));
-    b->t_iter += t1; b->n_iter += 1; b->t_res += t2; b->n_res += 1;
-  }
+  b->n_launch += K;
+  int done_max = 0;
   for (int a = 0; a < nact; ++a) {
     int done = 0;
     for (int j = 0; j < K; ++j) {
@@ -755,6 +753,12 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
                                      std::to_string(PDSDP_BMAX) + " holds (PDSDP_BMAX)");
     }
     if (steps_done) steps_done[a] = done;
+    done_max = std::max(done_max, done);
+  }
+  if (b->timing && done_max > 0) {
+    float t1 = 0.f;
+    CK(cudaEventElapsedTime(&t1, b->tev[0], b->tev[done_max]));
+    b->t_iter += t1; b->n_iter += done_max;
   }
   return PDSDP_OK;
 }
@@ -768,8 +772,10 @@ int pdsdp_set_timing(pdsdp_batch* b, int enable) {
   if (!b) return fail(PDSDP_EINVAL, "batch is NULL");
   for (int k = 0; k < 3; ++k)
     if (!b->ev[k]) CK(cudaEventCreate(&b->ev[k]));
+  for (int k = 0; k <= PDSDP_KMAX; ++k)
+    if (!b->tev[k]) CK(cudaEventCreate(&b->tev[k]));
   b->timing = enable ? 1 : 0;
-  b->t_iter = b->n_iter = b->t_res = b->n_res = 0.0;
+  b->t_iter = b->n_iter = b->t_res = b->n_res = b->n_launch = 0.0;
   return PDSDP_OK;
 }
 
@@ -801,7 +807,7 @@ int pdsdp_debug(pdsdp_batch* b, int inst, double* out) {
 
 int pdsdp_kernel_times(pdsdp_batch* b, double* out) {
   if (!b || !out) return fail(PDSDP_EINVAL, "bad arguments");
-  out[0] = b->t_iter; out[1] = b->n_iter; out[2] = b->t_res; out[3] = b->n_res;
+  out[0] = b->t_iter; out[1] = b->n_iter; out[2] = b->t_res; out[3] = b->n_res; out[4] = b->n_launch;
   return PDSDP_OK;
 }
 

@@ -167,10 +167,10 @@ class DeviceBatch:
         _check(self.lib.pdsdp_set_verify_residual(self.h, 1 if enable else 0))
 
     def kernel_times(self) -> dict:
-        out = np.zeros(4)
+        out = np.zeros(5)
         _check(self.lib.pdsdp_kernel_times(self.h, _ptr(out)))
-        return {"iterate_ms": out[0], "iterate_launches": int(out[1]),
-                "residual_ms": out[2], "residual_launches": int(out[3])}
+        return {"iterate_ms": out[0], "iterations": int(out[1]),
+                "residual_ms": out[2], "residual_launches": int(out[3]), "launches": int(out[4])}
 
     def debug(self, inst: int = 0) -> dict:
         out = np.zeros(4504 + 16 * 2048)

@@ -25,7 +25,7 @@ for k in range(K):
     pc += b.debug(0)["prof_cycles"]
 dt = time.perf_counter() - t
 kt = b.kernel_times()
-print(f"n={prob.n} r={r} K={K}: loop {1e6*dt/K:.1f} us/iter; iterate kernel {1e3*kt['iterate_ms']/K:.1f} us; "
+print(f"n={prob.n} r={r} K={K}: loop {1e6*dt/K:.1f} us/iter; iterate kernel {1e3*kt['iterate_ms']/max(1,kt['iterations']):.1f} us; "
       f"residual kernel {1e3*kt['residual_ms']/K:.1f} us; matvecs/iter {mv/K:.2f} passes/iter {ps/K:.2f}")
 names = ["prologue/epilogue", "op gram", "op cluster-reduce", "op apply", "R2 reduce, R3+assess+plan", "rotations+R2 gram", "dual step", "adjoint+epilogue",
          "chol", "tri_inv+M1", "DHD+gemms", "jacobi", "sort+B", "apply: staging issue", "apply: staging wait", "jacobi sweeps (count)"]

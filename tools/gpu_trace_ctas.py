@@ -26,6 +26,7 @@ same = all(np.array_equal(e[:n, 0], labels[:n]) for e in evs)
 print("identical label sequences:", same)
 tot = np.array([(e[n - 1, 1] - e[0, 1]) / 1965.0 for e in evs])
 print("total us per CTA:", np.round(tot, 1))
-for i in range(1, min(n, nshow)):
+lo = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+for i in range(max(1, lo), min(n, nshow)):
     d = np.array([(e[i, 1] - e[i - 1, 1]) / 1965.0 for e in evs])
     print(f"{i:3d} [{int(labels[i-1]):2d}->{int(labels[i]):2d}]  min {d.min():6.2f}  med {np.median(d):6.2f}  max {d.max():6.2f} (cta {d.argmax():2d})  cta0 {d[0]:6.2f}")
