@@ -1337,24 +1337,47 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     const int iw = (iy == 0) ? fre(0) : fre((m) % 3);          // free of {Y_m, Y_{m-1}} ring
     int iw1 = -1;
     for (int q2 = 0; q2 < 3; ++q2) if (fre(q2) != iy && fre(q2) != iw) { iw1 = fre(q2); break; }
-    {
-      double* slot = red_slot(d, x, x.c);
+    if (s.own) {
+      // W = S Y through the own-row operator step (multicast all-gather of the
+      // block, smem-resident F rows); G1 = Y^T Y rides in the step's reduction
+      const int nl = x.r1 - x.r0, bcp = own_stride(b);
       prof_mark(pf, 1);
-      gram_mma(buf(iy), b, buf(iy), b, ld, x.r0, x.r1, slot, s.gsc);
-      gram_mma(d.F, rFx, buf(iy), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
-      // reduce T now; G1 after the product (whose staging buffer overlays A)
-      cg::this_cluster().sync();
-      for (int i = tid; i < rFx * b; i += blockDim.x) s.T[i] = cluster_sum(d, x, b * b + i, false);
+      for (int it = tid; it < nl * b; it += blockDim.x) {
+        const int lr = it / b, jj = it - lr * b;
+        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = buf(iy)[(size_t)(x.r0 + lr) * ld + jj];
+      }
+      fence_proxy_async();
+      __syncthreads();
+      gram_mma2(d.Yc + (size_t)x.r0 * bcp, bcp, b, d.Yc + (size_t)x.r0 * bcp, bcp, b, 0, nl,
+                red_slot(d, x, x.c) + rFx * b, s.gsc);
+      int ycp_rr = 0;
+      bool gr = false;
+      operator_step_own(d, x, s, zv, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0, pf, ycp_rr, &mbar_sm, mphase, gr, false);
+      __syncthreads();
+      Cta xp = x;
+      xp.par ^= 1;    // the step's reduction slot
+      for (int i = tid; i < b * b; i += blockDim.x) s.A[(i / b) * lds + (i % b)] = cluster_sum(d, xp, rFx * b + i, false);
+      __syncthreads();
+    } else {
+      {
+        double* slot = red_slot(d, x, x.c);
+        prof_mark(pf, 1);
+        gram_mma(buf(iy), b, buf(iy), b, ld, x.r0, x.r1, slot, s.gsc);
+        gram_mma(d.F, rFx, buf(iy), b, ld, x.r0, x.r1, slot + b * b, s.gsc);
+        // reduce T now; G1 after the product (whose staging buffer overlays A)
+        cg::this_cluster().sync();
+        for (int i = tid; i < rFx * b; i += blockDim.x) s.T[i] = cluster_sum(d, x, b * b + i, false);
+        __syncthreads();
+      }
+      scale_T(s, rFx, 0, b);
+      prof_mark(pf, 3);
+      if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
+      else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
+      __syncthreads();
+      for (int i = tid; i < b * b; i += blockDim.x) s.A[(i / b) * lds + (i % b)] = cluster_sum(d, x, i, false);
+      x.par ^= 1;
       __syncthreads();
     }
-    scale_T(s, rFx, 0, b);
-    prof_mark(pf, 3);
-    if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
-    else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
-    __syncthreads();
-    for (int i = tid; i < b * b; i += blockDim.x) s.A[(i / b) * lds + (i % b)] = cluster_sum(d, x, i, false);
-    x.par ^= 1;
-    __syncthreads();
     prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
