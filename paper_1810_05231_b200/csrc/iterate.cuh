@@ -585,6 +585,11 @@ __device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s
 #define PDSDP_OWN_ITEMS 3      // (row, 4-column chunk) items per thread
 #endif
 __device__ __forceinline__ int own_stride(int bc) { return (bc + 3) & ~3; }
+// row stride of the compact operand block: an odd number of 16-byte units,
+// so the 16-byte loads of different rows at the same column chunk fall in
+// different shared-memory bank groups (a multiple of 128 bytes put them all
+// in the same group: 2-way conflicts on every operand load)
+__device__ __forceinline__ int own_ystr(int bc) { return own_stride(bc) + 2; }
 // the locked pairs' own rows are copied next to F's in shared memory when
 // they fit the row stride of SF
 __device__ __forceinline__ bool own_lock_sm(int rFx, int nlock, int sl) { return nlock > 0 && rFx + nlock <= sl; }
@@ -596,7 +601,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
                                                   bool& gram_ready, bool gram_next) {
   prof_mark(pf, 1);
   const int nl = x.r1 - x.r0, sl = s.sld, ld = d.ld, n = d.n, tid = threadIdx.x;
-  const int bcp = own_stride(bc), nch = bcp >> 2;
+  const int bcp = own_stride(bc), nch = bcp >> 2, ys_ = own_ystr(bc);
   const size_t nld = (size_t)n * (ld + 4);
   const double* Ycur = d.Yc + (size_t)ycp * nld;
   double* Ynxt = d.Yc + (size_t)(ycp ^ 1) * nld;
@@ -604,10 +609,10 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
-      gram_mma2(s.SF, sl, rF + nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
+      gram_mma2(s.SF, sl, rF + nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
     } else {
-      gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl, slot, s.gsc);
-      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * bcp, bcp, bc, 0, nl,
+      gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl,
                 slot + rF * bc, s.gsc);
     }
   }
@@ -618,7 +623,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const double alpha = d.alpha;
   const double* ys = s.ys;
   const int C = x.C;
-  const int rows_cap = s.ycap / bcp;
+  const int rows_cap = s.ycap / ys_;
   const unsigned short mask = (unsigned short)((1u << C) - 1u);
   const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
   const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
@@ -642,11 +647,11 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     while (g1 < C && s.gb[g1 + 1] - R0 <= rows_cap) ++g1;
     const int R1 = s.gb[g1];
     if (tid == 0) {
-      mbar_expect_tx(mbar, (unsigned)((R1 - R0) * bcp * 8));
+      mbar_expect_tx(mbar, (unsigned)((R1 - R0) * ys_ * 8));
       if (x.c >= g0 && x.c < g1) {
-        const char* src = reinterpret_cast<const char*>(Ycur + (size_t)x.r0 * bcp);
-        char* dst = reinterpret_cast<char*>(s.ys + (size_t)(x.r0 - R0) * bcp);
-        unsigned left = (unsigned)(nl * bcp * 8), off = 0;
+        const char* src = reinterpret_cast<const char*>(Ycur + (size_t)x.r0 * ys_);
+        char* dst = reinterpret_cast<char*>(s.ys + (size_t)(x.r0 - R0) * ys_);
+        unsigned left = (unsigned)(nl * ys_ * 8), off = 0;
         while (left > 0) {
           const unsigned piece = left > 65536u ? 65536u : left;
           bulk_multicast(dst + off, src + off, piece, mbar, mask);
@@ -678,7 +683,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       const int it = tid + u * blockDim.x;
       if (it >= nitems) break;
       const int cq = it % nch;
-      const double* yb = ys + 4 * cq - (size_t)R0 * bcp;
+      const double* yb = ys + 4 * cq - (size_t)R0 * ys_;
       int e = ep[u];
       const int e1 = ee[u];
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -686,8 +691,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
         const int q = zcol[e];
         if (q >= R1) break;
         const double zv_ = zval[e];
-        const double2 p0 = *reinterpret_cast<const double2*>(yb + (size_t)q * bcp);
-        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q * bcp + 2);
+        const double2 p0 = *reinterpret_cast<const double2*>(yb + (size_t)q * ys_);
+        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q * ys_ + 2);
         a0 = fma(zv_, p0.x, a0); a1 = fma(zv_, p0.y, a1);
         a2 = fma(zv_, p1.x, a2); a3 = fma(zv_, p1.y, a3);
       }
@@ -712,7 +717,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     const int lr = it / nch, cq = it - lr * nch;
     const double* Fr = s.SF + (size_t)lr * sl;
     const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
-    const size_t oc = (size_t)(x.r0 + lr) * bcp + 4 * cq;
+    const size_t oc = (size_t)(x.r0 + lr) * ys_ + 4 * cq;
     // recurrence terms Y_j, Y_{j-1} of the item, loaded before its stores
     // (which may alias them as far as the compiler knows: one L2 round trip
     // per item instead of one per element)
@@ -769,15 +774,15 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       if (it >= nitems) break;
       const int lr = it / nch, cq = it - lr * nch;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) yo[(size_t)lr * bcp + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
+      for (int v = 0; v < 4; ++v) yo[(size_t)lr * ys_ + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
     }
     __syncthreads();
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
-      gram_mma2(s.SF, sl, rF + nlock, yo, bcp, bc, 0, nl, slot, s.gsc);
+      gram_mma2(s.SF, sl, rF + nlock, yo, ys_, bc, 0, nl, slot, s.gsc);
     } else {
-      gram_mma2(s.SF, sl, rF, yo, bcp, bc, 0, nl, slot, s.gsc);
-      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, yo, bcp, bc, 0, nl, slot + rF * bc, s.gsc);
+      gram_mma2(s.SF, sl, rF, yo, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, yo, ys_, bc, 0, nl, slot + rF * bc, s.gsc);
     }
     gram_ready = true;
   }
@@ -1068,7 +1073,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.sld = lcap;
     s.ycap = ycap + 4 * sq;
     {
-      const int nl = x.r1 - x.r0, sp = own_stride(lcap);
+      const int nl = x.r1 - x.r0, sp = own_ystr(lcap);
       s.own = (owncap > 0 && nl * lcap <= owncap && nl <= nlmax && nl * sp <= s.ycap &&
                nl * (sp / 4) <= PDSDP_OWN_ITEMS * PDSDP_NTHR) ? 1 : 0;
     }
@@ -1239,7 +1244,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (m > 0 && s.own) {
       // own rows of V (the recurrence's Y_0) into the compact multicast source
       const int nl = x.r1 - x.r0;
-      const int bcp = own_stride(bc);
+      const int bcp = own_ystr(bc);   // compact row stride
       const size_t nld = (size_t)n * (ld + 4);
       int ycp = 0;
       bool gram_ready = false;
@@ -1340,7 +1345,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (s.own) {
       // W = S Y through the own-row operator step (multicast all-gather of the
       // block, smem-resident F rows); G1 = Y^T Y rides in the step's reduction
-      const int nl = x.r1 - x.r0, bcp = own_stride(b);
+      const int nl = x.r1 - x.r0, bcp = own_ystr(b);   // compact row stride
       prof_mark(pf, 1);
       for (int it = tid; it < nl * b; it += blockDim.x) {
         const int lr = it / b, jj = it - lr * b;
