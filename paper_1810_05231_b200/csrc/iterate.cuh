@@ -1386,7 +1386,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     prof_mark(pf, 8);
     ++matvecs;
     // ---- small: M1 = D L^-T ----
-    bool okc = chol_scaled_1s(s.A, b, lds, s.dsc);
+    bool okc = chol_scaled_rows(s.A, b, lds, s.dsc);
     if (!okc) {
       // breakdown: the filtered block lost rank; retry from V with half the degree
       if (++fails >= 8 || m == 0) break;
@@ -1395,7 +1395,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       continue;
     }
     prof_mark(pf, 9);
-    tri_inv_lower_1s(s.A, s.L, b, lds);
+    tri_inv_lower_rows(s.A, s.L, b, lds);
     for (int e = tid; e < b * b; e += blockDim.x) {
       int i = e / b, j = e % b;
       s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
@@ -1444,7 +1444,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe
     prof_mark(pf, 8);
-    okc = chol_scaled_1s(s.A, b, lds, s.dsc);
+    okc = chol_scaled_rows(s.A, b, lds, s.dsc);
     if (!okc) {
       if (++fails >= 8 || m == 0) break;
       force_m = m / 2;
@@ -1452,7 +1452,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     if (nlock == 0) msucc += m;
     prof_mark(pf, 9);
-    tri_inv_lower_1s(s.A, s.L, b, lds);            // L = L2^-1
+    tri_inv_lower_rows(s.A, s.L, b, lds);            // L = L2^-1
     prof_mark(pf, 10);
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
@@ -1628,14 +1628,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const int i = i0 + gid;
       double s2 = 0.0, sd = 0.0;
       if (i < a1) {
-        for (int e = d.aptr[i] + sub; e < d.aptr[i + 1]; e += G) {
-          const int p = d.ai[e], q = d.aj[e];
+        for (int e = __ldg(d.aptr + i) + sub; e < __ldg(d.aptr + i + 1); e += G) {
+          const int p = __ldg(d.ai + e), q = __ldg(d.aj + e);
           const double* Vp = d.V + (size_t)p * ld; const double* Vq = d.V + (size_t)q * ld;
           const double* Fp = d.F + (size_t)p * ld; const double* Fq = d.F + (size_t)q * ld;
           double xn = 0.0, xo = 0.0;
           for (int l = 0; l < rN; ++l) if (s.lamN[l] != 0.0) xn = fma(Vp[l] * s.lamN[l], Vq[l], xn);
           for (int l = 0; l < rF; ++l) if (s.lamF[l] != 0.0) xo = fma(Fp[l] * s.lamF[l], Fq[l], xo);
-          const double g = d.ag[e];
+          const double g = __ldg(d.ag + e);
           s2 = fma(g, 2.0 * xn - xo, s2);
           sd = fma(g, xn - xo, sd);
         }
@@ -1711,17 +1711,23 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   double corr = 0.0;
   double cu[PDSDP_NDMAX] = {0.0, 0.0};   // <M^T dy (sparse part), u u^T> per dense row
   {
+    // the slot tables are read-only for the kernel's lifetime (__ldg: the
+    // loads may move ahead of the stores below); y+ / dy come from other
+    // CTAs of the cluster (coherent L2 loads)
     const int e0 = d.zptr[x.r0], e1 = d.zptr[x.r1];
+    double* zsm = s.zstaged ? (double*)s.zvs - s.zoff : nullptr;   // Z_k is dead: keep Z_k+1 here too
     for (int e = e0 + tid; e < e1; e += blockDim.x) {
-      double z = d.cval[e], a = 0.0;
-      for (int t = d.tptr[e]; t < d.tptr[e + 1]; ++t) {
-        const int row = d.trow[t];
-        const double cf = d.tcoef[t];
-        z = fma(yn[row], cf, z);
-        a = fma(d.dy[row], cf, a);
+      double z = __ldg(d.cval + e), a = 0.0;
+      const int t0 = __ldg(d.tptr + e), t1 = __ldg(d.tptr + e + 1);
+      for (int t = t0; t < t1; ++t) {
+        const int row = __ldg(d.trow + t);
+        const double cf = __ldg(d.tcoef + t);
+        z = fma(__ldcg(yn + row), cf, z);
+        a = fma(__ldcg(d.dy + row), cf, a);
       }
       zvn[e] = z;
-      const int i = d.zrow[e], j = d.zcol[e];
+      if (zsm) zsm[e] = z;
+      const int i = __ldg(d.zrow + e), j = __ldg(d.zcol + e);
       if (j >= i) {
         const double w = (i == j) ? 1.0 : 2.0;
         corr = fma(w * a, a, corr);
@@ -1729,13 +1735,19 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       }
     }
   }
+  prof_tick(pf, 80);
   __syncthreads();
+  prof_tick(pf, 81);
   double gmax = 0.0;
-  for (int rho = x.r0 + tid; rho < x.r1; rho += blockDim.x) {
-    double sacc = 0.0;
-    for (int e = d.zptr[rho]; e < d.zptr[rho + 1]; ++e) sacc += fabs(zvn[e]);
-    gmax = fmax(gmax, sacc);
+  {
+    const double* zsrc = s.zstaged ? (const double*)s.zvs - s.zoff : zvn;
+    for (int rho = x.r0 + tid; rho < x.r1; rho += blockDim.x) {
+      double sacc = 0.0;
+      for (int e = __ldg(d.zptr + rho); e < __ldg(d.zptr + rho + 1); ++e) sacc += fabs(zsrc[e]);
+      gmax = fmax(gmax, sacc);
+    }
   }
+  prof_tick(pf, 82);
   {
     double v = warp_sum(corr);
     double g = gmax;

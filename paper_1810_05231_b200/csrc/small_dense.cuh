@@ -515,6 +515,67 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return r;
 }
 
+// Same contract and arithmetic as chol_scaled_1s, with a fixed thread map:
+// thread (i, p) owns row i and the columns k = j+1+p, j+1+p+P, ... of each
+// step j (P = blockDim / b parts per row): no per-element index division and
+// one barrier per step.
+__device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < b; i += nt) {
+    const double g = G[i * lds + i];
+    dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    G[i * lds + j] = (j <= i) ? G[i * lds + j] * dsc[i] * dsc[j] : 0.0;
+  }
+  __syncthreads();
+  const int P = max(1, nt / b);
+  const int ri = tid / P, pp = tid - ri * P;
+  for (int j = 0; j < b; ++j) {
+    const double djj = G[j * lds + j];
+    if (!(djj > 1e-28)) { __syncthreads(); return false; }
+    if (ri < b && ri > j) {
+      const double gij = G[ri * lds + j] * fast_rcp(djj);
+      double* Gi = G + ri * lds;
+      for (int k = j + 1 + pp; k <= ri; k += P) Gi[k] = fma(-gij, G[k * lds + j], Gi[k]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e % b;
+    if (j < i) G[i * lds + j] = G[i * lds + j] / sqrt(G[j * lds + j]);
+  }
+  __syncthreads();
+  for (int j = tid; j < b; j += nt) G[j * lds + j] = sqrt(G[j * lds + j]);
+  __syncthreads();
+  return true;
+}
+
+// X = L^{-1} (lower) as tri_inv_lower_1s, with the fixed (row, part) thread map.
+__device__ void tri_inv_lower_rows(const double* L, double* X, int b, int lds) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < b * b; e += nt) X[(e / b) * lds + (e % b)] = (e / b == e % b) ? 1.0 : 0.0;
+  __syncthreads();
+  const int P = max(1, nt / b);
+  const int ri = tid / P, pp = tid - ri * P;
+  for (int kk = 0; kk < b - 1; ++kk) {
+    if (ri < b && ri > kk) {
+      const double f = L[ri * lds + kk] * fast_rcp(L[kk * lds + kk]);
+      double* Xi = X + ri * lds;
+      const double* Xk = X + kk * lds;
+      for (int c = pp; c <= kk; c += P) Xi[c] = fma(-f, Xk[c], Xi[c]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, c = e % b;
+    X[i * lds + c] = (c <= i) ? X[i * lds + c] / L[i * lds + i] : 0.0;
+  }
+  __syncthreads();
+}
+
 // Two-barrier-per-round cyclic Jacobi: (1) one thread per pair forms the
 // rotation from a precomputed pairing table, (2) every thread forms its
 // elements of J^T A J and Q J in one pass into ping-pong buffers.  The

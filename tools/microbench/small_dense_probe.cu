@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(512, 1) probe(const double* Gin, const double*
   int* tab = (int*)(theta + 64);
   int* perm = tab + 64 * 64;
   int* flag = perm + 64;
-  long long t_chol = 0, t_tri = 0, t_jac = 0, t_sort = 0, t_gemm = 0, t_j4 = 0;
+  long long t_chol = 0, t_tri = 0, t_jac = 0, t_sort = 0, t_gemm = 0, t_j4 = 0, t_cr = 0, t_tr = 0;
   int sweeps = 0, sweeps4 = 0;
   for (int rep = 0; rep < reps; ++rep) {
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[(e / b) * lds + e % b] = Gin[e];
@@ -36,6 +36,18 @@ __global__ void __launch_bounds__(512, 1) probe(const double* Gin, const double*
     long long t2 = clock64();
     sm_gemm(L, lds, A, lds, M, lds, b, b, b);
     long long t3 = clock64();
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) { out[300 + e % 64] = 0; }
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) Q[(e / b) * lds + e % b] = Gin[e];
+    __syncthreads();
+    long long t9 = clock64();
+    chol_scaled_rows(Q, b, lds, dsc);
+    long long t10 = clock64();
+    tri_inv_lower_rows(Q, T, b, lds);
+    long long t11 = clock64();
+    double md = 0.0;
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) md = fmax(md, fabs(T[(e / b) * lds + e % b] - L[(e / b) * lds + e % b]));
+    if (md > 1e-12) out[1] = md;
+    t_cr += t10 - t9; t_tr += t11 - t10;
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[(e / b) * lds + e % b] = Hin[e];
     __syncthreads();
     long long t4 = clock64();
@@ -62,7 +74,7 @@ __global__ void __launch_bounds__(512, 1) probe(const double* Gin, const double*
   }
   if (threadIdx.x == 0) {
     cyc[0] = t_chol / reps; cyc[1] = t_tri / reps; cyc[2] = t_gemm / reps; cyc[3] = t_jac / reps;
-    cyc[4] = t_sort / reps; cyc[5] = sweeps; cyc[6] = t_j4 / reps; cyc[7] = sweeps4;
+    cyc[4] = t_sort / reps; cyc[5] = sweeps; cyc[6] = t_j4 / reps; cyc[7] = sweeps4; cyc[8] = t_cr / reps; cyc[9] = t_tr / reps;
   }
 }
 
@@ -88,11 +100,13 @@ int main() {
       cudaMemcpy(H, h.data(), b * b * 8, cudaMemcpyHostToDevice);
       probe<<<1, 512, smem>>>(G, H, b, reps, cyc, out);
       cudaError_t e = cudaDeviceSynchronize();
-      long long c[8]; cudaMemcpy(c, cyc, 8 * 8, cudaMemcpyDeviceToHost);
+      long long c[10]; cudaMemcpy(c, cyc, 10 * 8, cudaMemcpyDeviceToHost);
+      double o1; cudaMemcpy(&o1, out + 1, 8, cudaMemcpyDeviceToHost);
       double dv[64]; cudaMemcpy(dv, out + 200, 64 * 8, cudaMemcpyDeviceToHost);
       double mx = 0; for (int i = 0; i < b; ++i) mx = fmax(mx, fabs(dv[i]));
       printf("b=%2d off=%.0e: chol %6lld  tri_inv %6lld  gemm %6lld  jacobi %7lld (%.2f sweeps, %5.0f cyc/sweep)  sort %5lld  [%s]\n",
              b, off, c[0], c[1], c[2], c[3], c[5] / (double)reps, c[3] / (c[5] / (double)reps), c[4], cudaGetErrorString(e));
+      printf("        chol_rows %6lld  tri_inv_rows %6lld  (max |L^-1 diff| flag %.1e)\n", c[8], c[9], o1);
       printf("        jacobi_eig4 %7lld (%.2f sweeps, %5.0f cyc/sweep)  max |dtheta| vs eig3 %.2e\n", c[6], c[7] / (double)reps,
              c[6] / (c[7] / (double)reps), mx);
     }
