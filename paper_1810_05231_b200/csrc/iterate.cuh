@@ -1002,8 +1002,8 @@ __device__ int choose_block(int k, int n) {
 
 __global__ void __launch_bounds__(PDSDP_NTHR, 1)
 lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,
-                      const int* __restrict__ active, int step, int lcap, int zcap, int ycap, int owncap,
-                      int nlmax) {
+                      const int* __restrict__ active, int step0, int nsteps, int lcap, int zcap, int ycap,
+                      int owncap, int nlmax) {
   const int lds = lcap + 1;   // odd stride of the b x b workspaces (no bank conflicts)
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -1022,8 +1022,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   }
   __syncthreads();
   const Inst& d = d_sm;
-  if (*(volatile int*)d.stopf) return;            // an earlier step of this chunk ended it
-  const Ctl ctl = ctls[inst_id * PDSDP_KMAX + step];
+  if (*(volatile int*)d.stopf) return;            // an earlier launch of this chunk ended it
+  const int flags0 = ctls[inst_id * PDSDP_KMAX + step0].flags;
   State* st = d.st;
   const int n = d.n, ld = d.ld, tid = threadIdx.x;
   x.r0 = (int)(((long long)n * x.c) / x.C);
@@ -1037,9 +1037,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
     pf.ntr = 0;
     pf.cap = PDSDP_TRACE_CAP;
-    pf.trace = ((ctl.flags & 32) && x.c == 0) ? d.st->hdump : nullptr;
-    if (ctl.flags & 64) { pf.trace = d.trace + (size_t)x.c * 2 * PDSDP_TRACE_CTA; pf.cap = PDSDP_TRACE_CTA - 1; }
+    pf.trace = ((flags0 & 32) && x.c == 0) ? d.st->hdump : nullptr;
+    if (flags0 & 64) { pf.trace = d.trace + (size_t)x.c * 2 * PDSDP_TRACE_CTA; pf.cap = PDSDP_TRACE_CTA - 1; }
   }
+  prof_tick(pf, 29);
   __shared__ Sm s_sm;
   Sm& s = s_sm;
   if (threadIdx.x == 0) {
@@ -1086,6 +1087,14 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   auto buf = [&](int i) -> double* {
     return i == 0 ? d.V : i == 1 ? d.AV : i == 2 ? d.Y0 : i == 3 ? d.Y1 : d.Y2;
   };
+  const int own_base = s.own;
+
+  // Persistent over the chunk: one launch runs the chunk's iterations until
+  // the host's control logic may act (the stop flag set by CTA 0 at the end
+  // of an iteration); iterations are separated by one cluster barrier, which
+  // publishes the iterate to every CTA of the cluster.
+  for (int step = step0; step < step0 + nsteps; ++step) {
+  const Ctl ctl = ctls[inst_id * PDSDP_KMAX + step];
 
   // ---------------- prologue: F <- V[:, :rF] (X_k), block setup ----------------
   // flags: bit0 cold start; bit1 the certificate eigenvalue lambda_{r+1} must be
@@ -1133,7 +1142,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     s.res[i] = (!cold && i < b_old) ? st->res[i] : 1.0e300;
   }
-  if (tid == 0 && s.own && rF + d.nd > s.sld) s.own = 0;
+  if (tid == 0) s.own = (own_base && rF + d.nd <= s.sld) ? 1 : 0;
   __syncthreads();
   const int rFx = rF + d.nd;       // factor columns of the operator S = F_x diag(lamF) F_x^T - alpha Z
   const double lo = st->lo_par[ctl.ypar & 1];
@@ -1168,6 +1177,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   if (x.c == 0 && tid < PDSDP_BMAX) st->lamF[tid] = s.lamF[tid];
   if (x.c == 0 && tid == 0) st->rF_used = rF;
   int grow_err = 0, since_grow = 0;
+  prof_tick(pf, 30);
 
   // ---------------- eigensolver: warm-started Chebyshev-filtered subspace iteration ----
   bool av_valid = false;
@@ -1855,6 +1865,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       if (grow_err || fin_tot != 1.0 || ec <= ctl.conv_thr || ec >= ctl.stall_thr) *d.stopf = 1;
     }
   }
+  // publish the iterate (and the stop flag) to the whole cluster
+  cg::this_cluster().sync();
+  if (*(volatile int*)d.stopf) break;
+  }   // step loop
 }
 
 }  // namespace pdsdp

@@ -452,7 +452,7 @@ int check_inst(pdsdp_batch* b, int inst) {
   return PDSDP_OK;
 }
 
-int launch_iterate(pdsdp_batch* b, int nact, int lds, int step) {
+int launch_iterate(pdsdp_batch* b, int nact, int lds, int step0, int nsteps) {
   // shared memory plan beyond the fixed workspaces, in priority order:
   // (1) the CTA's Z rows (all-or-nothing; they feed every sparse product),
   // (2) own rows of F, Y_j, Y_{j-1} (smem-resident filter recurrence),
@@ -485,7 +485,7 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds, int step) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, lrpdhg_iterate_kernel, (const Inst*)b->d_insts, (const Ctl*)b->d_ctl,
-                        (const int*)b->d_active, step, lds, zcap, ycap, owncap, nlmax));
+                        (const int*)b->d_active, step0, nsteps, lds, zcap, ycap, owncap, nlmax));
   return PDSDP_OK;
 }
 
@@ -729,18 +729,26 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
   const size_t rsm = (size_t)2 * RES_TILE * (kp + 1) * sizeof(double);
   // timing: one event before the chunk and one after every iteration launch,
   // so the span of exactly the executed iterations is known after the sync
+  // one persistent launch per chunk (the kernel loops over the steps and stops
+  // where the host must look); the verification mode interleaves the
+  // entry-wise residual kernel, so it launches step by step
   if (b->timing) CK(cudaEventRecord(b->tev[0], b->stream));
-  for (int j = 0; j < K; ++j) {
-    int rc = launch_iterate(b, nact, lds, j);
+  if (!b->verify_residual) {
+    int rc = launch_iterate(b, nact, lds, 0, K);
     if (rc) return rc;
-    if (b->verify_residual) {
+    if (b->timing) CK(cudaEventRecord(b->tev[1], b->stream));
+    b->n_launch += 1;
+  } else {
+    for (int j = 0; j < K; ++j) {
+      int rc = launch_iterate(b, nact, lds, j, 1);
+      if (rc) return rc;
       residual_kernel<<<dim3(b->max_tiles, nact), RES_THREADS, rsm, b->stream>>>(b->d_insts, b->d_ctl, b->d_active, j);
       CK(cudaGetLastError());
+      if (b->timing) CK(cudaEventRecord(b->tev[j + 1], b->stream));
     }
-    if (b->timing) CK(cudaEventRecord(b->tev[j + 1], b->stream));
+    b->n_launch += K;
   }
   CK(cudaStreamSynchronize(b->stream));
-  b->n_launch += K;
   int done_max = 0;
   for (int a = 0; a < nact; ++a) {
     int done = 0;
@@ -757,7 +765,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
   }
   if (b->timing && done_max > 0) {
     float t1 = 0.f;
-    CK(cudaEventElapsedTime(&t1, b->tev[0], b->tev[done_max]));
+    CK(cudaEventElapsedTime(&t1, b->tev[0], b->tev[b->verify_residual ? done_max : 1]));
     b->t_iter += t1; b->n_iter += done_max;
   }
   return PDSDP_OK;

@@ -22,6 +22,7 @@ for c in range(C):
 n = min(len(e) for e in evs)
 print(f"r={r} C={C} events per CTA {[len(e) for e in evs]} passes {o[4]:.0f} matvecs {o[5]:.0f}")
 labels = evs[0][:, 0]
+print("first events (label, us from CTA start):", [(int(l), round((c - evs[0][0, 1]) / 1965.0, 2)) for l, c in evs[0][:4]])
 same = all(np.array_equal(e[:n, 0], labels[:n]) for e in evs)
 print("identical label sequences:", same)
 tot = np.array([(e[n - 1, 1] - e[0, 1]) / 1965.0 for e in evs])
