@@ -1088,6 +1088,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     return i == 0 ? d.V : i == 1 ? d.AV : i == 2 ? d.Y0 : i == 3 ? d.Y1 : d.Y2;
   };
   const int own_base = s.own;
+  // launch invariants: Z column indices of the own rows, row pointers, groups
+  if (s.zstaged) {
+    const int nzl = d.zptr[x.r1] - s.zoff;
+    for (int e = tid; e < nzl; e += blockDim.x) ((int*)s.zc)[e] = d.zcol[s.zoff + e];
+  }
+  if (own_base) {
+    for (int lr = tid; lr <= x.r1 - x.r0; lr += blockDim.x) s.szp[lr] = d.zptr[x.r0 + lr];
+    for (int c = tid; c <= x.C; c += blockDim.x) s.gb[c] = (int)(((long long)n * c) / x.C);
+  }
+  __syncthreads();
 
   // Persistent over the chunk: one launch runs the chunk's iterations until
   // the host's control logic may act (the stop flag set by CTA 0 at the end
@@ -1149,16 +1159,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   const double alpha = d.alpha;
   const double* zv = (ctl.ypar & 1) ? d.zbuf1 : d.zbuf0;     // Z_k  = C + M^T y_k
   double* zvn = (ctl.ypar & 1) ? d.zbuf0 : d.zbuf1;          // Z_k+1
-  if (s.zstaged) {
+  // Z_k values of the own rows: the previous iteration of this launch left
+  // them in shared memory (its adjoint gather), otherwise stage them
+  if (s.zstaged && (step == step0 || rerun)) {
     const int nzl = d.zptr[x.r1] - s.zoff;
-    for (int e = tid; e < nzl; e += blockDim.x) {
-      ((int*)s.zc)[e] = d.zcol[s.zoff + e];
-      ((double*)s.zvs)[e] = zv[s.zoff + e];
-    }
-  }
-  if (s.own) {
-    for (int lr = tid; lr <= x.r1 - x.r0; lr += blockDim.x) s.szp[lr] = d.zptr[x.r0 + lr];
-    for (int c = tid; c <= x.C; c += blockDim.x) s.gb[c] = (int)(((long long)n * c) / x.C);
+    for (int e = tid; e < nzl; e += blockDim.x) ((double*)s.zvs)[e] = zv[s.zoff + e];
   }
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
     const int rho = x.r0 + it / b, j = it % b;
