@@ -27,7 +27,9 @@ namespace pdsdp {
 #define PDSDP_TOL_X 1e-12      // admissible per-iteration error of X+ (relative to ||X+||_F)
 #define PDSDP_TOL_CERT 1e-8
 #define PDSDP_TOL_CLIP 1e-6
-#define PDSDP_MMAX 24
+#ifndef PDSDP_MMAX
+#define PDSDP_MMAX 48          // largest filter degree per pass (slow clustered columns after a rank doubling)
+#endif
 // largest amplification of a column's contamination the filter may cause:
 // CholQR2 re-orthonormalises blocks with condition up to ~1e8, so 1e6 keeps
 // a 100x margin (was 1e4)
