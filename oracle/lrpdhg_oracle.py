@@ -270,3 +270,58 @@ def solve_lr(prob, cfg, record_at=(), progress=None, alpha=None, stop_after=None
         checkpoints=checkpoints, residual_scale=scale, snapshots=snaps,
         history=hist, wall_time_s=time.perf_counter() - t0,
     )
+
+
+# ----------------------------------------------------------------------------
+# Exact PD-SDP driver (pdhg.py:221-288) and the solution report
+# (problem.py:213-240) -- checkers for SURVEY.md 8(f) rows 1 and 2.
+
+def solve_pd(prob, cfg, alpha=None):
+    """``pdhg.solve_pd_sdp``: X+ = proj_psd(X - alpha (M^T y + C)) with the
+    full eigendecomposition, the same dual step and residuals, relative stop."""
+    cfg.validate()
+    t0 = time.perf_counter()
+    n = prob.n
+    M = stacked_csr(prob)
+    C = prob.C.data
+    if alpha is None:
+        alpha = cfg.alpha_override if cfg.alpha_override is not None else \
+            cfg.alpha_safety / op_norm(M, cfg.seed)
+    X = np.zeros(n * (n + 1) // 2)
+    y = np.zeros(prob.m + prob.p)
+    status, res, scale, k_done = None, (math.nan,) * 3, 1.0, 0
+    for k in range(1, cfg.max_iter + 1):
+        Xn = proj_psd(X - alpha * (M.T @ y + C), n)           # pdhg.py:166-174
+        yn = dual_update(M, y, Xn, X, alpha, prob.b, prob.h)
+        if not (np.all(np.isfinite(Xn)) and np.all(np.isfinite(yn))):
+            status = "diverged"
+            break
+        res = fixed_point_residuals(M, Xn, X, yn, y, alpha)
+        X, y, k_done = Xn, yn, k
+        if k == 1 and cfg.relative_residuals:
+            scale = 1.0 + res[2]
+        if res[2] <= cfg.eps_tol * scale:
+            status = "optimal"
+            break
+        if time.perf_counter() - t0 > cfg.time_limit_s:
+            status = "time_limit"
+            break
+    if status is None:
+        status = "max_iterations"
+    return OracleResult(status=status, X=X, y=y, iterations=k_done, final_residuals=res,
+                        primal_objective=float(C @ X),
+                        dual_objective=-float(prob.b @ y[:prob.m] + prob.h @ y[prob.m:]),
+                        residual_scale=scale)
+
+
+def check_solution(prob, Xp, y):
+    """``problem.check_solution``: (pobj, dobj, eq. violation, ineq.
+    violation, min eigenvalue, gap)."""
+    M = stacked_csr(prob)
+    mx = M @ Xp
+    eq = float(np.linalg.norm(mx[:prob.m] - prob.b))
+    ineq = float(np.linalg.norm(np.maximum(mx[prob.m:] - prob.h, 0.0)))
+    pobj = float(prob.C.data @ Xp)
+    dobj = -float(prob.b @ y[:prob.m] + prob.h @ y[prob.m:])
+    lmin = float(np.linalg.eigvalsh(unpack(Xp, prob.n)).min())
+    return np.array([pobj, dobj, eq, ineq, lmin, pobj - dobj])

@@ -10,6 +10,7 @@ from .config import (
     Checkpoint,
     ProgressInfo,
     RankController,
+    SolutionReport,
     SolveResult,
     SolveStatus,
     SolverConfig,
@@ -20,12 +21,20 @@ from .config import (
 from .layout import EigenDecomposition, SymMatrix, approx_error_bound, packed_index, packed_length, smat, svec
 from .model import SdpProblem, SparseRow
 from .operators import apply_M, apply_M_adjoint, aproj_psd
-from .solver import estimate_operator_norm, solve_lr_pd_sdp, solve_lr_pd_sdp_batch, step_size
+from .solver import (
+    check_solution,
+    estimate_operator_norm,
+    solve_lr_pd_sdp,
+    solve_lr_pd_sdp_batch,
+    solve_pd_sdp,
+    step_size,
+)
 
 __all__ = [
     "Checkpoint", "EigenDecomposition", "ProgressInfo", "RankController", "SdpProblem",
     "SolveResult", "SolveStatus", "SolverConfig", "SparseRow", "SymMatrix", "apply_M",
     "apply_M_adjoint", "aproj_psd", "approx_error_bound", "estimate_operator_norm",
+    "SolutionReport", "check_solution", "solve_pd_sdp",
     "packed_index", "packed_length", "rank_certificate_satisfied", "smat", "solve_lr_pd_sdp", "solve_lr_pd_sdp_batch",
     "stall_detected", "step_size", "svec", "update_rank",
 ]

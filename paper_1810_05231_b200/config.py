@@ -102,6 +102,22 @@ class SolveResult:
 
 
 @dataclass
+class SolutionReport:
+    """Feasibility and optimality summary of a primal-dual pair (reference
+    ``problem.py:186-210``)."""
+
+    primal_objective: float
+    dual_objective: float
+    equality_violation: float
+    inequality_violation: float
+    min_eigenvalue: float
+    duality_gap: float
+
+    def max_violation(self) -> float:
+        return max(self.equality_violation, self.inequality_violation, -min(self.min_eigenvalue, 0.0))
+
+
+@dataclass
 class Checkpoint:
     """Feasible pair saved on inner convergence (reference ``lowrank.py:39-47``)."""
 

@@ -20,6 +20,7 @@ import numpy as np
 
 from .config import (
     DEFAULT_EPS_LAMBDA_PER_N,
+    SolutionReport,
     Checkpoint,
     ProgressCallback,
     ProgressInfo,
@@ -359,3 +360,110 @@ def solve_lr_pd_sdp_batch(problems, config: SolverConfig | None = None) -> list:
     results = [_result(p, config, o, a, t0) for p, o, a in zip(problems, outs, alphas)]
     batch.close()
     return results
+
+
+# ---------------------------------------------------------------------------
+# Exact PD-SDP (reference pdhg.py:221-288) with the full PSD projection
+# (symmat.py:223-226).  On the device the full projection is the eigen block
+# covering all of R^n (r = n: the Rayleigh-Ritz step is then the complete
+# eigendecomposition), so it is available for n <= PDSDP_BLOCK_MAX; larger n
+# need a full dense eigensolver (not built).
+EXACT_N_MAX = 64
+
+
+def solve_pd_sdp(
+    prob: SdpProblem,
+    config: SolverConfig | None = None,
+    callback: ProgressCallback | None = None,
+) -> SolveResult:
+    """Exact primal-dual iteration from a zero start (reference
+    ``pdhg.py:221-288``): X+ = proj_psd(X - alpha (M^T y + C)), the dual step
+    and residuals as in the LR solver, stop on the (relative) combined
+    residual, no rank control (``rank_path = [(0, n)]``)."""
+    config = config or SolverConfig()
+    config.validate()
+    n = prob.n
+    if n > EXACT_N_MAX:
+        raise ValueError(f"exact projection on the device supports n <= {EXACT_N_MAX} (n={n}); "
+                         "use solve_lr_pd_sdp")
+    t0 = time.perf_counter()
+    alpha = step_size(prob, config)
+    batch = _device_batch(prob)
+    batch.set_alpha(0, alpha)
+    batch.reset(0, 0.0)
+    it = _DeviceIterate(batch, 0)
+    status, res, scale, k = None, (math.nan, math.nan, math.nan), 1.0, 1
+    while status is None and k <= config.max_iter:
+        K = 1 if k == 1 else min(KMAX, config.max_iter - k + 1)
+        if callback is not None and k > 1:
+            K = min(K, config.progress_every - (k - 1) % config.progress_every)
+        conv = config.eps_tol * scale if k > 1 else -1.0
+        outs, done = batch.iterate_many([0], [n], [it.ypar], K, [conv], np.full(K, np.inf))
+        for j in range(int(done[0])):
+            out = outs[0][j]
+            if out[OUT_FINITE] != 1.0:                   # pdhg.py:251-253
+                status = SolveStatus.DIVERGED
+                it.which = 1
+                break
+            it.k = k
+            it.ypar ^= 1
+            it.which = 0
+            ep, ed = float(out[OUT_EPS_P]), float(out[OUT_EPS_D])
+            res = (ep, ed, ep + ed)
+            if k == 1 and config.relative_residuals:
+                scale = 1.0 + res[2]
+            if callback is not None and k % config.progress_every == 0:
+                callback(ProgressInfo(k, *res, n, it.objective()))
+            k += 1
+            if res[2] <= config.eps_tol * scale:
+                status = SolveStatus.OPTIMAL
+                break
+        if status is None and time.perf_counter() - t0 > config.time_limit_s:
+            status = SolveStatus.TIME_LIMIT
+    if status is None:
+        status = SolveStatus.MAX_ITERATIONS
+    X, y = it.X(), it.y()
+    pobj = prob.C.inner(X)
+    dobj = -float(prob.b @ y[: prob.m] + prob.h @ y[prob.m:])
+    return SolveResult(status=status, X=X, y=y, primal_objective=pobj, dual_objective=dobj,
+                       final_residuals=res, iterations=it.k, rank_path=[(0, n)], checkpoints=[],
+                       wall_time_s=time.perf_counter() - t0, residual_scale=scale,
+                       objective_sign=prob.objective_sign)
+
+
+def check_solution(prob: SdpProblem, X: SymMatrix, y, tol: float = 1e-3) -> SolutionReport:
+    """Objectives, constraint violations, minimum eigenvalue and duality gap
+    (reference ``problem.py:213-240``).  A(X) runs on the device; the minimum
+    eigenvalue comes from the device eigensolver instead of a dense O(n^3)
+    ``eigvalsh``: lambda_min(X) = c - lambda_max(c I - X) with c above the
+    Gershgorin bound of X, lambda_max read off the rank-1 projection."""
+    from .device import aproj_psd_packed
+    from .layout import packed_coords
+    y = np.asarray(y, dtype=float)
+    if X.n != prob.n or y.shape != (prob.m + prob.p,):
+        raise ValueError("solution dimensions do not match the problem")
+    mx = _device_batch(prob).apply_M(0, X.data)
+    eq = float(np.linalg.norm(mx[: prob.m] - prob.b))
+    ineq = float(np.linalg.norm(np.maximum(mx[prob.m:] - prob.h, 0.0)))
+    pobj = prob.C.inner(X)
+    dobj = -float(prob.b @ y[: prob.m] + prob.h @ y[prob.m:])
+    n = X.n
+    i, j = packed_coords(n, np.arange(X.data.size))
+    diag = i == j
+    dense_abs = np.where(diag, np.abs(X.data), np.abs(X.data) / math.sqrt(2.0))
+    rowsum = np.bincount(i, dense_abs, minlength=n) + np.bincount(j[~diag], dense_abs[~diag], minlength=n)
+    c = float(rowsum.max()) + 1.0
+    S = -X.data.copy()
+    S[diag] += c
+    if n == 1:
+        lam_max = float(S[0])
+    else:
+        P, _ = aproj_psd_packed(n, S, 1)
+        lam_max = float(np.sum(P[diag]))
+    min_eig = c - lam_max
+    report = SolutionReport(primal_objective=pobj, dual_objective=dobj, equality_violation=eq,
+                            inequality_violation=ineq, min_eigenvalue=min_eig, duality_gap=pobj - dobj)
+    if report.max_violation() > tol:
+        logger.debug("solution violates constraints beyond tol=%.1e (max violation %.3e)",
+                     tol, report.max_violation())
+    return report

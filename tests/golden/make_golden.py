@@ -12,6 +12,10 @@ records, for seeded inputs built with ``paper_1810_05231_b200.workloads``:
   random problems shaped like the reference's own ``conftest.random_problem``;
 * ``lr_small.npz``    — full LR-PD-SDP solves of small problems (with
   inequalities, so the box projection branch is exercised);
+* ``pd_small.npz``    — exact PD-SDP solves (``solve_pd_sdp``, full projection)
+  of small problems incl. a MIMO relaxation, iterates at K = 1, 10;
+* ``mimo.npz``        — LR-PD-SDP on MIMO relaxations (inequality-heavy);
+* ``check.npz``       — ``check_solution`` reports;
 * ``cfg1.npz``        — BASELINE config 1 (n=100 Max-Cut): iterates at
   K = 1, 10, 100 and at the stop iteration, per-iteration residual history,
   final objective / rank path / checkpoints;
@@ -261,6 +265,109 @@ def make_sketch(path, idx, Ks):
     np.savez_compressed(path, **out)
 
 
+def _well_posed(prob, rng):
+    """The reference conftest's random problem made feasible-ish (PSD
+    objective, positive right-hand sides) so that solves converge."""
+    n = prob.n
+    R = rng.standard_normal((n, n))
+    return pdsdp.SdpProblem(n=n, C=pdsdp.SymMatrix.from_dense(R @ R.T / n), A=prob.A,
+                            b=np.abs(prob.b) + 0.5, G=prob.G, h=np.abs(prob.h) + 0.5)
+
+
+def _mimo(n, sigma, seed):
+    from pdsdp.instances import gen_mimo, random_mimo_instance
+    return gen_mimo(random_mimo_instance(n, sigma, seed))
+
+
+def make_pd_small(path):
+    """Exact PD-SDP (reference pdhg.solve_pd_sdp, full projection) on small
+    problems: random with inequalities, Max-Cut shaped, MIMO (box
+    inequalities on every off-diagonal entry).  Iterates at K = 1, 10 and
+    the full solve."""
+    rng = np.random.default_rng(77)
+    out = {}
+    probs = [_well_posed(random_problem(10, 6, 4, rng, nnz=4), rng),
+             to_ref(workloads.maxcut_problem(30, 0.2, 5, signed=True)),
+             _mimo(12, 0.3, 3),
+             _well_posed(random_problem(48, 20, 8, rng, nnz=4), rng)]
+    for ci, prob in enumerate(probs):
+        pre = f"c{ci}_"
+        flatten_problem(pre, prob, out)
+        for K in (1, 10):
+            cfg = pdsdp.SolverConfig(eps_tol=1e-4, max_iter=K, time_limit_s=1e9)
+            res = pdsdp.solve_pd_sdp(prob, cfg)
+            out[pre + f"X{K}"] = res.X.data
+            out[pre + f"y{K}"] = res.y
+            out[pre + f"res{K}"] = np.array(res.final_residuals)
+        cfg = pdsdp.SolverConfig(eps_tol=1e-4, max_iter=3000, time_limit_s=1e9)
+        res = pdsdp.solve_pd_sdp(prob, cfg)
+        out[pre + "status"] = res.status.value
+        out[pre + "iters"] = res.iterations
+        out[pre + "X"] = res.X.data
+        out[pre + "y"] = res.y
+        out[pre + "pobj"] = res.primal_objective
+        out[pre + "dobj"] = res.dual_objective
+        out[pre + "res"] = np.array(res.final_residuals)
+        out[pre + "scale"] = res.residual_scale
+        print("pd", ci, prob.n, res.status, res.iterations, res.primal_objective)
+    np.savez_compressed(path, **out)
+
+
+def make_mimo(path):
+    """LR-PD-SDP on MIMO relaxations (reference instances.gen_mimo): n+1
+    diagonal pins and the box -1 <= X_ij <= 1 as 2 n (n+1) / 2 inequality
+    rows -- the inequality-heavy regime (proj_box branch of the dual step)."""
+    out = {}
+    for ci, (n, sigma, seed, K) in enumerate([(12, 0.3, 3, 400), (40, 0.5, 8, 60)]):
+        prob = _mimo(n, sigma, seed)
+        pre = f"c{ci}_"
+        flatten_problem(pre, prob, out)
+        cfg = pdsdp.SolverConfig(eps_tol=1e-4, max_iter=K, initial_rank=1, window_ell=50, time_limit_s=1e9)
+        res = pdsdp.solve_lr_pd_sdp(prob, cfg)
+        out[pre + "K"] = K
+        out[pre + "status"] = res.status.value
+        out[pre + "iters"] = res.iterations
+        out[pre + "X"] = res.X.data
+        out[pre + "y"] = res.y
+        out[pre + "pobj"] = res.primal_objective
+        out[pre + "dobj"] = res.dual_objective
+        out[pre + "res"] = np.array(res.final_residuals)
+        out[pre + "rank_path"] = np.array(res.rank_path)
+        print("mimo", n, res.status, res.iterations, res.rank_path, res.primal_objective)
+    np.savez_compressed(path, **out)
+
+
+def make_check(path):
+    """Reference problem.check_solution reports (objectives, violations,
+    min eigenvalue, gap) on solver outputs and on perturbed / indefinite X."""
+    from pdsdp.problem import check_solution
+    rng = np.random.default_rng(99)
+    out = {}
+    cases = []
+    d = np.load(os.path.join(HERE, "lr_small.npz"))
+    for ci in (1, 2, 4):
+        pre = f"c{ci}_"
+        n = int(d[pre + "n"])
+        cases.append((pre, n, d[pre + "X"], d[pre + "y"]))
+    for k, (pre, n, Xd, y) in enumerate(cases):
+        ref = RProblem
+        indptr, idx, val = d[pre + "indptr"], d[pre + "idx"], d[pre + "val"]
+        rows = [RRow(idx[indptr[i]:indptr[i + 1]], val[indptr[i]:indptr[i + 1]]) for i in range(len(indptr) - 1)]
+        m = d[pre + "b"].size
+        prob = ref(n=n, C=RSym(n, d[pre + "C"]), A=rows[:m], b=d[pre + "b"], G=rows[m:], h=d[pre + "h"])
+        R = rng.standard_normal((n, n))
+        Xs = [Xd, Xd + pdsdp.SymMatrix.from_dense(0.3 * (R + R.T)).data]
+        for j, X in enumerate(Xs):
+            rep = check_solution(prob, RSym(n, X.copy()), y)
+            q = f"k{k}_{j}_"
+            flatten_problem(q, prob, out)
+            out[q + "X"] = X
+            out[q + "yv"] = y
+            out[q + "report"] = np.array([rep.primal_objective, rep.dual_objective, rep.equality_violation,
+                                          rep.inequality_violation, rep.min_eigenvalue, rep.duality_gap])
+    np.savez_compressed(path, **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -270,6 +377,9 @@ if __name__ == "__main__":
         "ops_small": lambda: make_ops_small(os.path.join(HERE, "ops_small.npz")),
         "lr_small": lambda: make_lr_small(os.path.join(HERE, "lr_small.npz")),
         "cfg1": lambda: make_cfg1(os.path.join(HERE, "cfg1.npz")),
+        "pd_small": lambda: make_pd_small(os.path.join(HERE, "pd_small.npz")),
+        "mimo": lambda: make_mimo(os.path.join(HERE, "mimo.npz")),
+        "check": lambda: make_check(os.path.join(HERE, "check.npz")),
     }
     if a.big:
         jobs["cfg2"] = lambda: make_sketch(os.path.join(HERE, "cfg2_sketch.npz"), 1, (1, 5))

@@ -327,3 +327,75 @@ def test_dense_residual_factored_matches_entrywise(ci, K, r):
         checked += 1
     b.close()
     assert checked == K
+
+
+# ------------------------------------------------ exact PD-SDP
+
+@pytest.mark.parametrize("ci", range(4))
+def test_exact_pd_sdp_matches_reference(ci):
+    """solve_pd_sdp (reference pdhg.py:221-288, full projection) against the
+    reference's own solves: iterates at K = 1, 10 and the full run (status,
+    iteration count, iterates, objectives)."""
+    d = load_golden("pd_small.npz")
+    pre = f"c{ci}_"
+    prob = problem_from_golden(d, pre)
+    for K in (1, 10):
+        res = pk.solve_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=K, time_limit_s=1e9))
+        assert res.iterations == K
+        # an iterate that is zero up to rounding (the MIMO objective is PSD, so
+        # proj_psd(-alpha C) = 0; LAPACK leaves ~1e-16 eigenvalues, the device
+        # clips them) is compared absolutely against the floor
+        assert rel(res.X.data, d[pre + f"X{K}"], floor=1e-6) <= ITER_TOL
+        assert rel(res.y, d[pre + f"y{K}"]) <= ITER_TOL
+        np.testing.assert_allclose(res.final_residuals, d[pre + f"res{K}"], rtol=1e-7, atol=1e-12)
+    res = pk.solve_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=3000, time_limit_s=1e9))
+    assert res.status.value == str(d[pre + "status"])
+    assert res.iterations == int(d[pre + "iters"])
+    assert res.rank_path == [(0, prob.n)] and res.checkpoints == []
+    assert rel(res.X.data, d[pre + "X"]) <= ITER_TOL
+    assert rel(res.y, d[pre + "y"]) <= ITER_TOL
+    assert res.primal_objective == pytest.approx(float(d[pre + "pobj"]), rel=OBJ_TOL, abs=1e-9)
+    assert res.dual_objective == pytest.approx(float(d[pre + "dobj"]), rel=OBJ_TOL, abs=1e-9)
+
+
+# ------------------------------------ inequality-heavy MIMO (SURVEY 8(f) 3)
+
+@pytest.mark.parametrize("ci", range(2))
+def test_mimo_lr_matches_reference(ci):
+    """LR-PD-SDP on the reference's MIMO relaxation (instances.gen_mimo: n+1
+    pins and 2 per off-diagonal box inequality rows, i.e. the proj_box branch
+    of the dual step on n(n+1) rows)."""
+    d = load_golden("mimo.npz")
+    pre = f"c{ci}_"
+    prob = problem_from_golden(d, pre)
+    K = int(d[pre + "K"])
+    res = pk.solve_lr_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=K, initial_rank=1, window_ell=50,
+                                                time_limit_s=1e9))
+    assert res.status.value == str(d[pre + "status"])
+    assert res.iterations == int(d[pre + "iters"])
+    assert [tuple(x) for x in res.rank_path] == [tuple(x) for x in d[pre + "rank_path"].tolist()]
+    assert rel(res.X.data, d[pre + "X"]) <= ITER_TOL
+    assert rel(res.y, d[pre + "y"]) <= ITER_TOL
+    assert res.primal_objective == pytest.approx(float(d[pre + "pobj"]), rel=OBJ_TOL)
+
+
+# --------------------------------------- check_solution (SURVEY 8(f) 2)
+
+def test_check_solution_matches_reference():
+    """check_solution (reference problem.py:213-240) with A(X) and the
+    minimum eigenvalue on the device, against the reference's reports."""
+    d = load_golden("check.npz")
+    keys = sorted({k.split("_")[0] + "_" + k.split("_")[1] for k in d.files if k.startswith("k")})
+    assert keys
+    for q in keys:
+        q = q + "_"
+        prob = problem_from_golden(d, q)
+        rep = pk.check_solution(prob, pk.SymMatrix(prob.n, d[q + "X"]), d[q + "yv"])
+        ref = d[q + "report"]
+        got = np.array([rep.primal_objective, rep.dual_objective, rep.equality_violation,
+                        rep.inequality_violation, rep.min_eigenvalue, rep.duality_gap])
+        scale = max(1.0, float(np.abs(d[q + "X"]).max()))
+        np.testing.assert_allclose(got[[0, 1, 5]], ref[[0, 1, 5]], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(got[[2, 3]], ref[[2, 3]], rtol=1e-10, atol=1e-12)
+        assert abs(got[4] - ref[4]) <= 1e-8 * scale, (q, got[4], ref[4])
+        assert rep.max_violation() == pytest.approx(max(ref[2], ref[3], -min(ref[4], 0.0)), rel=1e-6, abs=1e-8 * scale)

@@ -86,3 +86,39 @@ def test_config1_matches_reference():
     assert res.primal_objective == pytest.approx(float(d["pobj"]), rel=1e-10)
     hist = np.array(res.history)
     np.testing.assert_allclose(hist[:, 2], d["history"][:, 3], rtol=1e-7)
+
+
+@pytest.mark.parametrize("ci", range(4))
+def test_exact_pd_oracle_matches_reference(ci):
+    d = load_golden("pd_small.npz")
+    pre = f"c{ci}_"
+    prob = problem_from_golden(d, pre)
+    for K in (1, 10):
+        r = orc.solve_pd(prob, SolverConfig(eps_tol=1e-4, max_iter=K, time_limit_s=1e9))
+        assert np.linalg.norm(r.X - d[pre + f"X{K}"]) <= 1e-10 * max(1.0, np.linalg.norm(d[pre + f"X{K}"]))
+        assert np.linalg.norm(r.y - d[pre + f"y{K}"]) <= 1e-10 * max(1.0, np.linalg.norm(d[pre + f"y{K}"]))
+    if prob.n <= 30:    # the full runs of the small cases (the n = 48 case runs 3000 iterations)
+        r = orc.solve_pd(prob, SolverConfig(eps_tol=1e-4, max_iter=3000, time_limit_s=1e9))
+        assert r.status == str(d[pre + "status"]) and r.iterations == int(d[pre + "iters"])
+        assert r.primal_objective == pytest.approx(float(d[pre + "pobj"]), rel=1e-9, abs=1e-12)
+
+
+def test_mimo_oracle_matches_reference():
+    d = load_golden("mimo.npz")
+    pre = "c0_"
+    prob = problem_from_golden(d, pre)
+    K = int(d[pre + "K"])
+    r = orc.solve_lr(prob, SolverConfig(eps_tol=1e-4, max_iter=K, initial_rank=1, window_ell=50,
+                                        time_limit_s=1e9))
+    assert r.status == str(d[pre + "status"]) and r.iterations == int(d[pre + "iters"])
+    assert [tuple(x) for x in r.rank_path] == [tuple(x) for x in d[pre + "rank_path"].tolist()]
+    assert np.linalg.norm(r.X - d[pre + "X"]) <= 1e-8 * np.linalg.norm(d[pre + "X"])
+
+
+def test_check_solution_oracle_matches_reference():
+    d = load_golden("check.npz")
+    keys = sorted({"_".join(k.split("_")[:2]) + "_" for k in d.files if k.startswith("k")})
+    for q in keys:
+        prob = problem_from_golden(d, q)
+        got = orc.check_solution(prob, d[q + "X"], d[q + "yv"])
+        np.testing.assert_allclose(got, d[q + "report"], rtol=1e-10, atol=1e-12)
