@@ -18,6 +18,16 @@ from .config import (
     stall_detected,
     update_rank,
 )
+from .io import (
+    ParseError,
+    load_problem,
+    parse_extended,
+    parse_sdpa,
+    read_solution,
+    write_extended,
+    write_sdpa,
+    write_solution,
+)
 from .layout import EigenDecomposition, SymMatrix, approx_error_bound, packed_index, packed_length, smat, svec
 from .model import SdpProblem, SparseRow
 from .operators import apply_M, apply_M_adjoint, aproj_psd
@@ -35,6 +45,8 @@ __all__ = [
     "SolveResult", "SolveStatus", "SolverConfig", "SparseRow", "SymMatrix", "apply_M",
     "apply_M_adjoint", "aproj_psd", "approx_error_bound", "estimate_operator_norm",
     "SolutionReport", "check_solution", "solve_pd_sdp",
+    "ParseError", "load_problem", "parse_extended", "parse_sdpa", "read_solution", "write_extended",
+    "write_sdpa", "write_solution",
     "packed_index", "packed_length", "rank_certificate_satisfied", "smat", "solve_lr_pd_sdp", "solve_lr_pd_sdp_batch",
     "stall_detected", "step_size", "svec", "update_rank",
 ]

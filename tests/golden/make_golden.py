@@ -16,6 +16,8 @@ records, for seeded inputs built with ``paper_1810_05231_b200.workloads``:
   of small problems incl. a MIMO relaxation, iterates at K = 1, 10;
 * ``mimo.npz``        — LR-PD-SDP on MIMO relaxations (inequality-heavy);
 * ``check.npz``       — ``check_solution`` reports;
+* ``io.npz``          — SDPA / extended-JSON parses and rewrites, parse errors,
+  a solution document (reference ``io.py``);
 * ``cfg1.npz``        — BASELINE config 1 (n=100 Max-Cut): iterates at
   K = 1, 10, 100 and at the stop iteration, per-iteration residual history,
   final objective / rank path / checkpoints;
@@ -368,6 +370,77 @@ def make_check(path):
     np.savez_compressed(path, **out)
 
 
+SDPA_MULTIBLOCK = """* a two-block document: comments, braces, a diagonal block, a duplicate
+"hand written"
+3 =mdim
+2 =nblocks
+{3, -2}
+{1.0, 2.5, -1.0}
+0 1 1 1 2.0
+0 1 1 3 -0.5
+0 2 1 1 1.5
+1 1 1 1 1.0
+1 1 2 3 0.25
+1 1 2 3 0.25
+2 1 3 3 1.0
+2 2 2 2 -2.0
+3 1 1 2 1.0
+3 2 1 1 4.0
+"""
+
+SDPA_BAD = [
+    "1\n1\n2\n1.0\n0 1 2 1 1.0\n",            # lower triangle
+    "1\n1\n2\n1.0\n0 1 1 3 1.0\n",            # outside the block
+    "1\n1\n-2\n1.0\n0 1 1 2 1.0\n",           # off-diagonal in a diagonal block
+    "1\n1\n2\n1.0\n0 1 1 1\n",                # 4 fields
+    "1\n1\n2\nx\n0 1 1 1 1.0\n",              # non-numeric c
+    "2\n1\n2\n1.0\n0 1 1 1 1.0\n",            # short c vector (takes an entry line)
+    "1\n0\n2\n1.0\n0 1 1 1 1.0\n",            # zero blocks
+    "1\n1\n2\n1.0\n3 1 1 1 1.0\n",            # matrix index out of range
+    "1\n1\n2\n",                                  # too short
+]
+
+
+def make_io(path):
+    """Reference io.py on SDPA / extended / solution documents."""
+    from pdsdp import io as rio
+    from pdsdp.problem import check_solution
+    out = {}
+    docs = {"cfg1": rio.write_sdpa(to_ref(workloads.config(0)[0])), "multi": SDPA_MULTIBLOCK}
+    for name, text in docs.items():
+        prob = rio.parse_sdpa(text)
+        out[f"sdpa_{name}_text"] = np.array(text)
+        flatten_problem(f"sdpa_{name}_", prob, out)
+        out[f"sdpa_{name}_sign"] = prob.objective_sign
+        out[f"sdpa_{name}_rewrite"] = np.array(rio.write_sdpa(prob))
+    msgs = []
+    for text in SDPA_BAD:
+        try:
+            rio.parse_sdpa(text)
+            msgs.append("")
+        except rio.ParseError as exc:
+            msgs.append(str(exc))
+    out["sdpa_bad_text"] = np.array(SDPA_BAD)
+    out["sdpa_bad_msg"] = np.array(msgs)
+    d = np.load(os.path.join(HERE, "lr_small.npz"))
+    pre = "c1_"
+    n = int(d[pre + "n"])
+    indptr, idx, val = d[pre + "indptr"], d[pre + "idx"], d[pre + "val"]
+    rows = [RRow(idx[indptr[i]:indptr[i + 1]], val[indptr[i]:indptr[i + 1]]) for i in range(len(indptr) - 1)]
+    m = d[pre + "b"].size
+    prob = RProblem(n=n, C=RSym(n, d[pre + "C"]), A=rows[:m], b=d[pre + "b"], G=rows[m:], h=d[pre + "h"],
+                    name="lr_small_c1")
+    ext = rio.write_extended(prob)
+    out["ext_text"] = np.array(ext)
+    p2 = rio.parse_extended(ext)
+    flatten_problem("ext_", p2, out)
+    cfg = pdsdp.SolverConfig(eps_tol=1e-4, max_iter=400, initial_rank=1, window_ell=50, time_limit_s=1e9)
+    res = pdsdp.solve_lr_pd_sdp(prob, cfg)
+    rep = check_solution(prob, res.X, res.y)
+    out["sol_text"] = np.array(rio.write_solution(res, rep))
+    np.savez_compressed(path, **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -380,6 +453,7 @@ if __name__ == "__main__":
         "pd_small": lambda: make_pd_small(os.path.join(HERE, "pd_small.npz")),
         "mimo": lambda: make_mimo(os.path.join(HERE, "mimo.npz")),
         "check": lambda: make_check(os.path.join(HERE, "check.npz")),
+        "io": lambda: make_io(os.path.join(HERE, "io.npz")),
     }
     if a.big:
         jobs["cfg2"] = lambda: make_sketch(os.path.join(HERE, "cfg2_sketch.npz"), 1, (1, 5))
