@@ -56,6 +56,24 @@ struct State {
 // (label, cycle) pairs for a per-step timeline.
 #define PDSDP_TRACE_CAP 2040
 #define PDSDP_TRACE_CTA 1024
+// Pointer into this CTA's dynamic shared memory.  Workspace pointers are
+// carved out once and kept in a shared struct; loaded back from there, the
+// compiler no longer knows their address space and emits generic 64-bit
+// loads (LD.E, long scoreboard).  ShPtr keeps the byte offset instead and
+// rebuilds the pointer from the extern shared array on every use, so the
+// accesses compile to LDS/STS with 32-bit addressing.  (An assumed
+// __isShared() on the generic pointer miscompiles in cluster launches.)
+extern __shared__ __align__(16) unsigned char pdsdp_dsm[];
+template <class T>
+struct ShPtr {
+  unsigned off;
+  __device__ __forceinline__ ShPtr& operator=(T* q) {
+    off = (unsigned)(reinterpret_cast<const unsigned char*>(q) - pdsdp_dsm);
+    return *this;
+  }
+  __device__ __forceinline__ operator T*() const { return reinterpret_cast<T*>(pdsdp_dsm + off); }
+};
+
 struct Prof {
   long long last;
   long long acc[16];

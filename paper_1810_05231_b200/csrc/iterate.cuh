@@ -67,21 +67,21 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
 }
 
 struct Sm {
-  double *A, *Q, *L, *M, *T;   // lds x lds each
-  double *gsc;                 // PDSDP_GRAM_SCR
-  double* ys;                  // staged operand block (n x ycw)
-  double *SF, *SYc, *SYp;      // own rows of F (SYc/SYp unused)
-  int* szp;                    // own rows of zptr
-  int* gb;                     // [C+1] first row of each CTA (multicast row groups)
+  ShPtr<double> A, Q, L, M, T;  // lds x lds each
+  ShPtr<double> gsc;           // PDSDP_GRAM_SCR
+  ShPtr<double> ys;            // staged operand block (n x ycw)
+  ShPtr<double> SF;            // own rows of F
+  ShPtr<int> szp;              // own rows of zptr
+  ShPtr<int> gb;               // [C+1] first row of each CTA (multicast row groups)
   int own, sld;                // own-row buffers valid; their stride
   int ycap;                    // doubles in the staging buffer
   int ycw;                     // staged column chunk width (even; 0 = gather path)
-  const int* zc;               // staged Z columns of own rows
-  const double* zvs;           // staged Z values of own rows
+  ShPtr<const int> zc;         // staged Z columns of own rows
+  ShPtr<const double> zvs;     // staged Z values of own rows
   int zoff, zstaged;
-  double *scr;                 // NTHR
-  double *theta, *res, *lamF, *lamN, *dsc, *cs, *red1;  // BMAX each (red1: 2*BMAX)
-  int *perm, *pq, *flag;
+  ShPtr<double> scr;           // NTHR
+  ShPtr<double> theta, res, lamF, lamN, dsc, cs, red1;  // BMAX each (red1: 2*BMAX)
+  ShPtr<int> perm, pq, flag;
   int lds;
 };
 
@@ -596,6 +596,48 @@ __device__ __forceinline__ int own_ystr(int bc) { return own_stride(bc) + 2; }
 // they fit the row stride of SF
 __device__ __forceinline__ bool own_lock_sm(int rFx, int nlock, int sl) { return nlock > 0 && rFx + nlock <= sl; }
 
+// Sparse part of one operator-step row group: for every (own row, 4-column
+// chunk) item of this thread, accumulate Z[row, q] * Y[q, chunk] over the
+// row's slots whose column q lies in the staged rows [R0, R1).  The items of
+// a thread run interleaved (independent chains) and the next slot's column
+// is loaded before the current slot's products, so a thread keeps several
+// shared-memory round trips in flight.  SZ: Z slots staged in shared memory.
+template <bool SZ>
+__device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const double* __restrict__ zval,
+                                           const double* ys, int R0, int R1, int nitems, int nch, int ys_,
+                                           int (&ep)[PDSDP_OWN_ITEMS], const int (&ee)[PDSDP_OWN_ITEMS],
+                                           double (&zacc)[PDSDP_OWN_ITEMS][4]) {
+  const int tid = threadIdx.x;
+  constexpr int BIG = 0x7fffffff;
+  int q[PDSDP_OWN_ITEMS];
+  const double* yb[PDSDP_OWN_ITEMS];
+#pragma unroll
+  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+    const int it = tid + u * blockDim.x;
+    q[u] = (it < nitems && ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
+    yb[u] = ys + 4 * (it % nch) - (size_t)R0 * ys_;
+  }
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) any |= q[u] < R1;
+    if (!any) break;
+#pragma unroll
+    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      if (q[u] < R1) {
+        const int e = ep[u];
+        const double zv_ = zval[e];
+        const double2 p0 = *reinterpret_cast<const double2*>(yb[u] + (size_t)q[u] * ys_);
+        const double2 p1 = *reinterpret_cast<const double2*>(yb[u] + (size_t)q[u] * ys_ + 2);
+        ep[u] = e + 1;
+        q[u] = (e + 1 < ee[u]) ? zcol[e + 1] : BIG;
+        zacc[u][0] = fma(zv_, p0.x, zacc[u][0]); zacc[u][1] = fma(zv_, p0.y, zacc[u][1]);
+        zacc[u][2] = fma(zv_, p1.x, zacc[u][2]); zacc[u][3] = fma(zv_, p1.y, zacc[u][3]);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
                                                   double* out, int c0, int bc, int rF, int nlock,
                                                   double ca, double cb, double cd, Prof& pf,
@@ -680,27 +722,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     __syncthreads();
     prof_mark(pf, 14);
-#pragma unroll
-    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
-      const int it = tid + u * blockDim.x;
-      if (it >= nitems) break;
-      const int cq = it % nch;
-      const double* yb = ys + 4 * cq - (size_t)R0 * ys_;
-      int e = ep[u];
-      const int e1 = ee[u];
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (; e < e1; ++e) {
-        const int q = zcol[e];
-        if (q >= R1) break;
-        const double zv_ = zval[e];
-        const double2 p0 = *reinterpret_cast<const double2*>(yb + (size_t)q * ys_);
-        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q * ys_ + 2);
-        a0 = fma(zv_, p0.x, a0); a1 = fma(zv_, p0.y, a1);
-        a2 = fma(zv_, p1.x, a2); a3 = fma(zv_, p1.y, a3);
-      }
-      ep[u] = e;
-      zacc[u][0] += a0; zacc[u][1] += a1; zacc[u][2] += a2; zacc[u][3] += a3;
-    }
+    if (s.zstaged) own_gather<true>(s.zc, s.zvs, ys, R0, R1, nitems, nch, ys_, ep, ee, zacc);
+    else own_gather<false>(zcol, zval, ys, R0, R1, nitems, nch, ys_, ep, ee, zacc);
     g0 = g1;
     prof_tick(pf, 22);
     if (g0 < C) cg::this_cluster().sync();
@@ -1093,7 +1116,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   // launch invariants: Z column indices of the own rows, row pointers, groups
   if (s.zstaged) {
     const int nzl = d.zptr[x.r1] - s.zoff;
-    for (int e = tid; e < nzl; e += blockDim.x) ((int*)s.zc)[e] = d.zcol[s.zoff + e];
+    for (int e = tid; e < nzl; e += blockDim.x) const_cast<int*>(static_cast<const int*>(s.zc))[e] = d.zcol[s.zoff + e];
   }
   if (own_base) {
     for (int lr = tid; lr <= x.r1 - x.r0; lr += blockDim.x) s.szp[lr] = d.zptr[x.r0 + lr];
@@ -1165,7 +1188,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   // them in shared memory (its adjoint gather), otherwise stage them
   if (s.zstaged && (step == step0 || rerun)) {
     const int nzl = d.zptr[x.r1] - s.zoff;
-    for (int e = tid; e < nzl; e += blockDim.x) ((double*)s.zvs)[e] = zv[s.zoff + e];
+    for (int e = tid; e < nzl; e += blockDim.x) const_cast<double*>(static_cast<const double*>(s.zvs))[e] = zv[s.zoff + e];
   }
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
     const int rho = x.r0 + it / b, j = it % b;
@@ -1500,9 +1523,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // block-pair updates pay off once the per-element traffic dominates the
     // per-round latency (tools/microbench/small_dense_probe.cu: 1.4x at b = 28)
     if (b >= 24)
-      jacobi_eig4(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
+      jacobi_eig4(s.A, s.M, s.Q, s.T, b, lds, s.cs, reinterpret_cast<int*>(static_cast<double*>(s.gsc)), s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     else
-      jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, (int*)s.gsc, s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
+      jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, reinterpret_cast<int*>(static_cast<double*>(s.gsc)), s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     prof_mark(pf, 12);
     if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];
     sort_desc(Aj, b, lds, s.theta, s.perm);
@@ -1732,7 +1755,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // loads may move ahead of the stores below); y+ / dy come from other
     // CTAs of the cluster (coherent L2 loads)
     const int e0 = d.zptr[x.r0], e1 = d.zptr[x.r1];
-    double* zsm = s.zstaged ? (double*)s.zvs - s.zoff : nullptr;   // Z_k is dead: keep Z_k+1 here too
+    double* zsm = s.zstaged ? const_cast<double*>(static_cast<const double*>(s.zvs)) - s.zoff : nullptr;   // Z_k is dead: keep Z_k+1 here too
     for (int e = e0 + tid; e < e1; e += blockDim.x) {
       double z = __ldg(d.cval + e), a = 0.0;
       const int t0 = __ldg(d.tptr + e), t1 = __ldg(d.tptr + e + 1);

@@ -16,7 +16,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpdsdp_b200.so")
+LIB_PATH = os.environ.get("PDSDP_B200_LIB") or os.path.join(_HERE, "libpdsdp_b200.so")
 
 OUT_LEN = 16
 OUT_EPS_P, OUT_EPS_D, OUT_LAMBDA, OUT_FINITE = 0, 1, 2, 3
