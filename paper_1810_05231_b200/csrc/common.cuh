@@ -73,6 +73,13 @@ struct ShPtr {
   }
   __device__ __forceinline__ operator T*() const { return reinterpret_cast<T*>(pdsdp_dsm + off); }
 };
+// The same pointer rebuilt from the extern shared array (p must point into
+// this CTA's dynamic shared memory): accesses through it compile to LDS/STS.
+template <class T>
+__device__ __forceinline__ T* as_shared(T* p) {
+  const unsigned o = (unsigned)__cvta_generic_to_shared(p) - (unsigned)__cvta_generic_to_shared(pdsdp_dsm);
+  return reinterpret_cast<T*>(pdsdp_dsm + o);
+}
 
 struct Prof {
   long long last;

@@ -172,6 +172,8 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // on FP64 tensor cores: warps take (tile group, row chunk) work items, each
 // accumulating up to four 8x8 DMMA tiles over its rows (k = 4 rows per
 // mma.m8n8k4); chunks are then added in a fixed order through shared memory.
+// SA / SB: A / B lie in this CTA's shared memory (LDS instead of generic loads).
+template <bool SA = false, bool SB = false>
 __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const double* __restrict__ B, int ldb,
                           int nb, int r0, int r1, double* gout, double* wsm);
 
@@ -180,8 +182,12 @@ __device__ __forceinline__ void gram_mma(const double* __restrict__ A, int na, c
   gram_mma2(A, ld, na, B, ld, nb, r0, r1, gout, wsm);
 }
 
+template <bool SA, bool SB>
 __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const double* __restrict__ B, int ldb,
                           int nb, int r0, int r1, double* gout, double* wsm) {
+  if (SA) A = as_shared(A);
+  if (SB) B = as_shared(B);
+  wsm = as_shared(wsm);
   const int q = na * nb;
   if (q == 0) return;
   const int mt = (na + 7) >> 3, ntl = (nb + 7) >> 3, tiles = mt * ntl;
@@ -653,9 +659,9 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
-      gram_mma2(s.SF, sl, rF + nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2<true, false>(s.SF, sl, rF + nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
     } else {
-      gram_mma2(s.SF, sl, rF, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2<true, false>(s.SF, sl, rF, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
       gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl,
                 slot + rF * bc, s.gsc);
     }
@@ -804,10 +810,10 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     __syncthreads();
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
-      gram_mma2(s.SF, sl, rF + nlock, yo, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2<true, true>(s.SF, sl, rF + nlock, yo, ys_, bc, 0, nl, slot, s.gsc);
     } else {
-      gram_mma2(s.SF, sl, rF, yo, ys_, bc, 0, nl, slot, s.gsc);
-      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, yo, ys_, bc, 0, nl, slot + rF * bc, s.gsc);
+      gram_mma2<true, true>(s.SF, sl, rF, yo, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2<false, true>(d.V + (size_t)x.r0 * ld, ld, nlock, yo, ys_, bc, 0, nl, slot + rF * bc, s.gsc);
     }
     gram_ready = true;
   }
@@ -1465,8 +1471,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     {
       double* slot = red_slot(d, x, x.c);
       if (rsm) {
-        gram_mma2(S1, b, b, S1, b, b, 0, nlr, slot, s.gsc);
-        gram_mma2(S1, b, b, S2, b, b, 0, nlr, slot + b * b, s.gsc);
+        gram_mma2<true, true>(S1, b, b, S1, b, b, 0, nlr, slot, s.gsc);
+        gram_mma2<true, true>(S1, b, b, S2, b, b, 0, nlr, slot + b * b, s.gsc);
       } else {
         gram_mma(buf(iav), b, buf(iav), b, ld, x.r0, x.r1, slot, s.gsc);
         gram_mma(buf(iav), b, buf(iw1), b, ld, x.r0, x.r1, slot + b * b, s.gsc);

@@ -154,6 +154,10 @@ __device__ void jacobi_eig(double* A, double* Q, int b, int lds, double* cs, int
 
 // Descending order of the diagonal of A: perm[rank] = index (ties by index).
 __device__ void sort_desc(const double* A, int b, int lds, double* theta, int* perm) {
+  // every caller passes shared-memory workspaces: LDS/STS, not generic loads
+  A = as_shared(A);
+  theta = as_shared(theta);
+  perm = as_shared(perm);
   for (int i = threadIdx.x; i < b; i += blockDim.x) {
     double ti = A[i * lds + i];
     int rank = 0;
@@ -173,6 +177,10 @@ __device__ void sort_desc(const double* A, int b, int lds, double* theta, int* p
 // C = A * B   (a x k) * (k x c), all shared memory, leading dims given.
 __device__ void sm_gemm(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
                         int a, int k, int c) {
+  // every caller passes shared-memory workspaces: LDS/STS, not generic loads
+  A = as_shared(A);
+  B = as_shared(B);
+  C = as_shared(C);
   for (int e = threadIdx.x; e < a * c; e += blockDim.x) {
     int i = e / c, j = e % c;
     double s = 0.0;
@@ -520,6 +528,9 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
 // step j (P = blockDim / b parts per row): no per-element index division and
 // one barrier per step.
 __device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
+  // every caller passes shared-memory workspaces: LDS/STS, not generic loads
+  G = as_shared(G);
+  dsc = as_shared(dsc);
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < b; i += nt) {
     const double g = G[i * lds + i];
@@ -555,6 +566,9 @@ __device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
 
 // X = L^{-1} (lower) as tri_inv_lower_1s, with the fixed (row, part) thread map.
 __device__ void tri_inv_lower_rows(const double* L, double* X, int b, int lds) {
+  // every caller passes shared-memory workspaces: LDS/STS, not generic loads
+  L = as_shared(L);
+  X = as_shared(X);
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < b * b; e += nt) X[(e / b) * lds + (e % b)] = (e / b == e % b) ? 1.0 : 0.0;
   __syncthreads();
@@ -707,6 +721,14 @@ __device__ void jacobi_eig2(double* A, double* A2, double* Q, double* Q2, int b,
 // sweep).
 __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
                             int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
+  // every caller passes shared-memory workspaces: LDS/STS, not generic loads
+  A = as_shared(A);
+  A2 = as_shared(A2);
+  Q = as_shared(Q);
+  Q2 = as_shared(Q2);
+  cs = as_shared(cs);
+  tab = as_shared(tab);
+  sflag = as_shared(sflag);
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ double fro_part[32];
   double f = 0.0;
@@ -749,7 +771,9 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
           if (j > i && fabs(Ac[i * lds + j]) > ((i < nimp) ? thr_imp : thr_guard)) need = 1;
       if (!__syncthreads_or(need)) break;
       for (int t = 0; t < R; ++t) {
+        Ac = as_shared(Ac); An = as_shared(An); Qc = as_shared(Qc); Qn = as_shared(Qn);
         const int* pt = tab + t * bb;
+        int rot = 0;                    // a non-identity rotation in this round
         // (1) rotation of the pair (p, q), p < q, stored per index
         if (tid < b) {
           const int p = tid, q = pt[p];
@@ -775,12 +799,14 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
             // column lo_ -> c*col_lo - s*col_hi ; column hi_ -> s*col_lo + c*col_hi
             c0a[p] = c;
             c1a[p] = (p == lo_) ? -sn : sn;
+            rot |= (sn != 0.0);
           } else {
             c0a[p] = 1.0;
             c1a[p] = 0.0;
           }
         }
-        __syncthreads();
+        // a round of identity rotations leaves A and Q bit-for-bit unchanged: skip it
+        if (!__syncthreads_or(rot)) continue;
         // (2) A' = J^T A J and Q' = Q J
         for (int i = ri; i < b; i += rstep) {
           const int pi = pt[i];
@@ -820,6 +846,14 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
 // scratch: cs >= 4 * PDSDP_BMAX doubles; tab >= PDSDP_BMAX * (PDSDP_BMAX + 2) / 8 + 2 * PDSDP_BMAX ints.
 __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
                             int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
+  // every caller passes shared-memory workspaces: LDS/STS, not generic loads
+  A = as_shared(A);
+  A2 = as_shared(A2);
+  Q = as_shared(Q);
+  Q2 = as_shared(Q2);
+  cs = as_shared(cs);
+  tab = as_shared(tab);
+  sflag = as_shared(sflag);
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ double fro_part[32];
   double f = 0.0;
@@ -859,7 +893,9 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
           if (j > i && fabs(Ac[i * lds + j]) > ((i < nimp) ? thr_imp : thr_guard)) need = 1;
       if (!__syncthreads_or(need)) break;
       for (int t = 0; t < R; ++t) {
+        Ac = as_shared(Ac); An = as_shared(An); Qc = as_shared(Qc); Qn = as_shared(Qn);
         // (1) rotation of pair k (round-robin order of jacobi_eig3)
+        int rot = 0;                    // a non-identity rotation in this round
         for (int k = tid; k < np; k += nt) {
           const int p = (k == 0) ? 0 : 1 + (k - 1 + t) % R;
           const int q = 1 + (bb - 2 - k + t) % R;
@@ -887,8 +923,10 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
           phi[k] = (hi_ < b) ? hi_ : -1;
           pc[k] = c;
           ps[k] = sn;
+          rot |= (sn != 0.0);
         }
-        __syncthreads();
+        // a round of identity rotations leaves A and Q bit-for-bit unchanged: skip it
+        if (!__syncthreads_or(rot)) continue;
         // (2) A' = J^T A J by 2x2 blocks, Q' = Q J by row / column pair
         for (int it = tid; it < nA + nQ; it += nt) {
           if (it < nA) {

@@ -31,3 +31,15 @@ lo = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 for i in range(max(1, lo), min(n, nshow)):
     d = np.array([(e[i, 1] - e[i - 1, 1]) / 1965.0 for e in evs])
     print(f"{i:3d} [{int(labels[i-1]):2d}->{int(labels[i]):2d}]  min {d.min():6.2f}  med {np.median(d):6.2f}  max {d.max():6.2f} (cta {d.argmax():2d})  cta0 {d[0]:6.2f}")
+
+# aggregate: total CTA-0 time per transition (label_prev -> label)
+import collections
+agg = collections.defaultdict(lambda: [0, 0.0])
+for i in range(1, n):
+    key = (int(labels[i - 1]), int(labels[i]))
+    dmax = max((e[i, 1] - e[i - 1, 1]) / 1965.0 for e in evs)
+    agg[key][0] += 1
+    agg[key][1] += (evs[0][i, 1] - evs[0][i - 1, 1]) / 1965.0
+print("transition totals (CTA 0):")
+for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"  {k[0]:3d}->{k[1]:3d}  count {c:4d}  total {t:8.1f} us  mean {t / c:6.2f} us")
