@@ -610,19 +610,14 @@ __device__ __forceinline__ bool own_lock_sm(int rFx, int nlock, int sl) { return
 // shared-memory round trips in flight.  SZ: Z slots staged in shared memory.
 template <bool SZ>
 __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const double* __restrict__ zval,
-                                           const double* ys, int R0, int R1, int nitems, int nch, int ys_,
+                                           const double* ys, int R0, int R1, int cq, int ys_,
                                            int (&ep)[PDSDP_OWN_ITEMS], const int (&ee)[PDSDP_OWN_ITEMS],
                                            double (&zacc)[PDSDP_OWN_ITEMS][4]) {
-  const int tid = threadIdx.x;
   constexpr int BIG = 0x7fffffff;
   int q[PDSDP_OWN_ITEMS];
-  const double* yb[PDSDP_OWN_ITEMS];
+  const double* yb = ys + 4 * cq - (size_t)R0 * ys_;
 #pragma unroll
-  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
-    const int it = tid + u * blockDim.x;
-    q[u] = (it < nitems && ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
-    yb[u] = ys + 4 * (it % nch) - (size_t)R0 * ys_;
-  }
+  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) q[u] = (ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
   while (true) {
     bool any = false;
 #pragma unroll
@@ -633,8 +628,8 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
       if (q[u] < R1) {
         const int e = ep[u];
         const double zv_ = zval[e];
-        const double2 p0 = *reinterpret_cast<const double2*>(yb[u] + (size_t)q[u] * ys_);
-        const double2 p1 = *reinterpret_cast<const double2*>(yb[u] + (size_t)q[u] * ys_ + 2);
+        const double2 p0 = *reinterpret_cast<const double2*>(yb + (size_t)q[u] * ys_);
+        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q[u] * ys_ + 2);
         ep[u] = e + 1;
         q[u] = (e + 1 < ee[u]) ? zcol[e + 1] : BIG;
         zacc[u][0] = fma(zv_, p0.x, zacc[u][0]); zacc[u][1] = fma(zv_, p0.y, zacc[u][1]);
@@ -655,7 +650,11 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const size_t nld = (size_t)n * (ld + 4);
   const double* Ycur = d.Yc + (size_t)ycp * nld;
   double* Ynxt = d.Yc + (size_t)(ycp ^ 1) * nld;
-  const int nitems = nl * nch;
+  // work items: (own row, 4-column chunk).  Thread t takes chunk t % nch of
+  // rows t / nch + u * rps (u < PDSDP_OWN_ITEMS): its items share the column
+  // chunk, so the dense epilogue loads each T entry once for all of them
+  const int rps = blockDim.x / nch, cq = tid % nch, lr0 = tid / nch;
+  const bool tact = lr0 < rps;
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
@@ -682,10 +681,10 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   int ep[PDSDP_OWN_ITEMS], ee[PDSDP_OWN_ITEMS];
 #pragma unroll
   for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
-    const int it = tid + u * blockDim.x;
-    const int lr = (it < nitems) ? it / nch : 0;
-    ep[u] = s.szp[lr] - zoff;
-    ee[u] = (it < nitems) ? s.szp[lr + 1] - zoff : ep[u];
+    const int lr = lr0 + u * rps;
+    const bool ok = tact && lr < nl;
+    ep[u] = s.szp[ok ? lr : 0] - zoff;
+    ee[u] = ok ? s.szp[lr + 1] - zoff : ep[u];
 #pragma unroll
     for (int v = 0; v < 4; ++v) zacc[u][v] = 0.0;
   }
@@ -728,8 +727,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     __syncthreads();
     prof_mark(pf, 14);
-    if (s.zstaged) own_gather<true>(s.zc, s.zvs, ys, R0, R1, nitems, nch, ys_, ep, ee, zacc);
-    else own_gather<false>(zcol, zval, ys, R0, R1, nitems, nch, ys_, ep, ee, zacc);
+    if (s.zstaged) own_gather<true>(s.zc, s.zvs, ys, R0, R1, cq, ys_, ep, ee, zacc);
+    else own_gather<false>(zcol, zval, ys, R0, R1, cq, ys_, ep, ee, zacc);
     g0 = g1;
     prof_tick(pf, 22);
     if (g0 < C) cg::this_cluster().sync();
@@ -741,12 +740,34 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   // locked pairs' own rows sit after F's in SF when they fit (own_lock_sm)
   const int nsf = own_lock_sm(rF, nlock, sl) ? rF + nlock : rF;
   const int nglb = nsf == rF ? nlock : 0;
+  // dense part [F | V_lock] T of all items: T entries loaded once per thread
+  double w[PDSDP_OWN_ITEMS][4];
+#pragma unroll
+  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) w[u][v] = 0.0;
+  if (tact) {
+    const double* Fr[PDSDP_OWN_ITEMS];
+#pragma unroll
+    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      const int lr = lr0 + u * rps;
+      Fr[u] = s.SF + (size_t)(lr < nl ? lr : 0) * sl;
+    }
+    const double* Tc = s.T + 4 * cq;   // entries past bc are never used
+    for (int l = 0; l < nsf; ++l) {
+      const double t0 = Tc[l * bc], t1 = Tc[l * bc + 1], t2 = Tc[l * bc + 2], t3 = Tc[l * bc + 3];
+#pragma unroll
+      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+        const double f = Fr[u][l];
+        w[u][0] = fma(f, t0, w[u][0]); w[u][1] = fma(f, t1, w[u][1]);
+        w[u][2] = fma(f, t2, w[u][2]); w[u][3] = fma(f, t3, w[u][3]);
+      }
+    }
+  }
 #pragma unroll
   for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
-    const int it = tid + u * blockDim.x;
-    if (it >= nitems) break;
-    const int lr = it / nch, cq = it - lr * nch;
-    const double* Fr = s.SF + (size_t)lr * sl;
+    const int lr = lr0 + u * rps;
+    if (!tact || lr >= nl) break;
     const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
     const size_t oc = (size_t)(x.r0 + lr) * ys_ + 4 * cq;
     // recurrence terms Y_j, Y_{j-1} of the item, loaded before its stores
@@ -759,24 +780,17 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       yc[v] = (ok && cb != 0.0) ? __ldcg(Ycur + oc + v) : 0.0;
       yp[v] = (ok && cd != 0.0) ? __ldcg(Ynxt + oc + v) : 0.0;
     }
-    double w[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int l = 0; l < nsf; ++l) {
-      const double f = Fr[l];
-      const double* Tl = s.T + l * bc + 4 * cq;   // entries past bc are never used
-#pragma unroll
-      for (int v = 0; v < 4; ++v) w[v] = fma(f, Tl[v], w[v]);
-    }
     for (int t = 0; t < nglb; ++t) {
       const double f = __ldcg(Vr + t);
       const double* Tl = s.T + (rF + t) * bc + 4 * cq;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) w[v] = fma(f, Tl[v], w[v]);
+      for (int v = 0; v < 4; ++v) w[u][v] = fma(f, Tl[v], w[u][v]);
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int jj = 4 * cq + v;
       if (jj >= bc) break;
-      const double wv = fma(-alpha, zacc[u][v], w[v]);
+      const double wv = fma(-alpha, zacc[u][v], w[u][v]);
       double o = ca * wv;
       if (cb != 0.0) o = fma(cb, yc[v], o);
       if (cd != 0.0) o = fma(cd, yp[v], o);
@@ -801,9 +815,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     double* yo = s.ys;
 #pragma unroll
     for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
-      const int it = tid + u * blockDim.x;
-      if (it >= nitems) break;
-      const int lr = it / nch, cq = it - lr * nch;
+      const int lr = lr0 + u * rps;
+      if (!tact || lr >= nl) break;
 #pragma unroll
       for (int v = 0; v < 4; ++v) yo[(size_t)lr * ys_ + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
     }
@@ -1107,7 +1120,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     {
       const int nl = x.r1 - x.r0, sp = own_ystr(lcap);
       s.own = (owncap > 0 && nl * lcap <= owncap && nl <= nlmax && nl * sp <= s.ycap &&
-               nl * (sp / 4) <= PDSDP_OWN_ITEMS * PDSDP_NTHR) ? 1 : 0;
+               nl <= PDSDP_OWN_ITEMS * (PDSDP_NTHR / (sp / 4))) ? 1 : 0;
     }
   }
   __shared__ __align__(8) unsigned long long mbar_sm;   // completion barrier of the operand all-gather
