@@ -615,7 +615,12 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
                                            double (&zacc)[PDSDP_OWN_ITEMS][4]) {
   constexpr int BIG = 0x7fffffff;
   int q[PDSDP_OWN_ITEMS];
-  const double* yb = ys + 4 * cq - (size_t)R0 * ys_;
+  // chunks 4..7 of a quarter warp read their upper 16 bytes first: the eight
+  // first loads of a row's chunks then fall in eight distinct bank groups
+  // (zacc holds the two halves swapped for those threads; the caller undoes it)
+  const int sw = (cq >> 2) & 1;
+  const double* yb = ys + 4 * cq + 2 * sw - (size_t)R0 * ys_;
+  const int o2 = 2 - 4 * sw;
 #pragma unroll
   for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) q[u] = (ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
   while (true) {
@@ -629,7 +634,7 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
         const int e = ep[u];
         const double zv_ = zval[e];
         const double2 p0 = *reinterpret_cast<const double2*>(yb + (size_t)q[u] * ys_);
-        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q[u] * ys_ + 2);
+        const double2 p1 = *reinterpret_cast<const double2*>(yb + (size_t)q[u] * ys_ + o2);
         ep[u] = e + 1;
         q[u] = (e + 1 < ee[u]) ? zcol[e + 1] : BIG;
         zacc[u][0] = fma(zv_, p0.x, zacc[u][0]); zacc[u][1] = fma(zv_, p0.y, zacc[u][1]);
@@ -733,6 +738,13 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     prof_tick(pf, 22);
     if (g0 < C) cg::this_cluster().sync();
     prof_mark(pf, 3);
+  }
+  if ((cq >> 2) & 1) {        // own_gather kept this thread's chunk halves swapped
+#pragma unroll
+    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      double t = zacc[u][0]; zacc[u][0] = zacc[u][2]; zacc[u][2] = t;
+      t = zacc[u][1]; zacc[u][1] = zacc[u][3]; zacc[u][3] = t;
+    }
   }
 #ifdef PDSDP_PROF_EPI
   prof_mark(pf, 10);
