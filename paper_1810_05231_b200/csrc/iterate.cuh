@@ -1513,17 +1513,46 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       x.par ^= 1;
       __syncthreads();
     }
-    // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe
+    // L2 = chol(G2 scaled); H' = L2^-1 D H D L2^-T ; eig ; B = D L2^-T Qe.
+    // After the first CholQR the scaled G2 = D G2 D is I + E with E at the
+    // level of u kappa^2; when max|E| <= 1e-5 the second Cholesky is replaced
+    // by the series (I + E)^(-1/2) = I - E/2 + 3/8 E^2 + O(E^3) (symmetric
+    // K instead of the triangular L2^-1; V^T V = I + O(E^3)).
     prof_mark(pf, 8);
-    okc = chol_scaled_rows(s.A, b, lds, s.dsc);
-    if (!okc) {
-      if (++fails >= 8 || m == 0) break;
-      force_m = m / 2;
-      continue;
+    bool g2s = false;
+    {
+      for (int i = tid; i < b; i += blockDim.x) {
+        const double g = s.A[i * lds + i];
+        s.dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
+      }
+      __syncthreads();
+      int big = 0;
+      for (int e = tid; e < b * b; e += blockDim.x) {
+        const int i = e / b, j = e % b;
+        const double v = fma(s.A[i * lds + j] * s.dsc[i], s.dsc[j], (i == j) ? -1.0 : 0.0);
+        s.L[i * lds + j] = v;
+        big |= !(fabs(v) <= 1e-5);
+      }
+      g2s = !__syncthreads_or(big);
+    }
+    if (g2s) {
+      sm_gemm(s.L, lds, s.L, lds, s.M, lds, b, b, b);            // E^2
+      for (int e = tid; e < b * b; e += blockDim.x) {
+        const int i = e / b, j = e % b;
+        s.L[i * lds + j] = fma(0.375, s.M[i * lds + j], fma(-0.5, s.L[i * lds + j], (i == j) ? 1.0 : 0.0));
+      }
+      __syncthreads();
+    } else {
+      okc = chol_scaled_rows(s.A, b, lds, s.dsc);
+      if (!okc) {
+        if (++fails >= 8 || m == 0) break;
+        force_m = m / 2;
+        continue;
+      }
     }
     if (nlock == 0) msucc += m;
     prof_mark(pf, 9);
-    tri_inv_lower_rows(s.A, s.L, b, lds);            // L = L2^-1
+    if (!g2s) tri_inv_lower_rows(s.A, s.L, b, lds);            // L = L2^-1
     prof_mark(pf, 10);
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
@@ -1566,7 +1595,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       int i = e / b, j = e % b;
       const int pj = s.perm[j];
       double acc = 0.0;
-      for (int t = i; t < b; ++t) acc += s.L[t * lds + i] * Qj[t * lds + pj];
+      for (int t = g2s ? 0 : i; t < b; ++t) acc += s.L[t * lds + i] * Qj[t * lds + pj];   // L2^-T (lower) or K
       Bm[i * lds + j] = s.dsc[i] * acc;
     }
     __syncthreads();
