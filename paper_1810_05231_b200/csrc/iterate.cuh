@@ -661,13 +661,21 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const int rps = blockDim.x / nch, cq = tid % nch, lr0 = tid / nch;
   const bool tact = lr0 < rps;
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
+    // own rows of Y_j into the (still idle) staging buffer first: a Gram
+    // product reading L2 directly waits one round trip per k-step
+    double* yo = s.ys;
+    {
+      const double* src = Ycur + (size_t)x.r0 * ys_;
+      for (int i = tid; i < nl * ys_ / 2; i += blockDim.x)
+        reinterpret_cast<double2*>(yo)[i] = __ldcg(reinterpret_cast<const double2*>(src) + i);
+    }
+    __syncthreads();
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
-      gram_mma2<true, false>(s.SF, sl, rF + nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2<true, true>(s.SF, sl, rF + nlock, yo, ys_, bc, 0, nl, slot, s.gsc);
     } else {
-      gram_mma2<true, false>(s.SF, sl, rF, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl, slot, s.gsc);
-      gram_mma2(d.V + (size_t)x.r0 * ld, ld, nlock, Ycur + (size_t)x.r0 * ys_, ys_, bc, 0, nl,
-                slot + rF * bc, s.gsc);
+      gram_mma2<true, true>(s.SF, sl, rF, yo, ys_, bc, 0, nl, slot, s.gsc);
+      gram_mma2<false, true>(d.V + (size_t)x.r0 * ld, ld, nlock, yo, ys_, bc, 0, nl, slot + rF * bc, s.gsc);
     }
   }
   gram_ready = false;
@@ -1418,14 +1426,16 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       // block, smem-resident F rows); G1 = Y^T Y rides in the step's reduction
       const int nl = x.r1 - x.r0, bcp = own_ystr(b);   // compact row stride
       prof_mark(pf, 1);
+      double* yo = s.ys;   // own rows for the G1 product (staging buffer idle until the step's barrier)
       for (int it = tid; it < nl * b; it += blockDim.x) {
         const int lr = it / b, jj = it - lr * b;
-        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = buf(iy)[(size_t)(x.r0 + lr) * ld + jj];
+        const double v = buf(iy)[(size_t)(x.r0 + lr) * ld + jj];
+        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
+        yo[(size_t)lr * bcp + jj] = v;
       }
       fence_proxy_async();
       __syncthreads();
-      gram_mma2(d.Yc + (size_t)x.r0 * bcp, bcp, b, d.Yc + (size_t)x.r0 * bcp, bcp, b, 0, nl,
-                red_slot(d, x, x.c) + rFx * b, s.gsc);
+      gram_mma2<true, true>(yo, bcp, b, yo, bcp, b, 0, nl, red_slot(d, x, x.c) + rFx * b, s.gsc);
       int ycp_rr = 0;
       bool gr = false;
       operator_step_own(d, x, s, zv, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0, pf, ycp_rr, &mbar_sm, mphase, gr, false);
