@@ -623,6 +623,37 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
   const int o2 = 2 - 4 * sw;
 #pragma unroll
   for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) q[u] = (ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
+  if (SZ) {
+    // Z slots and operand rows in shared memory: 32-bit shared addresses
+    // kept in registers (the generic form recomputed 64-bit pointers per slot)
+    const unsigned zc_a = smem_u32(zcol), zv_a = smem_u32(zval);
+    const unsigned yb_a = smem_u32(ys) + 8u * (unsigned)(4 * cq + 2 * sw) - 8u * (unsigned)R0 * (unsigned)ys_;
+    const unsigned rowb = 8u * (unsigned)ys_, o2b = 8u * (unsigned)o2;
+    while (true) {
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) any |= q[u] < R1;
+      if (!any) break;
+#pragma unroll
+      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+        if (q[u] < R1) {
+          const int e = ep[u];
+          const unsigned a = yb_a + (unsigned)q[u] * rowb;
+          double zv_, y0, y1, y2, y3;
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(zv_) : "r"(zv_a + 8u * (unsigned)e));
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(y0), "=d"(y1) : "r"(a));
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(y2), "=d"(y3) : "r"(a + o2b));
+          int qn = BIG;
+          if (e + 1 < ee[u]) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qn) : "r"(zc_a + 4u * (unsigned)(e + 1)));
+          ep[u] = e + 1;
+          q[u] = qn;
+          zacc[u][0] = fma(zv_, y0, zacc[u][0]); zacc[u][1] = fma(zv_, y1, zacc[u][1]);
+          zacc[u][2] = fma(zv_, y2, zacc[u][2]); zacc[u][3] = fma(zv_, y3, zacc[u][3]);
+        }
+      }
+    }
+    return;
+  }
   while (true) {
     bool any = false;
 #pragma unroll
