@@ -277,9 +277,10 @@ def run_ours(args, rank, world, local_rank):
     roof = {"kernel": "lrpdhg_iterate_kernel (one launch = one PDHG iteration, residuals included)",
             "bound": "hbm", "achieved": achieved, "peak": B / 1e9, "unit": "GB/s", "frac": achieved / (B / 1e9),
             # dram__bytes_read.sum + dram__bytes_write.sum of one iteration-kernel
-            # launch (ncu --set full, profiles/r01s2_iterate_kernel_ncu_details.txt):
+            # launch = one iteration at the final rank (ncu --set full,
+            # profiles/r01s3_iterate_kernel_ncu_raw_r20.txt; 2340096 at rank 10):
             # the iterate stays L2-resident, the kernel is latency-bound
-            "traffic": 2211840, "traffic_source": "profiles/r01s2_iterate_kernel_ncu_details.txt",
+            "traffic": 2537728, "traffic_source": "profiles/r01s3_iterate_kernel_ncu_raw_r20.txt",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs",
             "algorithmic_bytes_per_iteration": algo_bytes, "algorithmic_flops_per_iteration": algo_flops,
             "basis": f"SURVEY 8(d) dense formulation, n={n}, b={b}, p_pass={mv:.2f}, r={r}",
