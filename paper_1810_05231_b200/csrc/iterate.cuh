@@ -83,7 +83,10 @@ struct Sm {
   ShPtr<double> theta, res, lamF, lamN, dsc, cs, red1;  // BMAX each (red1: 2*BMAX)
   ShPtr<int> perm, pq, flag;
   int lds;
+  int gnext[17];               // operator step: next row group's first CTA after group g (thread 0 plans it)
 };
+
+__device__ __forceinline__ Sm& s_mut(const Sm& s) { return const_cast<Sm&>(s); }
 
 struct Cta {
   int C, c, r0, r1, par;
@@ -690,6 +693,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   // rows t / nch + u * rps (u < PDSDP_OWN_ITEMS): its items share the column
   // chunk, so the dense epilogue loads each T entry once for all of them
   const int rps = blockDim.x / nch, cq = tid % nch, lr0 = tid / nch;
+  const int tstr = (bc + 1) & ~1;   // row stride of T in this step (even)
   const bool tact = lr0 < rps;
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
     // own rows of Y_j into the (still idle) staging buffer first: a Gram
@@ -710,6 +714,15 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
   }
   gram_ready = false;
+  if (tid == 0) {   // row groups that fit the staging buffer (published by the barrier below)
+    const int rc = s.ycap / ys_;
+    for (int g0 = 0; g0 < x.C;) {
+      int g1 = g0 + 1;
+      while (g1 < x.C && s.gb[g1 + 1] - s.gb[g0] <= rc) ++g1;
+      s_mut(s).gnext[g0] = g1;
+      g0 = g1;
+    }
+  }
   prof_mark(pf, 2);
   cg::this_cluster().sync();                 // publishes Y_j rows and the partials
   prof_tick(pf, 20);
@@ -736,8 +749,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   bool first = true;
   while (g0 < C) {
     const int R0 = s.gb[g0];
-    int g1 = g0 + 1;
-    while (g1 < C && s.gb[g1 + 1] - R0 <= rows_cap) ++g1;
+    const int g1 = s.gnext[g0];
     const int R1 = s.gb[g1];
     if (tid == 0) {
       mbar_expect_tx(mbar, (unsigned)((R1 - R0) * ys_ * 8));
@@ -763,7 +775,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
         const int l = i / bc;
         const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
         const double v = cluster_sum(d, x, i, false);
-        s.T[i] = (c == 0.0) ? 0.0 : v * c;
+        s.T[l * tstr + (i - l * bc)] = (c == 0.0) ? 0.0 : v * c;   // even row stride: 16-byte rows
       }
       x.par ^= 1;
       first = false;
@@ -804,14 +816,27 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       const int lr = lr0 + u * rps;
       Fr[u] = s.SF + (size_t)(lr < nl ? lr : 0) * sl;
     }
-    const double* Tc = s.T + 4 * cq;   // entries past bc are never used
+    // entries past bc are never used; chunks 4..7 of a quarter warp read the
+    // upper half of their chunk first (distinct bank groups for all seven
+    // chunks of a row), w then holds those halves swapped until the end
+    const int sw = (cq >> 2) & 1;
+    const double* Tc = s.T + 4 * cq + 2 * sw;
+    const int o2 = 2 - 4 * sw;
     for (int l = 0; l < nsf; ++l) {
-      const double t0 = Tc[l * bc], t1 = Tc[l * bc + 1], t2 = Tc[l * bc + 2], t3 = Tc[l * bc + 3];
+      const double2 ta = *reinterpret_cast<const double2*>(Tc + l * tstr);
+      const double2 tb = *reinterpret_cast<const double2*>(Tc + l * tstr + o2);
 #pragma unroll
       for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
         const double f = Fr[u][l];
-        w[u][0] = fma(f, t0, w[u][0]); w[u][1] = fma(f, t1, w[u][1]);
-        w[u][2] = fma(f, t2, w[u][2]); w[u][3] = fma(f, t3, w[u][3]);
+        w[u][0] = fma(f, ta.x, w[u][0]); w[u][1] = fma(f, ta.y, w[u][1]);
+        w[u][2] = fma(f, tb.x, w[u][2]); w[u][3] = fma(f, tb.y, w[u][3]);
+      }
+    }
+    if (sw) {
+#pragma unroll
+      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+        double t = w[u][0]; w[u][0] = w[u][2]; w[u][2] = t;
+        t = w[u][1]; w[u][1] = w[u][3]; w[u][3] = t;
       }
     }
   }
@@ -833,7 +858,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     for (int t = 0; t < nglb; ++t) {
       const double f = __ldcg(Vr + t);
-      const double* Tl = s.T + (rF + t) * bc + 4 * cq;
+      const double* Tl = s.T + (rF + t) * tstr + 4 * cq;
 #pragma unroll
       for (int v = 0; v < 4; ++v) w[u][v] = fma(f, Tl[v], w[u][v]);
     }
