@@ -1616,7 +1616,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         continue;
       }
     }
-    if (nlock == 0) msucc += m;
+    msucc += m;     // total degree of the iteration (the next first pass takes min(hint, spread cap))
     prof_mark(pf, 9);
     if (!g2s) tri_inv_lower_rows(s.A, s.L, b, lds);            // L = L2^-1
     prof_mark(pf, 10);
