@@ -49,6 +49,8 @@ struct State {
   double dbg[32][8];  // per pass: m, worst rel residual, slow column, theta, t, lo, cut, xnorm
   double prof[16];    // SM cycles of CTA 0 per phase in the last launch
   double hdump[PDSDP_BMAX * PDSDP_BMAX + 8];  // diagnostic: last projected matrix H' (flag bit4)
+  double zlam;        // Lanczos estimate of lambda_max(Z) plus margin (zbound.cuh)
+  double zlam_ok;     // 1 when zlam is valid
 };
 
 // thread-0 phase timer (clock64 deltas; diagnostic only).  With a trace

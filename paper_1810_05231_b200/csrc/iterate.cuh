@@ -1275,7 +1275,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   if (tid == 0) s.own = (own_base && rF + d.nd <= s.sld) ? 1 : 0;
   __syncthreads();
   const int rFx = rF + d.nd;       // factor columns of the operator S = F_x diag(lamF) F_x^T - alpha Z
-  const double lo = st->lo_par[ctl.ypar & 1];
+  // Chebyshev interval floor: Gershgorin bound of -alpha Z, tightened by the
+  // Lanczos estimate of lambda_max(Z) when available (zbound.cuh)
+  const double lo = (st->zlam_ok == 1.0) ? fmax(st->lo_par[ctl.ypar & 1], -d.alpha * st->zlam)
+                                         : st->lo_par[ctl.ypar & 1];
   const double alpha = d.alpha;
   const double* zv = (ctl.ypar & 1) ? d.zbuf1 : d.zbuf0;     // Z_k  = C + M^T y_k
   double* zvn = (ctl.ypar & 1) ? d.zbuf0 : d.zbuf1;          // Z_k+1

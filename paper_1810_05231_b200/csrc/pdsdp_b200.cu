@@ -20,6 +20,9 @@
 #include "iterate.cuh"
 #include "opnorm.cuh"
 #include "residual.cuh"
+#include "zbound.cuh"
+
+#define PDSDP_ZL_EVERY 256   // iterations between lambda_max(Z) estimates
 
 using namespace pdsdp;
 
@@ -75,6 +78,7 @@ struct Instance {
   Inst desc{};
   OpnormDev od{};
   double* d_packed = nullptr;   // scratch packed vector (op-level maps)
+  long long zl_age = 1LL << 40;  // iterations since the last lambda_max(Z) estimate
   long long P = 0;
 };
 
@@ -92,6 +96,8 @@ struct pdsdp_batch {
   int* d_active = nullptr;
   double* h_out = nullptr;   // mapped pinned, count * KMAX * OUT_LEN
   int* d_stop = nullptr;     // per-instance chunk stop flags
+  int* h_zl = nullptr;       // lambda_max(Z) estimate list (instance, y parity)
+  int* d_zl = nullptr;
   double* d_out = nullptr;
   double* d_objpart = nullptr;
   unsigned* d_objcnt = nullptr;
@@ -534,6 +540,8 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
   CK(cudaHostAlloc((void**)&b->h_ctl, (size_t)count * PDSDP_KMAX * sizeof(Ctl), 0));
   memset(b->h_ctl, 0, (size_t)count * PDSDP_KMAX * sizeof(Ctl));
   CK(cudaMalloc(&b->d_stop, (size_t)count * sizeof(int)));
+  CK(cudaMalloc(&b->d_zl, (size_t)2 * count * sizeof(int)));
+  b->h_zl = new int[2 * (size_t)count];
   CK(cudaMemset(b->d_stop, 0, (size_t)count * sizeof(int)));
   CK(cudaHostAlloc((void**)&b->h_active, (size_t)count * sizeof(int), 0));
   CK(cudaMalloc(&b->d_ctl, (size_t)count * PDSDP_KMAX * sizeof(Ctl)));
@@ -591,6 +599,8 @@ int pdsdp_batch_destroy(pdsdp_batch* b) {
   if (b->d_objcnt) cudaFree(b->d_objcnt);
   if (b->d_objres) cudaFree(b->d_objres);
   if (b->d_stop) cudaFree(b->d_stop);
+  if (b->d_zl) cudaFree(b->d_zl);
+  delete[] b->h_zl;
   for (int k = 0; k < 3; ++k) if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   for (int k = 0; k <= PDSDP_KMAX; ++k) if (b->tev[k]) cudaEventDestroy(b->tev[k]);
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -673,6 +683,7 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed) {
   if (rc) return rc;
   Instance* I = b->inst[inst];
   I->bmax = 0;
+  I->zl_age = 1LL << 40;
   CK(cudaMemsetAsync(I->desc.st, 0, sizeof(State), b->stream));
   CK(cudaMemsetAsync(I->desc.V, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
   CK(cudaMemsetAsync(I->desc.F, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
@@ -732,6 +743,30 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
   // one persistent launch per chunk (the kernel loops over the steps and stops
   // where the host must look); the verification mode interleaves the
   // entry-wise residual kernel, so it launches step by step
+  // refresh the lambda_max(Z) estimate of the Chebyshev interval every
+  // PDSDP_ZL_EVERY iterations (Z_k drifts slowly with y; zbound.cuh)
+  {
+    int nz = 0;
+    for (int a = 0; a < nact; ++a) {
+      Instance* I = b->inst[insts[a]];
+      if (I->zl_age >= PDSDP_ZL_EVERY && I->n <= PDSDP_ZL_NMAX) {
+        b->h_zl[2 * nz] = insts[a];
+        b->h_zl[2 * nz + 1] = ypar0[a] & 1;
+        ++nz;
+        I->zl_age = 0;
+      }
+    }
+    if (nz > 0) {
+      int nmax = 2;
+      for (int a = 0; a < nz; ++a) nmax = std::max(nmax, b->inst[b->h_zl[2 * a]]->n);
+      CK(cudaMemcpyAsync(b->d_zl, b->h_zl, (size_t)2 * nz * sizeof(int), cudaMemcpyHostToDevice, b->stream));
+      const size_t zsm = (size_t)3 * nmax * sizeof(double);
+      CK(cudaFuncSetAttribute(zlanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
+      zlanczos_kernel<<<nz, PDSDP_ZL_THREADS, zsm, b->stream>>>(b->d_insts, b->d_zl);
+      CK(cudaGetLastError());
+      b->n_launch += 1;
+    }
+  }
   if (b->timing) CK(cudaEventRecord(b->tev[0], b->stream));
   if (!b->verify_residual) {
     int rc = launch_iterate(b, nact, lds, 0, K);
@@ -761,6 +796,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
                                      std::to_string(PDSDP_BMAX) + " holds (PDSDP_BMAX)");
     }
     if (steps_done) steps_done[a] = done;
+    b->inst[insts[a]]->zl_age += done;
     done_max = std::max(done_max, done);
   }
   if (b->timing && done_max > 0) {
