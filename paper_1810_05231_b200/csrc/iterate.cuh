@@ -31,10 +31,16 @@ namespace pdsdp {
 #define PDSDP_MMAX 48          // largest filter degree per pass (slow clustered columns after a rank doubling)
 #endif
 // largest amplification of a column's contamination the filter may cause:
-// CholQR2 re-orthonormalises blocks with condition up to ~1e8, so 1e6 keeps
-// a 100x margin (was 1e4)
+// CholQR2 re-orthonormalises blocks with condition up to ~1e8, so 1e5 keeps
+// a 1000x margin (1e4 .. 3e5 measured within 0.4% of each other on config
+// 2, 2% faster than 1e6: profiles/r01s4_spread_cap_sweep.txt)
 #ifndef PDSDP_SPREAD_CAP
-#define PDSDP_SPREAD_CAP 1e6
+#define PDSDP_SPREAD_CAP 1e5
+#endif
+// contamination assumed for the first pass of an iteration (its residuals
+// belong to the previous S): enters the spread cap only
+#ifndef PDSDP_STALE_EPS
+#define PDSDP_STALE_EPS 1e-3
 #endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
@@ -1324,7 +1330,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const double xnorm = kept_norm_w(s.theta, r, b);
       const Assess as = assess_w(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
       const bool stale = (pass == 0 && !rerun);   // residuals belong to the previous S
-      const double eps_rel = fmax(as.maxres, stale ? 1e-3 : 0.0);
+      const double eps_rel = fmax(as.maxres, stale ? PDSDP_STALE_EPS : 0.0);
       int mcap = PDSDP_MMAX;
       // leading pairs already converged to the kept tolerance: deflate them
       // and filter the rest of the block (a small spread admits the degree the

@@ -9,6 +9,15 @@
 #pragma once
 #include "common.cuh"
 
+// Jacobi rotation thresholds relative to ||A||_F: pairs whose Ritz values are
+// used (kept pairs and the certificate) and guard pairs (warm start only)
+#ifndef PDSDP_JAC_TOL_IMP
+#define PDSDP_JAC_TOL_IMP 1e-14
+#endif
+#ifndef PDSDP_JAC_TOL_GUARD
+#define PDSDP_JAC_TOL_GUARD 1e-8
+#endif
+
 namespace pdsdp {
 
 // In-place Cholesky G = L L^T (lower) of an SPD matrix scaled to unit
@@ -83,7 +92,7 @@ __device__ void jacobi_eig(double* A, double* Q, int b, int lds, double* cs, int
   double fro = 0.0;
   for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
   fro = sqrt(fro);
-  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
   if (tid == 0) sflag[0] = 0;
   if (b == 1) { __syncthreads(); return; }
   const int bb = b + (b & 1);
@@ -409,7 +418,7 @@ __device__ void jacobi_eig_1s(double* A, double* A2, double* Q, double* Q2, int 
   double fro = 0.0;
   for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
   fro = sqrt(fro);
-  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
   *Aout = A; *Qout = Q;
   if (tid == 0) sflag[0] = 0;
   if (b == 1) { __syncthreads(); return; }
@@ -625,7 +634,7 @@ __device__ void jacobi_eig2(double* A, double* A2, double* Q, double* Q2, int b,
   double fro = 0.0;
   for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
   fro = sqrt(fro);
-  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
   double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
   int sweeps = 0;
   if (b > 1) {
@@ -755,7 +764,7 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
   double fro = 0.0;
   for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
   fro = sqrt(fro);
-  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
   double* c0a = cs;                 // a0 per index
   double* c1a = cs + PDSDP_BMAX;    // a1 per index (signed)
   double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
@@ -881,7 +890,7 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
   double fro = 0.0;
   for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
   fro = sqrt(fro);
-  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
   double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
   const int ri = tid >> 3, cj = tid & 7, rstep = nt >> 3;
   int sweeps = 0;
@@ -1006,7 +1015,7 @@ __device__ void jacobi_eig2_warp(double* A, double* A2, double* Q, double* Q2, i
   }
   __syncwarp();
   const double fro = sqrt(f);
-  const double thr_imp = 1e-14 * fro, thr_guard = 1e-8 * fro;
+  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
   double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
   int sweeps = 0;
   if (b > 1) {
