@@ -254,7 +254,7 @@ def run_ours(args, rank, world, local_rank):
     t_it = it_ms * 1e-3
     mv = sum(x.eig_matvecs for x in outcomes) / max(1, it_tot)
     kb = min(r + 1, n)
-    b = min(n, 64, ((kb + max(4, kb // 4) + 3) // 4) * 4)
+    b = min(n, 64, ((kb + 1 + 1) // 2) * 2)   # block_for(): one guard column, rounded to 2
     ip, _, _ = prob.stacked_arrays()
     nnz, mp = int(ip[-1]), prob.m + prob.p
     B = 6551.7
@@ -280,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
             # launch = one iteration at the final rank (ncu --set full,
             # profiles/r01s3_iterate_kernel_ncu_raw_r20.txt; 2340096 at rank 10):
             # the iterate stays L2-resident, the kernel is latency-bound
-            "traffic": 2537728, "traffic_source": "profiles/r01s3_iterate_kernel_ncu_raw_r20.txt",
+            "traffic": 3010560, "traffic_source": "profiles/r01s4_iterate_kernel_ncu_raw_r20.csv",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs",
             "algorithmic_bytes_per_iteration": algo_bytes, "algorithmic_flops_per_iteration": algo_flops,
             "basis": f"SURVEY 8(d) dense formulation, n={n}, b={b}, p_pass={mv:.2f}, r={r}",

@@ -25,7 +25,31 @@
 #define PDSDP_KMAX 64          // iterations per pdsdp_iterate_many call
 #define PDSDP_NDMAX 2          // dense rank-one constraint rows handled as vectors
 
+// Eigen block for k = r+1 wanted pairs: k plus max(GUARD_MIN, k / GUARD_DIV)
+// guard columns, rounded up to BLOCK_ROUND, <= min(BMAX, n).  One guard
+// (b = 12 at r = 10, 22 at r = 20) measured 11% faster on config 2 than
+// max(4, k/4) (16 / 28): the per-column cost of every operator step and
+// Rayleigh-Ritz pass outweighs the slower convergence (profiles/r01s4_block_sweep.txt).
+#ifndef PDSDP_GUARD_MIN
+#define PDSDP_GUARD_MIN 1
+#endif
+#ifndef PDSDP_GUARD_DIV
+#define PDSDP_GUARD_DIV 100
+#endif
+#ifndef PDSDP_BLOCK_ROUND
+#define PDSDP_BLOCK_ROUND 2
+#endif
+
 namespace pdsdp {
+
+__host__ __device__ inline int block_for(int k, int n) {
+  int g = k / PDSDP_GUARD_DIV;
+  if (g < PDSDP_GUARD_MIN) g = PDSDP_GUARD_MIN;
+  int b = (k + g + PDSDP_BLOCK_ROUND - 1) / PDSDP_BLOCK_ROUND * PDSDP_BLOCK_ROUND;
+  if (b > PDSDP_BMAX) b = PDSDP_BMAX;
+  if (b > n) b = n;
+  return b;
+}
 
 struct State {
   int b;            // current eigen block size

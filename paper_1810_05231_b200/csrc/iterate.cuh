@@ -1116,15 +1116,7 @@ inline size_t iterate_smem_bytes(int lds, int zcap, int ycap, int owncap, int nl
          (size_t)(3 * PDSDP_BMAX + 8 + 20 + zcap + (owncap ? nlmax + 2 : 0)) * sizeof(int) + 64;
 }
 
-__device__ int choose_block(int k, int n) {
-  int g = k / 4;
-  if (g < 4) g = 4;
-  int b = k + g;
-  b = (b + 3) & ~3;
-  if (b > PDSDP_BMAX) b = PDSDP_BMAX;
-  if (b > n) b = n;
-  return b;
-}
+__device__ int choose_block(int k, int n) { return block_for(k, n); }
 
 __global__ void __launch_bounds__(PDSDP_NTHR, 1)
 lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,

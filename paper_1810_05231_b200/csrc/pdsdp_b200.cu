@@ -727,8 +727,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
       b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_ERR] = 0.0;
     }
     b->h_active[a] = k;
-    const int g = std::max(kk / 4, 4);
-    const int bb = std::min(std::min((kk + g + 3) & ~3, PDSDP_BMAX), I->n);
+    const int bb = block_for(kk, I->n);
     I->bmax = std::max(I->bmax, bb);
     lds = std::max(lds, I->bmax);
     maxr = std::max(maxr, (int)rank[a]);
