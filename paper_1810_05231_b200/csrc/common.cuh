@@ -20,6 +20,9 @@
 #ifndef PDSDP_NTHR
 #define PDSDP_NTHR 384         // threads per CTA of the cluster kernel (168 registers each)
 #endif
+#ifndef PDSDP_CTA_ROWS
+#define PDSDP_CTA_ROWS 128     // cluster size: smallest power of 2 with C * CTA_ROWS >= n (C <= 16)
+#endif
 #define PDSDP_RED_MAX (2 * PDSDP_BMAX * PDSDP_BMAX + 64)
 #define PDSDP_OUT_LEN 16       // doubles per instance and step in the host-mapped output
 #define PDSDP_KMAX 64          // iterations per pdsdp_iterate_many call

@@ -523,7 +523,7 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
   int maxn = 0;
   for (int k = 0; k < count; ++k) maxn = std::max(maxn, (int)problems[k].n);
   int C = 1;
-  while (C < 16 && C * 128 < maxn) C <<= 1;
+  while (C < 16 && C * PDSDP_CTA_ROWS < maxn) C <<= 1;
   b->C = C;
   int lds = std::min(maxn, PDSDP_BMAX);
   b->lds = lds < 4 ? 4 : lds;
