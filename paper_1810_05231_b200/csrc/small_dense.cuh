@@ -720,6 +720,71 @@ __device__ void jacobi_eig2(double* A, double* A2, double* Q, double* Q2, int b,
 }
 
 
+// Second-order finish of a nearly diagonal A, in place of further Jacobi
+// sweeps: with every off-diagonal entry small against its diagonal gap,
+//   U = I + K,  K_ij = a_ij / (a_jj - a_ii)  (i != j),  columns normalised,
+//   Q <- Q U,   A <- diag(a_jj + sum_i a_ij K_ij),
+// leaves eigenvector errors O(a_ij^2 / gap) (first-order perturbation theory;
+// U is orthonormal to O(K^2)).  Applied only when that is below a tenth of
+// the pair's rotation threshold, so the result meets the same tolerance as
+// the sweeps it replaces; otherwise returns false and changes nothing.  Three
+// barriers instead of b - 1 rounds of two.  An / Qn receive the new A / Q.
+#ifndef PDSDP_JAC_PERTURB
+#define PDSDP_JAC_PERTURB 1
+#endif
+__device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double* An, double* Qn, int b, int lds,
+                                      int nimp, double thr_imp, double thr_guard, double* cs) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int bad = 0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e - (e / b) * b;
+    double k = 0.0;
+    if (i != j) {
+      const int lo_ = min(i, j), hi_ = max(i, j);
+      const double a = Ac[lo_ * lds + hi_];
+      const double gap = Ac[j * lds + j] - Ac[i * lds + i];
+      const double thr = (lo_ < nimp) ? thr_imp : thr_guard;
+      if (fabs(a) <= 1e-3 * fabs(gap)) {
+        k = a / gap;
+        if (fabs(a) > thr && !(a * a <= 0.1 * thr * fabs(gap))) bad = 1;
+      } else if (fabs(a) > thr) {
+        bad = 1;
+      }
+    }
+    An[i * lds + j] = k;
+  }
+  if (__syncthreads_or(bad)) return false;
+  double* nrm = cs;
+  double* lam = cs + PDSDP_BMAX;
+  if (tid < b) {
+    const int j = tid;
+    double s2 = 1.0, l = Ac[j * lds + j];
+    for (int i = 0; i < b; ++i) {
+      if (i == j) continue;
+      const double k = An[i * lds + j];
+      s2 = fma(k, k, s2);
+      l = fma(k, Ac[min(i, j) * lds + max(i, j)], l);
+    }
+    nrm[j] = 1.0 / sqrt(s2);
+    lam[j] = l;
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e - (e / b) * b;
+    double acc = Qc[i * lds + j];
+    for (int l = 0; l < b; ++l)
+      if (l != j) acc = fma(Qc[i * lds + l], An[l * lds + j], acc);
+    Qn[i * lds + j] = acc * nrm[j];
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e - (e / b) * b;
+    An[i * lds + j] = (i == j) ? lam[i] : 0.0;
+  }
+  __syncthreads();
+  return true;
+}
+
 // Parallel-order cyclic Jacobi for the b x b (b <= 64) projected matrix,
 // block-wide.  Same contract and rotations as jacobi_eig2, restructured for
 // latency: per round, thread p (< b) writes the row coefficients (a0, a1) of
@@ -779,6 +844,11 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
         for (int j = cj; j < b; j += 8)
           if (j > i && fabs(Ac[i * lds + j]) > ((i < nimp) ? thr_imp : thr_guard)) need = 1;
       if (!__syncthreads_or(need)) break;
+      if (PDSDP_JAC_PERTURB && jacobi_perturb_finish(Ac, Qc, An, Qn, b, lds, nimp, thr_imp, thr_guard, cs)) {
+        double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp;
+        ++sweeps;
+        break;
+      }
       for (int t = 0; t < R; ++t) {
         Ac = as_shared(Ac); An = as_shared(An); Qc = as_shared(Qc); Qn = as_shared(Qn);
         const int* pt = tab + t * bb;
@@ -901,6 +971,11 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
         for (int j = cj; j < b; j += 8)
           if (j > i && fabs(Ac[i * lds + j]) > ((i < nimp) ? thr_imp : thr_guard)) need = 1;
       if (!__syncthreads_or(need)) break;
+      if (PDSDP_JAC_PERTURB && jacobi_perturb_finish(Ac, Qc, An, Qn, b, lds, nimp, thr_imp, thr_guard, cs)) {
+        double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp;
+        ++sweeps;
+        break;
+      }
       for (int t = 0; t < R; ++t) {
         Ac = as_shared(Ac); An = as_shared(An); Qc = as_shared(Qc); Qn = as_shared(Qn);
         // (1) rotation of pair k (round-robin order of jacobi_eig3)
