@@ -64,7 +64,7 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
     // remaining effect on X+: |dtheta| <= ri plus rotation ~ 2 theta ri / gap (Davis-Kahan)
     const double thr = (r < b) ? theta[r] : -1.0e308;
     const double gap = th - thr;
-    const double impact = ri + 2.0 * fmax(th, 0.0) * fmin(1.0, ri / fmax(gap, 1e-300));
+    const double impact = ri + 2.0 * fmax(th, 0.0) * fmin(1.0, ri * fast_rcp(fmax(gap, 1e-300)));
     return impact <= PDSDP_TOL_X * xnorm;
   }
   // cert_tol < 0: sentinel column of an effective-rank block -- it must be
@@ -90,6 +90,7 @@ struct Sm {
   ShPtr<int> perm, pq, flag;
   int lds;
   int gnext[17];               // operator step: next row group's first CTA after group g (thread 0 plans it)
+  int gplan;                   // operand row stride the gnext plan was made for (-1: none)
 };
 
 __device__ __forceinline__ Sm& s_mut(const Sm& s) { return const_cast<Sm&>(s); }
@@ -720,7 +721,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
   }
   gram_ready = false;
-  if (tid == 0) {   // row groups that fit the staging buffer (published by the barrier below)
+  if (tid == 0 && s.gplan != ys_) {   // row groups that fit the staging buffer (published by the barrier below)
+    s_mut(s).gplan = ys_;
     const int rc = s.ycap / ys_;
     for (int g0 = 0; g0 < x.C;) {
       int g1 = g0 + 1;
@@ -987,8 +989,10 @@ __device__ Assess assess_w(const double* theta, const double* res, int r, int b,
                            double xnorm, double cert_tol) {
   Assess a{-1, false, false, 1.0, 0.0};
   const int lane = threadIdx.x & 31;
-  const double inv_scale = 1.0 / scale;
-  const double inv_tk = 1.0 / fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
+  // reciprocals by rcp.approx + two Newton steps: the software FP64 division
+  // sits on the critical path of every pass (planning needs a few digits)
+  const double inv_scale = fast_rcp(scale);
+  const double inv_tk = fast_rcp(fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
   int last = -1, cert = 0;
   double mr = 0.0, rk = 1.0;
   for (int i = lane; i < k; i += 32) {
@@ -1047,14 +1051,16 @@ __device__ int cheb_plan(const double* theta, int a1, double lo, double top, dou
   c_ = 0.5 * (cut + lo_);
   if (e_ < 1e-14 * scale) e_ = 1e-14 * scale;
   if (top - c_ <= e_) top = c_ + 1.0001 * e_;
-  s_ = e_ / (top - c_);
-  const double ts = (slow - c_) / e_;
+  s_ = e_ * fast_rcp(top - c_);
+  const double ie = fast_rcp(e_);
+  const double ts = (slow - c_) * ie;
   const double at = (ts > 1.0 + 1e-6) ? plan_acosh(ts) : 0.0;
-  mm = (at > 0.0) ? (int)ceil(plan_acosh(fmax(rho, 1.0)) / at) + 1 : 8;
-  const double tb = (theta[a1 - 1] - c_) / e_;
-  const double spread = plan_acosh(fmax((top - c_) / e_, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? plan_acosh(tb) : 0.0);
+  mm = (at > 0.0) ? (int)ceilf(__fdividef((float)plan_acosh(fmax(rho, 1.0)), (float)at)) + 1 : 8;
+  const double tb = (theta[a1 - 1] - c_) * ie;
+  const double spread = plan_acosh(fmax((top - c_) * ie, 1.0 + 1e-6)) - ((tb > 1.0 + 1e-6) ? plan_acosh(tb) : 0.0);
   int mcap = PDSDP_MMAX;
-  if (spread > 1e-3) mcap = (int)fmin((double)PDSDP_MMAX, floor(plan_log(PDSDP_SPREAD_CAP / fmin(fmax(eps_rel, 1e-16), 1.0)) / spread));
+  if (spread > 1e-3)
+    mcap = (int)fminf((float)PDSDP_MMAX, floorf(__fdividef((float)plan_log(PDSDP_SPREAD_CAP * fast_rcp(fmin(fmax(eps_rel, 1e-16), 1.0))), (float)spread)));
   if (mcap < 2) mcap = 2;
   return mcap;
 }
@@ -1215,6 +1221,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     for (int lr = tid; lr <= x.r1 - x.r0; lr += blockDim.x) s.szp[lr] = d.zptr[x.r0 + lr];
     for (int c = tid; c <= x.C; c += blockDim.x) s.gb[c] = (int)(((long long)n * c) / x.C);
   }
+  if (tid == 0) s.gplan = -1;   // the operator step plans its row groups per operand stride
   __syncthreads();
 
   // Persistent over the chunk: one launch runs the chunk's iterations until
@@ -1399,7 +1406,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       for (int j = 1; j <= m; ++j) {
         int io = fre((j - 1) % 3);
         if (j == 1) {
-          const double ca = sig1 / fe, cb = -fc * sig1 / fe;
+          const double ife = fast_rcp(fe), ca = sig1 * ife, cb = -fc * sig1 * ife;
           if (av_valid) {
             for (int it = tid; it < nl * bc; it += blockDim.x) {
               const int lr = it / bc, jj = it - lr * bc, jc = c0 + jj;
@@ -1417,8 +1424,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             ++matvecs;
           }
         } else {
-          const double sn = 1.0 / (2.0 / sig1 - sg);
-          const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
+          // recurrence coefficients by rcp.approx + Newton (identical in every CTA)
+          const double sn = fast_rcp(2.0 * fast_rcp(sig1) - sg), ife = fast_rcp(fe);
+          const double ca = 2.0 * sn * ife, cb = -2.0 * sn * fc * ife, cd = -sg * sn;
           operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase,
                             gram_ready, j < m);
           ++matvecs;
@@ -1442,7 +1450,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       for (int j = 1; j <= m; ++j) {
         int io = fre((j - 1) % 3);
         if (j == 1) {
-          const double ca = sig1 / fe, cb = -fc * sig1 / fe;
+          const double ife = fast_rcp(fe), ca = sig1 * ife, cb = -fc * sig1 * ife;
           if (av_valid) {
             for (int it = tid; it < (x.r1 - x.r0) * bc; it += blockDim.x) {
               const size_t o = (size_t)(x.r0 + it / bc) * ld + c0 + it % bc;
@@ -1453,8 +1461,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             ++matvecs;
           }
         } else {
-          const double sn = 1.0 / (2.0 / sig1 - sg);
-          const double ca = 2.0 * sn / fe, cb = -2.0 * sn * fc / fe, cd = -sg * sn;
+          // recurrence coefficients by rcp.approx + Newton (identical in every CTA)
+          const double sn = fast_rcp(2.0 * fast_rcp(sig1) - sg), ife = fast_rcp(fe);
+          const double ca = 2.0 * sn * ife, cb = -2.0 * sn * fc * ife, cd = -sg * sn;
           operator_step(d, x, s, zv, buf(iy), buf(iyp < 0 ? 0 : iyp), buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf);
           ++matvecs;
           sg = sn;
@@ -1733,11 +1742,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         if (m > 0 && pass == 0) {
           double sl = 1.0e300;
           const double tol = fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
-          const double ife = 1.0 / fe;
+          const double ife = fast_rcp(fe);
           for (int i = (tid & 31); i < r && i < b; i += 32) {
             const double t = (s.theta[i] - fc) * ife;
             if (t <= 1.0 + 1e-6) { sl = 0.0; continue; }
-            sl = fmin(sl, plan_log(tol / fmax(s.res[i], 1e-300)) / plan_acosh(t));
+            sl = fmin(sl, (double)__fdividef((float)plan_log(tol * fast_rcp(fmax(s.res[i], 1e-300))), (float)plan_acosh(t)));
           }
           sl = -warp_max(-sl);
           slack = (sl > 0.0 && sl < 64.0) ? (int)floor(sl) : (sl >= 64.0 ? 64 : 0);
