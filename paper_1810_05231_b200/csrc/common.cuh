@@ -157,6 +157,9 @@ struct Inst {
   const int* tptr;     // [nz+1] contributors of M^T y to the slot
   const int* trow;     // constraint row of each contributor
   const double* tcoef; // scatter coefficient (packed value / s, s = 1 or sqrt 2)
+  const int* dptr;     // [n+1] slots with contributors ("dynamic") in rows < i
+  const int* dslot;    // dynamic slot indices, row order (the others hold C for ever)
+  const double* zsabs; // [n] sum over the row's static slots of |C|
   double* zbuf0;       // [nz] Z = C + M^T y for y in ybuf0
   double* zbuf1;       // [nz] ... for y in ybuf1
   const int* aptr;     // [mp+1] constraint rows in dense coordinates

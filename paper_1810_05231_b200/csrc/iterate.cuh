@@ -1890,9 +1890,12 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // the slot tables are read-only for the kernel's lifetime (__ldg: the
     // loads may move ahead of the stores below); y+ / dy come from other
     // CTAs of the cluster (coherent L2 loads)
-    const int e0 = d.zptr[x.r0], e1 = d.zptr[x.r1];
+    // only the slots M^T y touches change (the others hold C in both Z
+    // buffers and in the staged copy)
+    const int k0 = __ldg(d.dptr + x.r0), k1 = __ldg(d.dptr + x.r1);
     double* zsm = s.zstaged ? const_cast<double*>(static_cast<const double*>(s.zvs)) - s.zoff : nullptr;   // Z_k is dead: keep Z_k+1 here too
-    for (int e = e0 + tid; e < e1; e += blockDim.x) {
+    for (int kk = k0 + tid; kk < k1; kk += blockDim.x) {
+      const int e = __ldg(d.dslot + kk);
       double z = __ldg(d.cval + e), a = 0.0;
       const int t0 = __ldg(d.tptr + e), t1 = __ldg(d.tptr + e + 1);
       for (int t = t0; t < t1; ++t) {
@@ -1918,8 +1921,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   {
     const double* zsrc = s.zstaged ? (const double*)s.zvs - s.zoff : zvn;
     for (int rho = x.r0 + tid; rho < x.r1; rho += blockDim.x) {
-      double sacc = 0.0;
-      for (int e = __ldg(d.zptr + rho); e < __ldg(d.zptr + rho + 1); ++e) sacc += fabs(zsrc[e]);
+      double sacc = __ldg(d.zsabs + rho);
+      for (int kk = __ldg(d.dptr + rho); kk < __ldg(d.dptr + rho + 1); ++kk) sacc += fabs(zsrc[__ldg(d.dslot + kk)]);
       gmax = fmax(gmax, sacc);
     }
   }

@@ -61,8 +61,8 @@ struct Instance {
   int group = 1;
   int ntile = 0;
   // host copies of the re-indexed problem
-  std::vector<int> zptr, zcol, zrow, tptr, trow, aptr, ai, aj;
-  std::vector<double> cval, tcoef, ag, bv, hv;
+  std::vector<int> zptr, zcol, zrow, tptr, trow, aptr, ai, aj, dptr, dslot;
+  std::vector<double> cval, tcoef, ag, bv, hv, zsabs;
   // dense rank-one constraint rows  D_r = sig u u^T  (kept out of the CSR)
   int nd = 0;
   int drow[PDSDP_NDMAX] = {0};
@@ -277,6 +277,17 @@ int build_instance(const pdsdp_problem& pr, Instance& I) {
     int o = I.tptr[s];
     for (int c = ccount[u]; c < ccount[u + 1]; ++c, ++o) { I.trow[o] = crow[c]; I.tcoef[o] = ccoef[c]; }
   }
+  // slots touched by M^T y, per row; the others keep their C value in both Z buffers
+  I.dptr.assign(n + 1, 0);
+  I.dslot.clear();
+  I.zsabs.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    for (long long s = I.zptr[i]; s < I.zptr[i + 1]; ++s) {
+      if (I.tptr[s + 1] > I.tptr[s]) I.dslot.push_back((int)s);
+      else I.zsabs[i] += std::fabs(I.cval[s]);
+    }
+    I.dptr[i + 1] = (int)I.dslot.size();
+  }
   // ---- constraint rows in dense coordinates (dense rank-one rows left empty) ----
   I.aptr.assign(mp + 1, 0);
   I.ai.clear(); I.aj.clear(); I.ag.clear();
@@ -349,6 +360,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   auto add = [&](size_t b) { bytes += ((b + 16) + 255) & ~size_t(255); };
   add((I.n + 1) * 4); add(I.nz * 4); add(I.nz * 4); add(I.nz * 8); add((I.nz + 1) * 4);
   add(I.trow.size() * 4 + 4); add(I.tcoef.size() * 8 + 8); add(I.nz * 8); add(I.nz * 8);
+  add((I.n + 1) * 4); add(I.dslot.size() * 4 + 4); add(I.n * 8 + 8);
   add((I.mp + 1) * 4); add(I.ai.size() * 4 + 4); add(I.aj.size() * 4 + 4); add(I.ag.size() * 8 + 8);
   add((C + 1) * 4); add(I.bv.size() * 8 + 8); add(I.hv.size() * 8 + 8);
   for (int k = 0; k < 6; ++k) add(nld * 8);
@@ -385,6 +397,13 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   if ((rc = upload(a, trow, I.trow))) return rc;
   if ((rc = upload(a, tcoef, I.tcoef))) return rc;
   d.zptr = zptr; d.zcol = zcol; d.zrow = zrow; d.cval = cval; d.tptr = tptr; d.trow = trow; d.tcoef = tcoef;
+  {
+    int *dp, *ds; double* za;
+    if ((rc = upload(a, dp, I.dptr))) return rc;
+    if ((rc = upload(a, ds, I.dslot))) return rc;
+    if ((rc = upload(a, za, I.zsabs))) return rc;
+    d.dptr = dp; d.dslot = ds; d.zsabs = za;
+  }
   d.zbuf0 = a.take<double>(I.nz + 1);
   d.zbuf1 = a.take<double>(I.nz + 1);
   int *aptr, *ai, *aj; double* ag;
