@@ -171,7 +171,9 @@ __device__ void gram_partial(const double* __restrict__ A, int na, const double*
   }
 }
 
+#ifndef PDSDP_GRAM_SCR
 #define PDSDP_GRAM_SCR 2048     // doubles of smem for the cross-warp Gram reduction
+#endif
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -618,13 +620,13 @@ __device__ __forceinline__ bool own_lock_sm(int rFx, int nlock, int sl) { return
 // a thread run interleaved (independent chains) and the next slot's column
 // is loaded before the current slot's products, so a thread keeps several
 // shared-memory round trips in flight.  SZ: Z slots staged in shared memory.
-template <bool SZ>
+template <bool SZ, int NI>
 __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const double* __restrict__ zval,
                                            const double* ys, int R0, int R1, int cq, int ys_,
-                                           int (&ep)[PDSDP_OWN_ITEMS], const int (&ee)[PDSDP_OWN_ITEMS],
-                                           double (&zacc)[PDSDP_OWN_ITEMS][4]) {
+                                           int (&ep)[NI], const int (&ee)[NI],
+                                           double (&zacc)[NI][4]) {
   constexpr int BIG = 0x7fffffff;
-  int q[PDSDP_OWN_ITEMS];
+  int q[NI];
   // chunks 4..7 of a quarter warp read their upper 16 bytes first: the eight
   // first loads of a row's chunks then fall in eight distinct bank groups
   // (zacc holds the two halves swapped for those threads; the caller undoes it)
@@ -632,7 +634,7 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
   const double* yb = ys + 4 * cq + 2 * sw - (size_t)R0 * ys_;
   const int o2 = 2 - 4 * sw;
 #pragma unroll
-  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) q[u] = (ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
+  for (int u = 0; u < NI; ++u) q[u] = (ep[u] < ee[u]) ? zcol[ep[u]] : BIG;
   if (SZ) {
     // Z slots and operand rows in shared memory: 32-bit shared addresses
     // kept in registers (the generic form recomputed 64-bit pointers per slot)
@@ -642,10 +644,10 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
     while (true) {
       bool any = false;
 #pragma unroll
-      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) any |= q[u] < R1;
+      for (int u = 0; u < NI; ++u) any |= q[u] < R1;
       if (!any) break;
 #pragma unroll
-      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      for (int u = 0; u < NI; ++u) {
         if (q[u] < R1) {
           const int e = ep[u];
           const unsigned a = yb_a + (unsigned)q[u] * rowb;
@@ -667,10 +669,10 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
   while (true) {
     bool any = false;
 #pragma unroll
-    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) any |= q[u] < R1;
+    for (int u = 0; u < NI; ++u) any |= q[u] < R1;
     if (!any) break;
 #pragma unroll
-    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+    for (int u = 0; u < NI; ++u) {
       if (q[u] < R1) {
         const int e = ep[u];
         const double zv_ = zval[e];
@@ -685,6 +687,7 @@ __device__ __forceinline__ void own_gather(const int* __restrict__ zcol, const d
   }
 }
 
+template <int NI>
 __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const Sm& s, const double* zv,
                                                   double* out, int c0, int bc, int rF, int nlock,
                                                   double ca, double cb, double cd, Prof& pf,
@@ -697,7 +700,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const double* Ycur = d.Yc + (size_t)ycp * nld;
   double* Ynxt = d.Yc + (size_t)(ycp ^ 1) * nld;
   // work items: (own row, 4-column chunk).  Thread t takes chunk t % nch of
-  // rows t / nch + u * rps (u < PDSDP_OWN_ITEMS): its items share the column
+  // rows t / nch + u * rps (u < NI): its items share the column
   // chunk, so the dense epilogue loads each T entry once for all of them
   const int rps = blockDim.x / nch, cq = tid % nch, lr0 = tid / nch;
   const int tstr = (bc + 1) & ~1;   // row stride of T in this step (even)
@@ -742,10 +745,10 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
   const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
   const int zoff = s.zstaged ? s.zoff : 0;
-  double zacc[PDSDP_OWN_ITEMS][4];
-  int ep[PDSDP_OWN_ITEMS], ee[PDSDP_OWN_ITEMS];
+  double zacc[NI][4];
+  int ep[NI], ee[NI];
 #pragma unroll
-  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+  for (int u = 0; u < NI; ++u) {
     const int lr = lr0 + u * rps;
     const bool ok = tact && lr < nl;
     ep[u] = s.szp[ok ? lr : 0] - zoff;
@@ -791,8 +794,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     __syncthreads();
     prof_mark(pf, 14);
-    if (s.zstaged) own_gather<true>(s.zc, s.zvs, ys, R0, R1, cq, ys_, ep, ee, zacc);
-    else own_gather<false>(zcol, zval, ys, R0, R1, cq, ys_, ep, ee, zacc);
+    if (s.zstaged) own_gather<true, NI>(s.zc, s.zvs, ys, R0, R1, cq, ys_, ep, ee, zacc);
+    else own_gather<false, NI>(zcol, zval, ys, R0, R1, cq, ys_, ep, ee, zacc);
     g0 = g1;
     prof_tick(pf, 22);
     if (g0 < C) cg::this_cluster().sync();
@@ -800,7 +803,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   }
   if ((cq >> 2) & 1) {        // own_gather kept this thread's chunk halves swapped
 #pragma unroll
-    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+    for (int u = 0; u < NI; ++u) {
       double t = zacc[u][0]; zacc[u][0] = zacc[u][2]; zacc[u][2] = t;
       t = zacc[u][1]; zacc[u][1] = zacc[u][3]; zacc[u][3] = t;
     }
@@ -812,15 +815,15 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const int nsf = own_lock_sm(rF, nlock, sl) ? rF + nlock : rF;
   const int nglb = nsf == rF ? nlock : 0;
   // dense part [F | V_lock] T of all items: T entries loaded once per thread
-  double w[PDSDP_OWN_ITEMS][4];
+  double w[NI][4];
 #pragma unroll
-  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u)
+  for (int u = 0; u < NI; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) w[u][v] = 0.0;
   if (tact) {
-    const double* Fr[PDSDP_OWN_ITEMS];
+    const double* Fr[NI];
 #pragma unroll
-    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+    for (int u = 0; u < NI; ++u) {
       const int lr = lr0 + u * rps;
       Fr[u] = s.SF + (size_t)(lr < nl ? lr : 0) * sl;
     }
@@ -834,7 +837,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       const double2 ta = *reinterpret_cast<const double2*>(Tc + l * tstr);
       const double2 tb = *reinterpret_cast<const double2*>(Tc + l * tstr + o2);
 #pragma unroll
-      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      for (int u = 0; u < NI; ++u) {
         const double f = Fr[u][l];
         w[u][0] = fma(f, ta.x, w[u][0]); w[u][1] = fma(f, ta.y, w[u][1]);
         w[u][2] = fma(f, tb.x, w[u][2]); w[u][3] = fma(f, tb.y, w[u][3]);
@@ -842,14 +845,14 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     }
     if (sw) {
 #pragma unroll
-      for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+      for (int u = 0; u < NI; ++u) {
         double t = w[u][0]; w[u][0] = w[u][2]; w[u][2] = t;
         t = w[u][1]; w[u][1] = w[u][3]; w[u][3] = t;
       }
     }
   }
 #pragma unroll
-  for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+  for (int u = 0; u < NI; ++u) {
     const int lr = lr0 + u * rps;
     if (!tact || lr >= nl) break;
     const double* Vr = d.V + (size_t)(x.r0 + lr) * ld;
@@ -898,7 +901,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     // of Y_{j+1} (the staging buffer is idle until the next cluster barrier)
     double* yo = s.ys;
 #pragma unroll
-    for (int u = 0; u < PDSDP_OWN_ITEMS; ++u) {
+    for (int u = 0; u < NI; ++u) {
       const int lr = lr0 + u * rps;
       if (!tact || lr >= nl) break;
 #pragma unroll
@@ -916,6 +919,22 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   }
   prof_tick(pf, 26);
   ycp ^= 1;
+}
+
+// Items per thread for this step: two when they cover the CTA's rows (fewer
+// interleaved gather chains per thread, config 2: 3% faster), else
+// PDSDP_OWN_ITEMS (the launch checked that those cover them).
+__device__ __forceinline__ void operator_step_own_any(const Inst& d, Cta& x, const Sm& s, const double* zv,
+                                                      double* out, int c0, int bc, int rF, int nlock,
+                                                      double ca, double cb, double cd, Prof& pf,
+                                                      int& ycp, unsigned long long* mbar, unsigned& mphase,
+                                                      bool& gram_ready, bool gram_next) {
+  const int rps = blockDim.x / (own_stride(bc) >> 2);
+  if (PDSDP_OWN_ITEMS > 2 && x.r1 - x.r0 <= 2 * rps)
+    operator_step_own<2>(d, x, s, zv, out, c0, bc, rF, nlock, ca, cb, cd, pf, ycp, mbar, mphase, gram_ready, gram_next);
+  else
+    operator_step_own<PDSDP_OWN_ITEMS>(d, x, s, zv, out, c0, bc, rF, nlock, ca, cb, cd, pf, ycp, mbar, mphase, gram_ready,
+                                       gram_next);
 }
 
 // Convergence state of the Ritz block (identical in every thread).
@@ -1419,7 +1438,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
             __syncthreads();
             ycp = 1;
           } else {
-            operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase,
+            operator_step_own_any(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, 0.0, pf, ycp, &mbar_sm, mphase,
                               gram_ready, j < m);
             ++matvecs;
           }
@@ -1427,7 +1446,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           // recurrence coefficients by rcp.approx + Newton (identical in every CTA)
           const double sn = fast_rcp(2.0 * fast_rcp(sig1) - sg), ife = fast_rcp(fe);
           const double ca = 2.0 * sn * ife, cb = -2.0 * sn * fc * ife, cd = -sg * sn;
-          operator_step_own(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase,
+          operator_step_own_any(d, x, s, zv, buf(io), c0, bc, rFx, nlock, ca, cb, cd, pf, ycp, &mbar_sm, mphase,
                             gram_ready, j < m);
           ++matvecs;
           sg = sn;
@@ -1504,7 +1523,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       gram_mma2<true, true>(yo, bcp, b, yo, bcp, b, 0, nl, red_slot(d, x, x.c) + rFx * b, s.gsc);
       int ycp_rr = 0;
       bool gr = false;
-      operator_step_own(d, x, s, zv, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0, pf, ycp_rr, &mbar_sm, mphase, gr, false);
+      operator_step_own_any(d, x, s, zv, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0, pf, ycp_rr, &mbar_sm, mphase, gr, false);
       __syncthreads();
       Cta xp = x;
       xp.par ^= 1;    // the step's reduction slot
