@@ -930,7 +930,9 @@ __device__ __forceinline__ void operator_step_own_any(const Inst& d, Cta& x, con
                                                       int& ycp, unsigned long long* mbar, unsigned& mphase,
                                                       bool& gram_ready, bool gram_next) {
   const int rps = blockDim.x / (own_stride(bc) >> 2);
-  if (PDSDP_OWN_ITEMS > 2 && x.r1 - x.r0 <= 2 * rps)
+  if (x.r1 - x.r0 <= rps)
+    operator_step_own<1>(d, x, s, zv, out, c0, bc, rF, nlock, ca, cb, cd, pf, ycp, mbar, mphase, gram_ready, gram_next);
+  else if (PDSDP_OWN_ITEMS > 2 && x.r1 - x.r0 <= 2 * rps)
     operator_step_own<2>(d, x, s, zv, out, c0, bc, rF, nlock, ca, cb, cd, pf, ycp, mbar, mphase, gram_ready, gram_next);
   else
     operator_step_own<PDSDP_OWN_ITEMS>(d, x, s, zv, out, c0, bc, rF, nlock, ca, cb, cd, pf, ycp, mbar, mphase, gram_ready,
