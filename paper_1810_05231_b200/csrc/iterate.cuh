@@ -471,6 +471,10 @@ __device__ void rot_mma(const double* __restrict__ In, int ldi, const double* __
                         const double* __restrict__ Msm, int lds, double* __restrict__ out, int ldo,
                         double* __restrict__ out2, int ldo2, int nl, int b, const double* __restrict__ th,
                         double* __restrict__ gout, double* __restrict__ scr) {
+  // In, In2 and Msm always lie in this CTA's shared memory: LDS, not generic loads
+  In = as_shared(In);
+  if (In2) In2 = as_shared(In2);
+  Msm = as_shared(Msm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int nw = blockDim.x >> 5;
   const int mt = (nl + 7) >> 3, ntl = (b + 7) >> 3;   // ntl <= 8
