@@ -83,6 +83,23 @@ def test_aproj_random_vs_oracle(rng):
         assert lam == pytest.approx(lr, rel=1e-8)
 
 
+def test_aproj_clustered_spectrum_vs_oracle(rng):
+    """Repeated and nearly repeated kept eigenvalues (the Jacobi pairs with
+    ~zero gap must take the rotation path, not the second-order finish) and a
+    negative tail; X+ is basis-independent within each cluster."""
+    for n, r in ((64, 6), (200, 10), (400, 21)):
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = -rng.random(n)
+        top = np.concatenate([[9.0, 9.0, 9.0 * (1 + 1e-9), 4.0, 4.0 + 1e-7, 2.0], 1.0 + rng.random(r)])[:r]
+        lam[:r] = top
+        D = (Q * lam) @ Q.T
+        S = orc.pack(0.5 * (D + D.T))
+        P, lm = pk.aproj_psd(pk.SymMatrix(n, S), r)
+        Pr, lr = orc.aproj_psd(S, n, r)
+        assert rel(P.data, Pr) <= ITER_TOL
+        assert lm == pytest.approx(lr, rel=1e-8, abs=1e-10)
+
+
 # ---------------------------------------------------------------- full solves
 
 @pytest.mark.parametrize("ci", range(5))
