@@ -42,6 +42,9 @@ namespace pdsdp {
 #ifndef PDSDP_STALE_EPS
 #define PDSDP_STALE_EPS 1e-3
 #endif
+#ifndef PDSDP_ONEPASS_RR
+#define PDSDP_ONEPASS_RR 1
+#endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
 #endif
@@ -1563,6 +1566,33 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     prof_mark(pf, 8);
     ++matvecs;
+    const int nlr = x.r1 - x.r0;
+    const bool rsm = 3 * nlmax * b <= ycap;
+    double* S0 = s.A + 4 * (size_t)lcap * lds;
+    double* S1 = S0 + (size_t)nlr * b;
+    double* S2 = S1 + (size_t)nlr * b;
+    // one-pass Rayleigh-Ritz when the filtered block is already well
+    // conditioned: D G1 D within 0.5/b of identity entrywise (cond <= 3 by
+    // Gershgorin), so the pairs of (Y^T S Y, Y^T Y) through L1 are as accurate
+    // as CholQR2's, and V = Y D L1^-T Q -- the rotations Y M1, W M1 and the
+    // second Gram are skipped
+    bool onep = false;
+#if PDSDP_ONEPASS_RR
+    if (rsm) {
+      for (int i = tid; i < b; i += blockDim.x) {
+        const double g = s.A[i * lds + i];
+        s.dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
+      }
+      __syncthreads();
+      const double eta = 0.5 / b;
+      int big = 0;
+      for (int e = tid; e < b * b; e += blockDim.x) {
+        const int i = e / b, j = e % b;
+        big |= !(fabs(fma(s.A[i * lds + j] * s.dsc[i], s.dsc[j], (i == j) ? -1.0 : 0.0)) <= eta);
+      }
+      onep = !__syncthreads_or(big);
+    }
+#endif
     // ---- small: M1 = D L^-T ----
     bool okc = chol_scaled_rows(s.A, b, lds, s.dsc);
     if (!okc) {
@@ -1579,14 +1609,24 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
     }
     __syncthreads();
+    bool g2s = false;
+    if (onep) {
+      prof_mark(pf, 5);
+      copy_rows_in(buf(iy) + (size_t)x.r0 * ld, ld, S1, nlr, b);
+      copy_rows_in(buf(iw) + (size_t)x.r0 * ld, ld, S2, nlr, b);
+      __syncthreads();
+      gram_mma2<true, true>(S1, b, b, S2, b, b, 0, nlr, red_slot(d, x, x.c), s.gsc);   // H0 = Y^T W
+      prof_mark(pf, 4);
+      cg::this_cluster().sync();
+      for (int i = tid; i < b * b; i += blockDim.x) s.Q[(i / b) * lds + (i % b)] = cluster_sum(d, x, i, false);
+      x.par ^= 1;
+      __syncthreads();
+      msucc += m;
+      prof_mark(pf, 9);
+    } else {
     // Y1 = Y M1 ; W1 = W M1 -- in shared memory (own rows) when they fit
     // after the Rayleigh-Ritz workspaces, else in buf(iav) / buf(iw1)
     prof_mark(pf, 5);
-    const int nlr = x.r1 - x.r0;
-    const bool rsm = 3 * nlmax * b <= ycap;
-    double* S0 = s.A + 4 * (size_t)lcap * lds;
-    double* S1 = S0 + (size_t)nlr * b;
-    double* S2 = S1 + (size_t)nlr * b;
     if (rsm) {
       copy_rows_in(buf(iy) + (size_t)x.r0 * ld, ld, S0, nlr, b);
       __syncthreads();
@@ -1626,7 +1666,6 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // by the series (I + E)^(-1/2) = I - E/2 + 3/8 E^2 + O(E^3) (symmetric
     // K instead of the triangular L2^-1; V^T V = I + O(E^3)).
     prof_mark(pf, 8);
-    bool g2s = false;
     {
       for (int i = tid; i < b; i += blockDim.x) {
         const double g = s.A[i * lds + i];
@@ -1660,6 +1699,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     msucc += m;     // total degree of the iteration (the next first pass takes min(hint, spread cap))
     prof_mark(pf, 9);
     if (!g2s) tri_inv_lower_rows(s.A, s.L, b, lds);            // L = L2^-1
+    }
     prof_mark(pf, 10);
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
       int i = e / b, j = e % b;
