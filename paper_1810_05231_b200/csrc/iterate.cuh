@@ -188,19 +188,23 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // accumulating up to four 8x8 DMMA tiles over its rows (k = 4 rows per
 // mma.m8n8k4); chunks are then added in a fixed order through shared memory.
 // SA / SB: A / B lie in this CTA's shared memory (LDS instead of generic loads).
-template <bool SA = false, bool SB = false>
+template <bool SA = false, bool SB = false, bool CAT = false>
 __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const double* __restrict__ B, int ldb,
-                          int nb, int r0, int r1, double* gout, double* wsm);
+                          int nb, int r0, int r1, double* gout, double* wsm,
+                          const double* __restrict__ A2 = nullptr, int lda2 = 0, int na1 = 0);
 
 __device__ __forceinline__ void gram_mma(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
                                          int ld, int r0, int r1, double* gout, double* wsm) {
   gram_mma2(A, ld, na, B, ld, nb, r0, r1, gout, wsm);
 }
 
-template <bool SA, bool SB>
+// CAT: A is the column concatenation [A (na1 columns) | A2 (na - na1 columns)]
+template <bool SA, bool SB, bool CAT>
 __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const double* __restrict__ B, int ldb,
-                          int nb, int r0, int r1, double* gout, double* wsm) {
+                          int nb, int r0, int r1, double* gout, double* wsm,
+                          const double* __restrict__ A2, int lda2, int na1) {
   if (SA) A = as_shared(A);
+  if (SA && CAT) A2 = as_shared(A2);
   if (SB) B = as_shared(B);
   wsm = as_shared(wsm);
   const int q = na * nb;
@@ -233,7 +237,10 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
         double av[4], bv[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          av[t] = (rv && ti[t] < na) ? A[(size_t)rho * lda + ti[t]] : 0.0;
+          if (CAT)
+            av[t] = (rv && ti[t] < na) ? (ti[t] < na1 ? A[(size_t)rho * lda + ti[t]] : A2[(size_t)rho * lda2 + ti[t] - na1]) : 0.0;
+          else
+            av[t] = (rv && ti[t] < na) ? A[(size_t)rho * lda + ti[t]] : 0.0;
           bv[t] = (rv && tj[t] < nb) ? B[(size_t)rho * ldb + tj[t]] : 0.0;
         }
 #pragma unroll
@@ -1535,9 +1542,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       }
       fence_proxy_async();
       __syncthreads();
-      gram_mma2<true, true>(yo, bcp, b, yo, bcp, b, 0, nl, red_slot(d, x, x.c) + rFx * b, s.gsc);
+      // [F_x | Y]^T Y in one Gram: the step's T partial (rows < rFx) and G1 = Y^T Y
+      // (rows rFx ..) -- the layout the step's reduction and G1 read
+      gram_mma2<true, true, true>(s.SF, s.sld, rFx + b, yo, bcp, b, 0, nl, red_slot(d, x, x.c), s.gsc, yo, bcp, rFx);
       int ycp_rr = 0;
-      bool gr = false;
+      bool gr = true;
       operator_step_own_any(d, x, s, zv, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0, pf, ycp_rr, &mbar_sm, mphase, gr, false);
       __syncthreads();
       Cta xp = x;
