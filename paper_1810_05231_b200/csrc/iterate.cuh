@@ -45,6 +45,9 @@ namespace pdsdp {
 #ifndef PDSDP_ONEPASS_RR
 #define PDSDP_ONEPASS_RR 1
 #endif
+#ifndef PDSDP_ONEPASS_ETA
+#define PDSDP_ONEPASS_ETA 0.5   // entrywise bound b * max|E| of the one-pass test (cond <= (1+eta)/(1-eta))
+#endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
 #endif
@@ -1593,7 +1596,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         s.dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
       }
       __syncthreads();
-      const double eta = 0.5 / b;
+      const double eta = PDSDP_ONEPASS_ETA / b;
       int big = 0;
       for (int e = tid; e < b * b; e += blockDim.x) {
         const int i = e / b, j = e % b;
