@@ -45,6 +45,9 @@ namespace pdsdp {
 #ifndef PDSDP_ONEPASS_RR
 #define PDSDP_ONEPASS_RR 1
 #endif
+#ifndef PDSDP_JAC4_MIN
+#define PDSDP_JAC4_MIN 24      // smallest block solved by the block-pair Jacobi (jacobi_eig4)
+#endif
 #ifndef PDSDP_ONEPASS_ETA
 #define PDSDP_ONEPASS_ETA 0.5   // entrywise bound b * max|E| of the one-pass test (cond <= (1+eta)/(1-eta))
 #endif
@@ -1741,7 +1744,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     double *Aj, *Qj;
     // block-pair updates pay off once the per-element traffic dominates the
     // per-round latency (tools/microbench/small_dense_probe.cu: 1.4x at b = 28)
-    if (b >= 24)
+    if (b >= PDSDP_JAC4_MIN)
       jacobi_eig4(s.A, s.M, s.Q, s.T, b, lds, s.cs, reinterpret_cast<int*>(static_cast<double*>(s.gsc)), s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     else
       jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, reinterpret_cast<int*>(static_cast<double*>(s.gsc)), s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
