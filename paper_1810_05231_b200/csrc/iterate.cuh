@@ -181,7 +181,7 @@ __device__ void gram_partial(const double* __restrict__ A, int na, const double*
 }
 
 #ifndef PDSDP_GRAM_SCR
-#define PDSDP_GRAM_SCR 2048     // doubles of smem for the cross-warp Gram reduction
+#define PDSDP_GRAM_SCR 3072     // doubles of smem for the cross-warp Gram reduction (12 work items: one per warp; 2048 / 4096 measured slower)
 #endif
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
