@@ -280,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
             # launch = one iteration at the final rank (ncu --set full,
             # profiles/r01s3_iterate_kernel_ncu_raw_r20.txt; 2340096 at rank 10):
             # the iterate stays L2-resident, the kernel is latency-bound
-            "traffic": 2981376, "traffic_source": "profiles/r01s4_iterate_kernel_ncu_raw_r20.csv",
+            "traffic": 2984448, "traffic_source": "profiles/r01s4_iterate_kernel_ncu_raw_r20.csv",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs",
             "algorithmic_bytes_per_iteration": algo_bytes, "algorithmic_flops_per_iteration": algo_flops,
             "basis": f"SURVEY 8(d) dense formulation, n={n}, b={b}, p_pass={mv:.2f}, r={r}",
