@@ -22,7 +22,9 @@
 #include "residual.cuh"
 #include "zbound.cuh"
 
+#ifndef PDSDP_ZL_EVERY
 #define PDSDP_ZL_EVERY 256   // iterations between lambda_max(Z) estimates
+#endif
 
 using namespace pdsdp;
 

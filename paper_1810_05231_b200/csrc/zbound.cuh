@@ -17,7 +17,9 @@
 
 namespace pdsdp {
 
+#ifndef PDSDP_ZL_STEPS
 #define PDSDP_ZL_STEPS 48      // Lanczos steps per estimate
+#endif
 #define PDSDP_ZL_THREADS 512
 #define PDSDP_ZL_NMAX 8192     // vectors q, q_prev, w in shared memory
 
