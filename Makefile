@@ -9,6 +9,7 @@ LIB := paper_1810_05231_b200/libpdsdp_b200.so
 all: $(LIB)
 
 $(LIB): $(SRC) $(HDR)
+	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -Xptxas -v 2> build/ptxas.log || (cat build/ptxas.log; false)
 
 build/ptxas.log: | build

@@ -29,7 +29,7 @@ from .io import (
     write_solution,
 )
 from .layout import EigenDecomposition, SymMatrix, approx_error_bound, packed_index, packed_length, smat, svec
-from .model import SdpProblem, SparseRow
+from .model import SdpProblem, SparseRow, as_problem
 from .operators import apply_M, apply_M_adjoint, aproj_psd
 from .solver import (
     check_solution,
@@ -43,7 +43,7 @@ from .solver import (
 __all__ = [
     "Checkpoint", "EigenDecomposition", "ProgressInfo", "RankController", "SdpProblem",
     "SolveResult", "SolveStatus", "SolverConfig", "SparseRow", "SymMatrix", "apply_M",
-    "apply_M_adjoint", "aproj_psd", "approx_error_bound", "estimate_operator_norm",
+    "apply_M_adjoint", "aproj_psd", "as_problem", "approx_error_bound", "estimate_operator_norm",
     "SolutionReport", "check_solution", "solve_pd_sdp",
     "ParseError", "load_problem", "parse_extended", "parse_sdpa", "read_solution", "write_extended",
     "write_sdpa", "write_solution",

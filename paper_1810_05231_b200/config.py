@@ -20,10 +20,26 @@ from .layout import SymMatrix, approx_error_bound
 
 
 class SolveStatus(Enum):
+    """Run outcome (reference ``pdhg.py:32-36``).  Members compare and hash
+    equal to the same-named members of any other ``SolveStatus`` enum with
+    the same value, so tables keyed by the reference's own members (its
+    ``cli._status_exit_code``, ``cli.py:178-186``) accept results of this
+    package without importing either side into the other."""
+
     OPTIMAL = "optimal"
     MAX_ITERATIONS = "max_iterations"
     TIME_LIMIT = "time_limit"
     DIVERGED = "diverged"
+
+    def __eq__(self, other):
+        if self is other:
+            return True
+        if isinstance(other, Enum) and type(other).__name__ == "SolveStatus":
+            return other.name == self.name and other.value == self.value
+        return NotImplemented
+
+    def __hash__(self):
+        return hash(self._name_)      # Enum's own hash: same bucket as the reference member
 
 
 # eps_lambda defaults to this times n (reference pdhg.py:39)

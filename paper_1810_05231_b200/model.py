@@ -12,6 +12,7 @@ into dense (i, j) coordinates when a problem is uploaded.
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -111,3 +112,42 @@ class SdpProblem:
             val = np.concatenate([r.values for r in rows]) if rows else np.zeros(0)
             self._csr = (indptr, idx.astype(np.int64), val.astype(float))
         return self._csr
+
+
+# Reference-typed problems (``pdsdp.SdpProblem``, reference ``problem.py:74-137``)
+# are accepted wherever this package takes a problem: they are read by duck
+# typing (n, C.data, the rows' indices / values, b, h, objective_sign) -- the
+# reference package is never imported -- and the converted problem, which owns
+# the device cache, is kept off-object for as long as the caller's object lives.
+_converted: dict = {}
+
+
+def as_problem(prob) -> "SdpProblem":
+    """This package's :class:`SdpProblem` for ``prob``: ``prob`` itself, or the
+    cached field-by-field conversion of any object laid out like the
+    reference's ``SdpProblem`` (``problem.py:74-87``)."""
+    if isinstance(prob, SdpProblem):
+        return prob
+    key = id(prob)
+    hit = _converted.get(key)
+    if hit is not None and hit[0]() is prob:
+        return hit[1]
+    try:
+        conv = SdpProblem(
+            n=int(prob.n),
+            C=SymMatrix(int(prob.C.n), np.asarray(prob.C.data, dtype=float)),
+            A=[SparseRow(r.indices, r.values) for r in prob.A],
+            b=np.asarray(prob.b, dtype=float),
+            G=[SparseRow(r.indices, r.values) for r in getattr(prob, "G", [])],
+            h=np.asarray(getattr(prob, "h", np.zeros(0)), dtype=float),
+            name=str(getattr(prob, "name", "")),
+            objective_sign=float(getattr(prob, "objective_sign", 1.0)),
+        )
+    except AttributeError as exc:
+        raise TypeError(f"not an SdpProblem-like object: {exc}") from None
+    try:
+        ref = weakref.ref(prob, lambda _r, k=key: _converted.pop(k, None))
+    except TypeError:                     # object without weakref support: convert every time
+        return conv
+    _converted[key] = (ref, conv)
+    return conv

@@ -12,17 +12,19 @@ import numpy as np
 
 from .device import aproj_psd_packed
 from .layout import SymMatrix
-from .model import SdpProblem
+from .model import SdpProblem, as_problem
 from .solver import _device_batch
 
 
 def apply_M(prob: SdpProblem, X: SymMatrix) -> np.ndarray:
+    prob = as_problem(prob)
     if X.n != prob.n:
         raise ValueError(f"matrix dimension {X.n} does not match problem {prob.n}")
     return _device_batch(prob).apply_M(0, X.data)
 
 
 def apply_M_adjoint(prob: SdpProblem, y) -> SymMatrix:
+    prob = as_problem(prob)
     y = np.asarray(y, dtype=float)
     if y.shape != (prob.m + prob.p,):
         raise ValueError(f"multiplier length {y.size} does not match m+p={prob.m + prob.p}")

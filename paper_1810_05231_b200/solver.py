@@ -37,7 +37,7 @@ from .device import (
     DeviceBatch,
 )
 from .layout import SymMatrix, approx_error_bound
-from .model import SdpProblem
+from .model import SdpProblem, as_problem
 
 logger = logging.getLogger(__name__)
 
@@ -51,6 +51,9 @@ FLAG_COLD, FLAG_CERT, FLAG_RERUN = 1, 2, 4
 
 
 def _device_batch(prob: SdpProblem) -> DeviceBatch:
+    """The resident single-instance batch of ``prob`` (created on first use);
+    reference-typed problems go through :func:`~.model.as_problem`."""
+    prob = as_problem(prob)
     cache = prob._device_cache
     if "batch" not in cache:
         cache["batch"] = DeviceBatch([prob])
@@ -323,6 +326,7 @@ def solve_lr_pd_sdp(
     config = config or SolverConfig()
     config.validate()
     t0 = time.perf_counter()
+    prob = as_problem(prob)
     batch = _device_batch(prob)
     alpha = step_size(prob, config)
     o = run_lr_loop(batch, 0, prob, config, alpha, callback, t0)
@@ -352,7 +356,8 @@ def solve_lr_pd_sdp_batch(problems, config: SolverConfig | None = None) -> list:
     config = config or SolverConfig()
     config.validate()
     t0 = time.perf_counter()
-    batch = DeviceBatch(list(problems))
+    problems = [as_problem(p) for p in problems]
+    batch = DeviceBatch(problems)
     alphas = [config.alpha_override if config.alpha_override is not None else
               config.alpha_safety / operator_norm_on_device(batch, i, config.seed)
               for i in range(batch.count)]
@@ -382,6 +387,7 @@ def solve_pd_sdp(
     residual, no rank control (``rank_path = [(0, n)]``)."""
     config = config or SolverConfig()
     config.validate()
+    prob = as_problem(prob)
     n = prob.n
     if n > EXACT_N_MAX:
         raise ValueError(f"exact projection on the device supports n <= {EXACT_N_MAX} (n={n}); "
@@ -439,6 +445,7 @@ def check_solution(prob: SdpProblem, X: SymMatrix, y, tol: float = 1e-3) -> Solu
     Gershgorin bound of X, lambda_max read off the rank-1 projection."""
     from .device import aproj_psd_packed
     from .layout import packed_coords
+    prob = as_problem(prob)
     y = np.asarray(y, dtype=float)
     if X.n != prob.n or y.shape != (prob.m + prob.p,):
         raise ValueError("solution dimensions do not match the problem")

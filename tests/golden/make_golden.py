@@ -267,6 +267,57 @@ def make_sketch(path, idx, Ks):
     np.savez_compressed(path, **out)
 
 
+def make_full(path, idx, seed=0):
+    """Run the UNMODIFIED reference to tolerance on BASELINE config idx
+    (0-based) and record what pins an end-to-end comparison: status, stop
+    iteration, rank path, checkpoints, final objectives / residuals, y, the
+    final X as eigen-factors (exact rank <= r, so V diag(lam) V^T reproduces
+    the packed X to rounding) and the progress history every 100 iterations.
+    Hours of CPU for configs 2 / 4; progress goes to stdout."""
+    prob, cfg = workloads.config(idx, seed)
+    rp = to_ref(prob)
+    hist = []
+    t0 = time.perf_counter()
+
+    def cb(info):
+        hist.append(tuple(info))
+        if info.k % 1000 == 0:
+            print(f"cfg{idx + 1} s{seed} k={info.k} eps_c={info.eps_comb:.3e} r={info.rank} "
+                  f"obj={info.objective:.9g} t={time.perf_counter() - t0:.0f}s", flush=True)
+
+    guard = ArpackErrorFallback() if idx == 3 else None
+    if guard:
+        guard.__enter__()
+    try:
+        with LambdaRecorder() as rec:
+            res = pdsdp.solve_lr_pd_sdp(rp, to_ref_cfg(cfg, progress_every=100), callback=cb)
+    finally:
+        if guard:
+            guard.__exit__()
+    wall = time.perf_counter() - t0
+    Xd = res.X.to_dense()
+    w, V = np.linalg.eigh(Xd)
+    keep = np.abs(w) > 1e-13 * max(np.abs(w).max(), 1e-300)
+    w, V = w[keep][::-1], V[:, keep][:, ::-1]
+    recon = (V * w) @ V.T
+    out = {
+        "n": prob.n, "seed": seed, "status": res.status.value, "iters": res.iterations,
+        "pobj": res.primal_objective, "dobj": res.dual_objective,
+        "res_final": np.array(res.final_residuals), "scale": res.residual_scale,
+        "rank_path": np.array(res.rank_path),
+        "checkpoints": np.array([(c.rank, c.objective) for c in res.checkpoints]),
+        "y_final": res.y, "X_lam": w, "X_V": V,
+        "X_fro": np.linalg.norm(Xd), "X_recon_err": np.linalg.norm(recon - Xd),
+        "history": np.array(hist), "lam_last": rec.values[-1],
+        "lam_at_rank_change": np.array([rec.values[k - 1] for k, _ in res.rank_path[1:]]),
+        "wall": wall, "threads": os.environ.get("OMP_NUM_THREADS", ""),
+    }
+    np.savez_compressed(path, **out)
+    print(f"cfg{idx + 1} s{seed} FULL {res.status} iters={res.iterations} pobj={res.primal_objective!r} "
+          f"dobj={res.dual_objective!r} rank_path={res.rank_path} wall={wall:.0f}s "
+          f"recon_err={out['X_recon_err']:.2e}", flush=True)
+
+
 def _well_posed(prob, rng):
     """The reference conftest's random problem made feasible-ish (PSD
     objective, positive right-hand sides) so that solves converge."""
@@ -445,7 +496,16 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--full", default="",
+                    help="comma list of to-tolerance reference runs: cfg2, cfg4, cfg5sN (seed N), cfg1")
     a = ap.parse_args()
+    if a.full:
+        for name in a.full.split(","):
+            if name.startswith("cfg5s"):
+                make_full(os.path.join(HERE, f"{name}_full.npz"), 4, int(name[5:]))
+            else:
+                make_full(os.path.join(HERE, f"{name}_full.npz"), int(name[3:]) - 1)
+        sys.exit(0)
     jobs = {
         "ops_small": lambda: make_ops_small(os.path.join(HERE, "ops_small.npz")),
         "lr_small": lambda: make_lr_small(os.path.join(HERE, "lr_small.npz")),

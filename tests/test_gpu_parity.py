@@ -416,3 +416,53 @@ def test_check_solution_matches_reference():
         np.testing.assert_allclose(got[[2, 3]], ref[[2, 3]], rtol=1e-10, atol=1e-12)
         assert abs(got[4] - ref[4]) <= 1e-8 * scale, (q, got[4], ref[4])
         assert rep.max_violation() == pytest.approx(max(ref[2], ref[3], -min(ref[4], 0.0)), rel=1e-6, abs=1e-8 * scale)
+
+
+# ---------------------------------------------------------------- reference-typed inputs
+
+class _RefLayoutSym:
+    """Stand-in with the reference SymMatrix's layout (``symmat.py:104-113``)."""
+    def __init__(self, n, data):
+        self.n, self.data = n, data
+
+
+class _RefLayoutRow:
+    def __init__(self, indices, values):
+        self.indices, self.values = indices, values
+
+
+class _RefLayoutProblem:
+    """Stand-in with the fields of the reference's ``SdpProblem``
+    (``problem.py:74-87``) and none of this package's (no ``_device_cache``,
+    no ``stacked_arrays``): what ``cli._solve_one`` would hand over.  The real
+    reference types are exercised in tests/test_dropin_cpu.py (the reference
+    tree does not exist on the GPU box)."""
+    def __init__(self, prob):
+        self.n = prob.n
+        self.C = _RefLayoutSym(prob.n, prob.C.data.copy())
+        self.A = [_RefLayoutRow(r.indices.copy(), r.values.copy()) for r in prob.A]
+        self.b = prob.b.copy()
+        self.G = [_RefLayoutRow(r.indices.copy(), r.values.copy()) for r in prob.G]
+        self.h = prob.h.copy()
+        self.name = "ref-layout"
+        self.objective_sign = 1.0
+
+
+def test_reference_layout_problem_solves_identically():
+    d = load_golden("lr_small.npz")
+    pre = "c1_"
+    prob = problem_from_golden(d, pre)
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=400, initial_rank=int(d[pre + "r0"]),
+                       window_ell=50, time_limit_s=1e9)
+    dup = _RefLayoutProblem(prob)
+    res = pk.solve_lr_pd_sdp(dup, cfg)
+    assert res.status.value == str(d[pre + "status"]) and res.iterations == int(d[pre + "iters"])
+    assert rel(res.X.data, d[pre + "X"]) <= ITER_TOL and rel(res.y, d[pre + "y"]) <= ITER_TOL
+    # op-level entry points and the report take the same object
+    own = pk.solve_lr_pd_sdp(prob, cfg)
+    assert np.array_equal(own.X.data, res.X.data) and np.array_equal(own.y, res.y)
+    np.testing.assert_array_equal(pk.apply_M(dup, res.X), pk.apply_M(prob, res.X))
+    np.testing.assert_array_equal(pk.apply_M_adjoint(dup, res.y).data, pk.apply_M_adjoint(prob, res.y).data)
+    assert pk.estimate_operator_norm(dup, 0) == pk.estimate_operator_norm(prob, 0)
+    assert pk.check_solution(dup, res.X, res.y) == pk.check_solution(prob, res.X, res.y)
+    assert not hasattr(dup, "_device_cache")
