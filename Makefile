@@ -16,7 +16,14 @@ build/ptxas.log: | build
 build:
 	mkdir -p build
 
-clean:
-	rm -f $(LIB)
+# Diagnostic build with the in-kernel phase timer / per-CTA timeline compiled in
+# (tools/gpu_trace*.py: PDSDP_B200_LIB=paper_1810_05231_b200/libpdsdp_b200_trace.so).
+TRACE_LIB := paper_1810_05231_b200/libpdsdp_b200_trace.so
+trace: $(TRACE_LIB)
+$(TRACE_LIB): $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DPDSDP_TRACE=1 -shared -o $@ $(SRC)
 
-.PHONY: all clean
+clean:
+	rm -f $(LIB) $(TRACE_LIB)
+
+.PHONY: all clean trace

@@ -118,6 +118,12 @@ struct Prof {
   int cap;
   double* trace;
 };
+// Compiled in only with -DPDSDP_TRACE=1 (tools/gpu_trace*.py builds): the
+// production kernel carries no clock64 reads or trace stores.
+#ifndef PDSDP_TRACE
+#define PDSDP_TRACE 0
+#endif
+#if PDSDP_TRACE
 __device__ __forceinline__ void prof_log(Prof& p, int label, long long now) {
   if (p.trace && p.ntr < p.cap) {
     p.trace[2 * p.ntr] = label;
@@ -137,6 +143,10 @@ __device__ __forceinline__ void prof_mark(Prof& p, int phase) {
 __device__ __forceinline__ void prof_tick(Prof& p, int label) {
   if (threadIdx.x == 0) prof_log(p, label, clock64());
 }
+#else
+__device__ __forceinline__ void prof_mark(Prof&, int) {}
+__device__ __forceinline__ void prof_tick(Prof&, int) {}
+#endif
 
 // Per-instance descriptor (device resident).  Sizes and pointers only.
 struct Inst {

@@ -135,51 +135,6 @@ __device__ __forceinline__ void cluster_reduce(const Inst& d, Cta& x, int q_sum,
   __syncthreads();
 }
 
-// partial[o] = sum over own rows of A[rho, i] * B[rho, j], o = i*nb + j.
-// Written to the global reduction slot (deterministic, one finisher per o).
-// Each thread owns one output and one contiguous row chunk; rows are read
-// four at a time so that eight independent loads are in flight.
-__device__ void gram_partial(const double* __restrict__ A, int na, const double* __restrict__ B, int nb,
-                             int ld, int r0, int r1, double* gout, double* scr) {
-  const int q = na * nb;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if (q == 0) return;
-  auto dot = [&](int i, int j, int ra, int rb) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int rho = ra;
-    for (; rho + 4 <= rb; rho += 4) {
-      const double a0 = A[(size_t)rho * ld + i], a1 = A[(size_t)(rho + 1) * ld + i];
-      const double a2 = A[(size_t)(rho + 2) * ld + i], a3 = A[(size_t)(rho + 3) * ld + i];
-      const double b0 = B[(size_t)rho * ld + j], b1 = B[(size_t)(rho + 1) * ld + j];
-      const double b2 = B[(size_t)(rho + 2) * ld + j], b3 = B[(size_t)(rho + 3) * ld + j];
-      s0 = fma(a0, b0, s0); s1 = fma(a1, b1, s1); s2 = fma(a2, b2, s2); s3 = fma(a3, b3, s3);
-    }
-    for (; rho < rb; ++rho) s0 = fma(A[(size_t)rho * ld + i], B[(size_t)rho * ld + j], s0);
-    return (s0 + s1) + (s2 + s3);
-  };
-  if (q >= nt / 2) {
-    for (int o = tid; o < q; o += nt) gout[o] = dot(o / nb, o % nb, r0, r1);
-  } else {
-    const int S = nt / q;
-    const int o = tid % q, sl = tid / q;
-    double s = 0.0;
-    if (sl < S) {
-      const int len = (r1 - r0 + S - 1) / S;
-      const int ra = r0 + sl * len;
-      const int rb = min(r1, ra + len);
-      if (ra < rb) s = dot(o / nb, o % nb, ra, rb);
-    }
-    scr[tid] = s;
-    __syncthreads();
-    if (tid < q) {
-      double t = 0.0;
-      for (int k = 0; k < S; ++k) t += scr[k * q + tid];
-      gout[tid] = t;
-    }
-    __syncthreads();
-  }
-}
-
 #ifndef PDSDP_GRAM_SCR
 #define PDSDP_GRAM_SCR 3072     // doubles of smem for the cross-warp Gram reduction (12 work items: one per warp; 2048 / 4096 measured slower)
 #endif
@@ -570,24 +525,6 @@ __device__ void rot_mma(const double* __restrict__ In, int ldi, const double* __
   __syncthreads();
 }
 
-// out (nl x b, stride ldo) = In (nl x b, stride ldi) * Msm (b x b, stride lds);
-// In in shared memory, out in shared or global memory
-__device__ __forceinline__ void rot_block(const double* In, int ldi, const double* Msm, int lds,
-                                          double* out, int ldo, int nl, int b) {
-  for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
-    const int lr = it / b, j = it - lr * b;
-    const double* row = In + (size_t)lr * ldi;
-    double a0 = 0.0, a1 = 0.0;
-    int t = 0;
-    for (; t + 2 <= b; t += 2) {
-      a0 = fma(row[t], Msm[t * lds + j], a0);
-      a1 = fma(row[t + 1], Msm[(t + 1) * lds + j], a1);
-    }
-    if (t < b) a0 = fma(row[t], Msm[t * lds + j], a0);
-    out[(size_t)lr * ldo + j] = a0 + a1;
-  }
-}
-
 // T (smem, (rF + nlock) x bc) <- [diag(lamF); -diag(theta)] .* T  (in place)
 __device__ void scale_T(const Sm& s, int rF, int nlock, int bc) {
   for (int e = threadIdx.x; e < (rF + nlock) * bc; e += blockDim.x) {
@@ -974,36 +911,7 @@ struct Assess {
   double maxres;    // worst relative residual among columns needing work
 };
 
-__device__ Assess assess(const double* theta, const double* res, int r, int b, int k, double scale,
-                         double xnorm, double cert_tol) {
-  Assess a{-1, false, false, 1.0, 0.0};
-  for (int i = 0; i < k; ++i) {
-    const double ri = res[i];
-    if (col_ok(i, ri, theta, r, b, scale, xnorm, cert_tol)) continue;
-    a.maxres = fmax(a.maxres, ri / scale);
-    if (i < r) {
-      a.last_bad = i;
-      a.rho_k = fmax(a.rho_k, ri / fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
-    } else {
-      a.cert_bad = true;
-    }
-  }
-  // The kept set must be the true top r: the first excluded Ritz pair has to
-  // be either clearly below the last kept one or itself converged.
-  if (r < b && r < k + 1 && r >= 1) {
-    const double lo_k = theta[r - 1] - 2.0 * res[r - 1];
-    const double hi_t = theta[r] + 2.0 * res[r];
-    if (!(hi_t < lo_k) && res[r] > PDSDP_TOL_CERT * scale &&
-        !(theta[r] + res[r] < 0.0 && res[r] <= PDSDP_TOL_CLIP * scale) &&
-        !(cert_tol < 0.0 && theta[r] < 0.0 && res[r] <= 0.1 * -theta[r])) {
-      a.tail_bad = true;
-      a.maxres = fmax(a.maxres, res[r] / scale);
-    }
-  }
-  return a;
-}
-
-// Warp-parallel forms of the per-column scans above: every warp evaluates
+// Warp-parallel per-column scans: every warp evaluates
 // them independently (lanes stride the columns, fixed xor-shuffle trees), so
 // all threads of all CTAs hold identical results without a barrier.  A
 // sequential scan over up to 64 columns with FP64 divisions was several
@@ -1201,8 +1109,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   x.r1 = (int)(((long long)n * (x.c + 1)) / x.C);
   x.par = 0;
 
-  __shared__ Prof pf_sm;                 // thread-0 phase timer (kept out of local memory)
+  __shared__ Prof pf_sm;                 // thread-0 phase timer (PDSDP_TRACE builds only)
   Prof& pf = pf_sm;
+#if PDSDP_TRACE
   if (threadIdx.x == 0) {
     pf.last = clock64(); pf.cur = 0;
     for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
@@ -1211,6 +1120,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     pf.trace = ((flags0 & 32) && x.c == 0) ? d.st->hdump : nullptr;
     if (flags0 & 64) { pf.trace = d.trace + (size_t)x.c * 2 * PDSDP_TRACE_CTA; pf.cap = PDSDP_TRACE_CTA - 1; }
   }
+#else
+  (void)flags0;
+#endif
   prof_tick(pf, 29);
   __shared__ Sm s_sm;
   Sm& s = s_sm;
@@ -1749,7 +1661,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     else
       jacobi_eig3(s.A, s.M, s.Q, s.T, b, lds, s.cs, reinterpret_cast<int*>(static_cast<double*>(s.gsc)), s.flag, need_cert ? b : min(b, r + 1), &Aj, &Qj);
     prof_mark(pf, 12);
-    if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];
+#if PDSDP_TRACE
+    if (x.c == 0 && tid == 0) st->prof[15] += s.flag[0];   // Jacobi sweeps
+#endif
     sort_desc(Aj, b, lds, s.theta, s.perm);
     // B = D L^-T Q[:, perm]  -> the Jacobi scratch that does not hold Q
     double* Bm = (Qj == s.Q) ? s.M : s.Q;
@@ -2063,6 +1977,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
 
   // ---------------- epilogue: state for the next iteration + scalars ----------------
   prof_mark(pf, 0);
+#if PDSDP_TRACE
   if (x.c == 0 && tid == 0) {
     for (int q = 0; q < 15; ++q) st->prof[q] = (double)pf.acc[q];
     if (pf.trace && !(ctl.flags & 64)) { prof_tick(pf, 99); st->hdump[PDSDP_BMAX * PDSDP_BMAX + 7] = pf.ntr; }
@@ -2071,6 +1986,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     prof_tick(pf, 99);
     pf.trace[2 * PDSDP_TRACE_CTA - 1] = pf.ntr;
   }
+#endif
   if (x.c == 0) {
     for (int i = tid; i < PDSDP_BMAX; i += blockDim.x) {
       st->theta[i] = (i < b) ? s.theta[i] : 0.0;

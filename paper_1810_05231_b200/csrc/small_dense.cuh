@@ -20,146 +20,6 @@
 
 namespace pdsdp {
 
-// In-place Cholesky G = L L^T (lower) of an SPD matrix scaled to unit
-// diagonal first: G' = D G D, D = diag(G)^-1/2.  On exit G holds L' (lower,
-// upper triangle zeroed) and dsc[i] = D_ii.  Returns false on breakdown.
-__device__ bool chol_scaled(double* G, int b, int lds, double* dsc, int* sflag) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if (tid == 0) *sflag = 1;
-  for (int i = tid; i < b; i += nt) {
-    double g = G[i * lds + i];
-    dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
-  }
-  __syncthreads();
-  for (int e = tid; e < b * b; e += nt) {
-    int i = e / b, j = e % b;
-    G[i * lds + j] = (j <= i) ? G[i * lds + j] * dsc[i] * dsc[j] : 0.0;
-  }
-  __syncthreads();
-  for (int j = 0; j < b; ++j) {
-    double d = G[j * lds + j];
-    if (!(d > 1e-28)) {  // breakdown (also catches NaN)
-      if (tid == 0) *sflag = 0;
-      __syncthreads();
-      return false;
-    }
-    d = sqrt(d);
-    __syncthreads();
-    for (int i = j + 1 + tid; i < b; i += nt) G[i * lds + j] /= d;
-    if (tid == 0) G[j * lds + j] = d;
-    __syncthreads();
-    const int rem = b - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) G[i * lds + k] -= G[i * lds + j] * G[k * lds + j];
-    }
-    __syncthreads();
-  }
-  return true;
-}
-
-// X = L^{-1} (lower triangular inverse), one column per thread.
-__device__ void tri_inv_lower(const double* L, double* X, int b, int lds) {
-  for (int c = threadIdx.x; c < b; c += blockDim.x) {
-    for (int i = 0; i < c; ++i) X[i * lds + c] = 0.0;
-    for (int i = c; i < b; ++i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) s -= L[i * lds + k] * X[k * lds + c];
-      X[i * lds + c] = s / L[i * lds + i];
-    }
-  }
-  __syncthreads();
-}
-
-// Cyclic parallel two-sided Jacobi: A (b x b symmetric) -> diag, Q columns =
-// eigenvectors.  Round-robin pairing, b/2 disjoint rotations per round.
-// Rotations below 2.2e-16 ||A||_F are skipped (they cannot move an
-// eigenvalue by more than rounding); pairs with both indices >= nimp (trailing
-// guard columns) are only reduced to 1e-8 ||A||_F.  sflag[0] returns sweeps.
-__device__ void jacobi_eig(double* A, double* Q, int b, int lds, double* cs, int* pq, int* sflag, int nimp) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ double fro_part[32];
-  double f = 0.0;
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
-    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
-    const double v = A[i * lds + j];
-    f = fma(v, v, f);
-  }
-  f = warp_sum(f);
-  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
-  __syncthreads();
-  double fro = 0.0;
-  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
-  fro = sqrt(fro);
-  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
-  if (tid == 0) sflag[0] = 0;
-  if (b == 1) { __syncthreads(); return; }
-  const int bb = b + (b & 1);
-  const int np = bb / 2;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    if (tid == 0) sflag[1] = 0;
-    __syncthreads();
-    for (int round = 0; round < bb - 1; ++round) {
-      for (int j = tid; j < np; j += nt) {
-        int t0 = j, t1 = bb - 1 - j;
-        int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + round) % (bb - 1);
-        int q = 1 + (t1 - 1 + round) % (bb - 1);
-        if (p > q) { int tmp = p; p = q; q = tmp; }
-        double c = 1.0, s = 0.0;
-        if (q < b) {
-          const double apq = A[p * lds + q];
-          const double thr = (p < nimp) ? thr_imp : thr_guard;
-          if (fabs(apq) > thr) {
-            const double tau = (A[q * lds + q] - A[p * lds + p]) / (2.0 * apq);
-            double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            if (!isfinite(tau)) t = 0.0;
-            c = rsqrt(1.0 + t * t);
-            s = t * c;
-            if (t != 0.0) sflag[1] = 1;
-          }
-        }
-        cs[2 * j] = c; cs[2 * j + 1] = s;
-        pq[2 * j] = p; pq[2 * j + 1] = q;
-      }
-      __syncthreads();
-      // rows p, q  <-  J^T A
-      for (int e = tid; e < np * b; e += nt) {
-        int j = e / b, col = e % b;
-        int p = pq[2 * j], q = pq[2 * j + 1];
-        double s = cs[2 * j + 1];
-        if (q >= b || s == 0.0) continue;
-        double c = cs[2 * j];
-        double ap = A[p * lds + col], aq = A[q * lds + col];
-        A[p * lds + col] = c * ap - s * aq;
-        A[q * lds + col] = s * ap + c * aq;
-      }
-      __syncthreads();
-      // columns p, q  <-  A J ;  Q <- Q J
-      for (int e = tid; e < np * b; e += nt) {
-        int j = e / b, row = e % b;
-        int p = pq[2 * j], q = pq[2 * j + 1];
-        double s = cs[2 * j + 1];
-        if (q >= b || s == 0.0) continue;
-        double c = cs[2 * j];
-        double ap = A[row * lds + p], aq = A[row * lds + q];
-        double np_ = c * ap - s * aq, nq_ = s * ap + c * aq;
-        if (row == p) nq_ = 0.0;
-        if (row == q) np_ = 0.0;
-        A[row * lds + p] = np_;
-        A[row * lds + q] = nq_;
-        double qp = Q[row * lds + p], qq = Q[row * lds + q];
-        Q[row * lds + p] = c * qp - s * qq;
-        Q[row * lds + q] = s * qp + c * qq;
-      }
-      __syncthreads();
-    }
-    if (tid == 0) sflag[0] = sweep + 1;
-    int f = sflag[1];
-    __syncthreads();
-    if (!f) break;
-  }
-}
 
 // Descending order of the diagonal of A: perm[rank] = index (ties by index).
 __device__ void sort_desc(const double* A, int b, int lds, double* theta, int* perm) {
@@ -199,322 +59,6 @@ __device__ void sm_gemm(const double* A, int lda, const double* B, int ldb, doub
   __syncthreads();
 }
 
-
-// ---------------------------------------------------------------------------
-// Single-warp variants (warp 0 only; the rest of the block waits at a
-// __syncthreads): the b x b problems are tiny, so block-wide barriers
-// (hundreds per pass) cost far more than the arithmetic.
-
-// In-place scaled Cholesky (see chol_scaled); returns false on breakdown.
-__device__ bool chol_scaled_warp(double* G, int b, int lds, double* dsc) {
-  const int lane = threadIdx.x & 31;
-  for (int i = lane; i < b; i += 32) {
-    const double g = G[i * lds + i];
-    dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
-  }
-  __syncwarp();
-  for (int e = lane; e < b * b; e += 32) {
-    const int i = e / b, j = e % b;
-    G[i * lds + j] = (j <= i) ? G[i * lds + j] * dsc[i] * dsc[j] : 0.0;
-  }
-  __syncwarp();
-  for (int j = 0; j < b; ++j) {
-    double d = G[j * lds + j];
-    if (!(d > 1e-28)) return false;
-    d = sqrt(d);
-    __syncwarp();
-    for (int i = j + 1 + lane; i < b; i += 32) G[i * lds + j] /= d;
-    if (lane == 0) G[j * lds + j] = d;
-    __syncwarp();
-    const int rem = b - j - 1;
-    for (int e = lane; e < rem * rem; e += 32) {
-      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) G[i * lds + k] -= G[i * lds + j] * G[k * lds + j];
-    }
-    __syncwarp();
-  }
-  return true;
-}
-
-// Cyclic two-sided Jacobi in one warp; rotations below 2.2e-16 ||A||_F are
-// skipped (they cannot move an eigenvalue by more than rounding).  Returns
-// the number of sweeps.
-__device__ int jacobi_eig_warp(double* A, double* Q, int b, int lds, double* cs, int* pq) {
-  const int lane = threadIdx.x & 31;
-  double f = 0.0;
-  for (int e = lane; e < b * b; e += 32) {
-    const int i = e / b, j = e % b;
-    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
-    const double v = A[i * lds + j];
-    f = fma(v, v, f);
-  }
-  f = warp_sum(f);
-  const double thr = 2.2e-16 * sqrt(f);
-  __syncwarp();
-  if (b == 1) return 0;
-  const int bb = b + (b & 1), np = bb / 2;
-  int sweeps = 0;
-  for (int sweep = 0; sweep < 30; ++sweep) {
-    bool any = false;
-    for (int round = 0; round < bb - 1; ++round) {
-      for (int j = lane; j < np; j += 32) {
-        const int t0 = j, t1 = bb - 1 - j;
-        int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + round) % (bb - 1);
-        int q = 1 + (t1 - 1 + round) % (bb - 1);
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        double c = 1.0, sn = 0.0;
-        if (q < b) {
-          const double apq = A[p * lds + q];
-          if (fabs(apq) > thr) {
-            const double tau = (A[q * lds + q] - A[p * lds + p]) / (2.0 * apq);
-            double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            if (!isfinite(tau)) t = 0.0;
-            c = rsqrt(1.0 + t * t);
-            sn = t * c;
-            if (t != 0.0) any = true;
-          }
-        }
-        cs[2 * j] = c; cs[2 * j + 1] = sn;
-        pq[2 * j] = p; pq[2 * j + 1] = q;
-      }
-      __syncwarp();
-      for (int e = lane; e < np * b; e += 32) {
-        const int j = e / b, col = e % b;
-        const double sn = cs[2 * j + 1];
-        const int p = pq[2 * j], q = pq[2 * j + 1];
-        if (q >= b || sn == 0.0) continue;
-        const double c = cs[2 * j];
-        const double ap = A[p * lds + col], aq = A[q * lds + col];
-        A[p * lds + col] = c * ap - sn * aq;
-        A[q * lds + col] = sn * ap + c * aq;
-      }
-      __syncwarp();
-      for (int e = lane; e < np * b; e += 32) {
-        const int j = e / b, row = e % b;
-        const double sn = cs[2 * j + 1];
-        const int p = pq[2 * j], q = pq[2 * j + 1];
-        if (q >= b || sn == 0.0) continue;
-        const double c = cs[2 * j];
-        const double ap = A[row * lds + p], aq = A[row * lds + q];
-        double np_ = c * ap - sn * aq, nq_ = sn * ap + c * aq;
-        if (row == p) nq_ = 0.0;
-        if (row == q) np_ = 0.0;
-        A[row * lds + p] = np_;
-        A[row * lds + q] = nq_;
-        const double qp = Q[row * lds + p], qq = Q[row * lds + q];
-        Q[row * lds + p] = c * qp - sn * qq;
-        Q[row * lds + q] = sn * qp + c * qq;
-      }
-      __syncwarp();
-    }
-    ++sweeps;
-    if (!__any_sync(0xffffffffu, any)) break;
-  }
-  return sweeps;
-}
-
-
-// ---------------------------------------------------------------------------
-// One-barrier-per-step variants (all threads of the CTA).
-
-// Scaled Cholesky with a single __syncthreads per column: step j updates the
-// trailing columns from the (final) column j without normalising it; the
-// normalisation happens once at the end.  Same contract as chol_scaled.
-__device__ bool chol_scaled_1s(double* G, int b, int lds, double* dsc) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < b; i += nt) {
-    const double g = G[i * lds + i];
-    dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
-  }
-  __syncthreads();
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
-    G[i * lds + j] = (j <= i) ? G[i * lds + j] * dsc[i] * dsc[j] : 0.0;
-  }
-  __syncthreads();
-  for (int j = 0; j < b; ++j) {
-    const double djj = G[j * lds + j];
-    if (!(djj > 1e-28)) { __syncthreads(); return false; }
-    const double inv = 1.0 / djj;
-    const int rem = b - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) G[i * lds + k] -= G[i * lds + j] * G[k * lds + j] * inv;
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
-    if (j <= i) {
-      const double sj = sqrt(G[j * lds + j]);
-      if (i != j) G[i * lds + j] = G[i * lds + j] / sj;
-    }
-  }
-  __syncthreads();
-  for (int j = tid; j < b; j += nt) G[j * lds + j] = sqrt(G[j * lds + j]);
-  __syncthreads();
-  return true;
-}
-
-// X = L^{-1} (lower) by row elimination, one barrier per row.
-__device__ void tri_inv_lower_1s(const double* L, double* X, int b, int lds) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < b * b; e += nt) X[(e / b) * lds + (e % b)] = (e / b == e % b) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int kk = 0; kk < b - 1; ++kk) {
-    const double lkk = L[kk * lds + kk];
-    const int rows = b - kk - 1, cols = kk + 1;
-    for (int e = tid; e < rows * cols; e += nt) {
-      const int i = kk + 1 + e / cols, c = e % cols;
-      X[i * lds + c] -= L[i * lds + kk] * (X[kk * lds + c] / lkk);
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, c = e % b;
-    X[i * lds + c] = (c <= i) ? X[i * lds + c] / L[i * lds + i] : 0.0;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ int jac_partner(int i, int t, int bb) {
-  if (i == 0) return 1 + (bb - 2 + t) % (bb - 1);
-  const int u = 1 + (((i - 1 - t) % (bb - 1)) + (bb - 1)) % (bb - 1);
-  const int v = bb - 1 - u;
-  return (v == 0) ? 0 : 1 + (v - 1 + t) % (bb - 1);
-}
-
-__device__ __forceinline__ void jac_rot(double app, double aqq, double apq, double thr, double& c, double& s) {
-  c = 1.0; s = 0.0;
-  if (fabs(apq) > thr) {
-    const double tau = (aqq - app) / (2.0 * apq);
-    double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-    if (!isfinite(tau)) t = 0.0;
-    c = rsqrt(1.0 + t * t);
-    s = t * c;
-  }
-}
-
-// Cyclic two-sided Jacobi with one __syncthreads per round: every thread
-// forms its elements of J^T A J and Q J in one pass (ping-pong buffers), and
-// the threads owning the entries of next round's pairs form next round's
-// rotations directly.  Same thresholds as jacobi_eig.  On return *Aout / *Qout
-// point at the buffers holding the diagonalised matrix and the eigenvectors;
-// sflag[0] = sweeps.
-__device__ void jacobi_eig_1s(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* csn,
-                              int* sflag, int nimp, double** Aout, double** Qout) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ double fro_part[32];
-  double f = 0.0;
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
-    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
-    const double v = A[i * lds + j];
-    f = fma(v, v, f);
-  }
-  f = warp_sum(f);
-  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
-  __syncthreads();
-  double fro = 0.0;
-  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
-  fro = sqrt(fro);
-  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
-  *Aout = A; *Qout = Q;
-  if (tid == 0) sflag[0] = 0;
-  if (b == 1) { __syncthreads(); return; }
-  const int bb = b + (b & 1);
-  // rotation tables indexed by the smaller index p of a pair: csn[2][2*BMAX]
-  double* cur = csn;
-  double* nxt = csn + 2 * PDSDP_BMAX;
-  // rotations of round 0
-  int any = 0;
-  for (int p = tid; p < b; p += nt) {
-    const int q = jac_partner(p, 0, bb);
-    double c = 1.0, sn = 0.0;
-    if (p < q && q < b) jac_rot(A[p * lds + p], A[q * lds + q], A[p * lds + q], (p < nimp) ? thr_imp : thr_guard, c, sn);
-    if (sn != 0.0) any = 1;
-    cur[2 * p] = c; cur[2 * p + 1] = sn;
-  }
-  any = __syncthreads_or(any);
-  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
-  int sweeps = 0, sweep_any = any;
-  for (int it = 0; it < 40 * (bb - 1); ++it) {
-    const int t = it % (bb - 1);
-    const int t1 = (t + 1) % (bb - 1);
-    int nany = 0;
-    for (int e = tid; e < 2 * b * b; e += nt) {
-      const bool isQ = e >= b * b;
-      const int ee = isQ ? e - b * b : e;
-      const int i = ee / b, j = ee % b;
-      // column coefficients (J[.][j])
-      const int pj = jac_partner(j, t, bb);
-      double cj0 = 1.0, cj1 = 0.0;       // J[j][j], J[pj][j]
-      if (pj < b) {
-        const int pp = min(j, pj);
-        const double c = cur[2 * pp], sn = cur[2 * pp + 1];
-        cj0 = c;
-        cj1 = (j == pp) ? -sn : sn;
-      }
-      if (isQ) {
-        const double v = cj0 * Qc[i * lds + j] + ((pj < b) ? cj1 * Qc[i * lds + pj] : 0.0);
-        Qn[i * lds + j] = v;
-        continue;
-      }
-      const int pi = jac_partner(i, t, bb);
-      double ri0 = 1.0, ri1 = 0.0;       // J[i][i], J[pi][i]
-      if (pi < b) {
-        const int pp = min(i, pi);
-        const double c = cur[2 * pp], sn = cur[2 * pp + 1];
-        ri0 = c;
-        ri1 = (i == pp) ? -sn : sn;
-      }
-      auto elem = [&](int ii, int jj) {
-        const int pii = jac_partner(ii, t, bb), pjj = jac_partner(jj, t, bb);
-        double a0 = 1.0, a1 = 0.0, b0 = 1.0, b1 = 0.0;
-        if (pii < b) { const int pp = min(ii, pii); a0 = cur[2 * pp]; a1 = (ii == pp) ? -cur[2 * pp + 1] : cur[2 * pp + 1]; }
-        if (pjj < b) { const int pp = min(jj, pjj); b0 = cur[2 * pp]; b1 = (jj == pp) ? -cur[2 * pp + 1] : cur[2 * pp + 1]; }
-        double v = a0 * (b0 * Ac[ii * lds + jj] + ((pjj < b) ? b1 * Ac[ii * lds + pjj] : 0.0));
-        if (pii < b) v += a1 * (b0 * Ac[pii * lds + jj] + ((pjj < b) ? b1 * Ac[pii * lds + pjj] : 0.0));
-        if (pii == jj && pii < b) {
-          const int pp = min(ii, pii);
-          if (cur[2 * pp + 1] != 0.0) v = 0.0;       // the rotated pair is annihilated
-        }
-        return v;
-      };
-      (void)ri0; (void)ri1;
-      const double v = elem(i, j);
-      An[i * lds + j] = v;
-      // owner of next round's pair (p', q') with p' = i < q' = j forms its rotation
-      const int q1 = jac_partner(i, t1, bb);
-      if (j == q1 && i < j) {
-        const double app = elem(i, i), aqq = elem(j, j);
-        double c, sn;
-        jac_rot(app, aqq, v, (i < nimp) ? thr_imp : thr_guard, c, sn);
-        nxt[2 * i] = c; nxt[2 * i + 1] = sn;
-        if (sn != 0.0) nany = 1;
-      }
-    }
-    // indices whose next partner is the dummy (odd b) or >= b: no rotation
-    for (int p = tid; p < b; p += nt) {
-      const int q = jac_partner(p, t1, bb);
-      if (q >= b && p < q) { nxt[2 * p] = 1.0; nxt[2 * p + 1] = 0.0; }
-    }
-    nany = __syncthreads_or(nany);
-    { double* tmp = Ac; Ac = An; An = tmp; tmp = Qc; Qc = Qn; Qn = tmp; tmp = cur; cur = nxt; nxt = tmp; }
-    if (t == bb - 2) {                  // a full sweep finished
-      ++sweeps;
-      if (!sweep_any) break;
-      sweep_any = nany;                 // rotations already decided for the next sweep's round 0
-    } else {
-      sweep_any |= nany;
-    }
-  }
-  *Aout = Ac; *Qout = Qc;
-  if (tid == 0) sflag[0] = sweeps;
-  __syncthreads();
-}
-
-
 // Fast, deterministic FP64 reciprocal / reciprocal square root: hardware
 // approximation + Newton steps (full double accuracy to within a few ulp).
 __device__ __forceinline__ double fast_rcp(double x) {
@@ -532,10 +76,14 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return r;
 }
 
-// Same contract and arithmetic as chol_scaled_1s, with a fixed thread map:
-// thread (i, p) owns row i and the columns k = j+1+p, j+1+p+P, ... of each
-// step j (P = blockDim / b parts per row): no per-element index division and
-// one barrier per step.
+// In-place Cholesky G = L L^T (lower) of an SPD matrix scaled to unit
+// diagonal first: G' = D G D, D = diag(G)^-1/2.  On exit G holds L' (lower,
+// upper triangle zeroed) and dsc[i] = D_ii.  Returns false on breakdown.
+// One __syncthreads per column: step j updates the trailing columns from the
+// (final) column j without normalising it; the normalisation happens once at
+// the end.  Fixed thread map: thread (i, p) owns row i and the columns
+// k = j+1+p, j+1+p+P, ... of each step j (P = blockDim / b parts per row), so
+// there is no per-element index division.
 __device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
   // every caller passes shared-memory workspaces: LDS/STS, not generic loads
   G = as_shared(G);
@@ -573,7 +121,7 @@ __device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
   return true;
 }
 
-// X = L^{-1} (lower) as tri_inv_lower_1s, with the fixed (row, part) thread map.
+// X = L^{-1} (lower triangular), one barrier per column, with the fixed (row, part) thread map.
 __device__ void tri_inv_lower_rows(const double* L, double* X, int b, int lds) {
   // every caller passes shared-memory workspaces: LDS/STS, not generic loads
   L = as_shared(L);
@@ -599,138 +147,26 @@ __device__ void tri_inv_lower_rows(const double* L, double* X, int b, int lds) {
   __syncthreads();
 }
 
-// Two-barrier-per-round cyclic Jacobi: (1) one thread per pair forms the
-// rotation from a precomputed pairing table, (2) every thread forms its
-// elements of J^T A J and Q J in one pass into ping-pong buffers.  The
-// rotation only needs to be an exact orthogonal matrix (c^2 + s^2 = 1 to
-// rounding); residual off-diagonals are removed by later sweeps.
-// Thresholds as jacobi_eig.  tab: >= (bb-1) * bb ints of scratch.
-__device__ void jacobi_eig2(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
-                            int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ double fro_part[32];
-  double f = 0.0;
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
-    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
-    const double v = A[i * lds + j];
-    f = fma(v, v, f);
-  }
-  f = warp_sum(f);
-  if ((tid & 31) == 0) fro_part[tid >> 5] = f;
-  const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
-  // pairing table: tab[t * bb + i] = partner of i in round t (>= b: none)
-  for (int e = tid; e < R * bb; e += nt) {
-    const int t = e / bb, j = e % bb;
-    if (j < np) {
-      const int t0 = j, t1 = bb - 1 - j;
-      const int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + t) % R;
-      const int q = 1 + (t1 - 1 + t) % R;
-      tab[t * bb + p] = q;
-      tab[t * bb + q] = p;
-    }
-  }
-  __syncthreads();
-  double fro = 0.0;
-  for (int w = 0; w < (int)(nt >> 5); ++w) fro += fro_part[w];
-  fro = sqrt(fro);
-  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
-  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
-  int sweeps = 0;
-  if (b > 1) {
-    for (int sweep = 0; sweep < 40; ++sweep) {
-      int any = 0;
-      for (int t = 0; t < R; ++t) {
-        const int* pt = tab + t * bb;
-        // (1) rotations, indexed by the smaller index of each pair
-        for (int p = tid; p < b; p += nt) {
-          const int q = pt[p];
-          if (p < q) {
-            double c = 1.0, sn = 0.0;
-            if (q < b) {
-              const double apq = Ac[p * lds + q];
-              if (fabs(apq) > ((p < nimp) ? thr_imp : thr_guard)) {
-                const double tau = (Ac[q * lds + q] - Ac[p * lds + p]) * fast_rcp(2.0 * apq);
-                const double at = fabs(tau);
-                double tt;
-                if (at < 1e150) {
-                  const double u = fma(tau, tau, 1.0);
-                  tt = fast_rcp(at + u * fast_rsqrt(u));
-                } else {
-                  tt = 0.5 * fast_rcp(at);
-                }
-                tt = (tau >= 0.0) ? tt : -tt;
-                if (!isfinite(tau)) tt = 0.0;
-                c = fast_rsqrt(fma(tt, tt, 1.0));
-                sn = tt * c;
-                if (sn != 0.0) any = 1;
-              }
-            }
-            cs[2 * p] = c;
-            cs[2 * p + 1] = sn;
-          }
-        }
-        __syncthreads();
-        // (2) A' = J^T A J and Q' = Q J, element-wise
-        for (int e = tid; e < 2 * b * b; e += nt) {
-          const bool isQ = e >= b * b;
-          const int ee = isQ ? e - b * b : e;
-          const int i = ee / b, j = ee % b;
-          const int pj = pt[j];
-          double b0 = 1.0, b1 = 0.0;
-          if (pj < b) {
-            const int pp = min(j, pj);
-            b0 = cs[2 * pp];
-            b1 = (j == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
-          }
-          if (isQ) {
-            double v = b0 * Qc[i * lds + j];
-            if (pj < b) v = fma(b1, Qc[i * lds + pj], v);
-            Qn[i * lds + j] = v;
-            continue;
-          }
-          const int pi = pt[i];
-          double a0 = 1.0, a1 = 0.0;
-          if (pi < b) {
-            const int pp = min(i, pi);
-            a0 = cs[2 * pp];
-            a1 = (i == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
-          }
-          double v = b0 * Ac[i * lds + j];
-          if (pj < b) v = fma(b1, Ac[i * lds + pj], v);
-          v *= a0;
-          if (pi < b) {
-            double w = b0 * Ac[pi * lds + j];
-            if (pj < b) w = fma(b1, Ac[pi * lds + pj], w);
-            v = fma(a1, w, v);
-            if (pi == j && cs[2 * min(i, pi) + 1] != 0.0) v = 0.0;   // annihilated pair
-          }
-          An[i * lds + j] = v;
-        }
-        __syncthreads();
-        { double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp; }
-      }
-      ++sweeps;
-      if (!__syncthreads_or(any)) break;
-    }
-  }
-  *Aout = Ac; *Qout = Qc;
-  if (tid == 0) sflag[0] = sweeps;
-  __syncthreads();
-}
-
 
 // Second-order finish of a nearly diagonal A, in place of further Jacobi
 // sweeps: with every off-diagonal entry small against its diagonal gap,
 //   U = I + K,  K_ij = a_ij / (a_jj - a_ii)  (i != j),  columns normalised,
 //   Q <- Q U,   A <- diag(a_jj + sum_i a_ij K_ij),
-// leaves eigenvector errors O(a_ij^2 / gap) (first-order perturbation theory;
-// U is orthonormal to O(K^2)).  Applied only when that is below a tenth of
-// the pair's rotation threshold, so the result meets the same tolerance as
-// the sweeps it replaces; otherwise returns false and changes nothing.  Three
-// barriers instead of b - 1 rounds of two.  An / Qn receive the new A / Q.
+// leaves eigenvector errors O(a_ij^2 / gap) (first-order perturbation theory).
+// K is antisymmetric, so U^T U = I + K^T K: the columns of U are orthogonal
+// only up to the off-diagonal entries of K^T K, which are formed explicitly
+// (three or more nearly equal eigenvalues make them large while every K_ij
+// still passes the entrywise test).  Applied only when the eigenvector error
+// is below a tenth of the pair's rotation threshold and every off-diagonal
+// entry of K^T K is below PDSDP_JAC_PERTURB_ORTH, so the result meets the
+// tolerance of the sweeps it replaces; otherwise returns false (An is
+// scratch then, Ac / Qc / Qn are unchanged).  Three barriers instead of b - 1
+// rounds of two.  An / Qn receive the new A / Q.
 #ifndef PDSDP_JAC_PERTURB
 #define PDSDP_JAC_PERTURB 1
+#endif
+#ifndef PDSDP_JAC_PERTURB_ORTH
+#define PDSDP_JAC_PERTURB_ORTH 1e-14
 #endif
 __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double* An, double* Qn, int b, int lds,
                                       int nimp, double thr_imp, double thr_guard, double* cs) {
@@ -744,7 +180,9 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
       const double a = Ac[lo_ * lds + hi_];
       const double gap = Ac[j * lds + j] - Ac[i * lds + i];
       const double thr = (lo_ < nimp) ? thr_imp : thr_guard;
-      if (fabs(a) <= 1e-3 * fabs(gap)) {
+      if (a == 0.0) {
+        k = 0.0;              // exact zero (e.g. a pair just rotated): nothing to correct, and 0/0 with equal diagonals
+      } else if (fabs(a) <= 1e-3 * fabs(gap)) {
         k = a / gap;
         if (fabs(a) > thr && !(a * a <= 0.1 * thr * fabs(gap))) bad = 1;
       } else if (fabs(a) > thr) {
@@ -756,19 +194,23 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
   if (__syncthreads_or(bad)) return false;
   double* nrm = cs;
   double* lam = cs + PDSDP_BMAX;
-  if (tid < b) {
-    const int j = tid;
-    double s2 = 1.0, l = Ac[j * lds + j];
-    for (int i = 0; i < b; ++i) {
-      if (i == j) continue;
-      const double k = An[i * lds + j];
-      s2 = fma(k, k, s2);
-      l = fma(k, Ac[min(i, j) * lds + max(i, j)], l);
+  // (K^T K)_ij for every column pair: the diagonal gives the column norms,
+  // the off-diagonal entries the loss of orthogonality of U
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e - (e / b) * b;
+    double g = 0.0;
+    for (int l = 0; l < b; ++l) g = fma(An[l * lds + i], An[l * lds + j], g);
+    if (i == j) {
+      double l_ = Ac[j * lds + j];
+      for (int l = 0; l < b; ++l)
+        if (l != j) l_ = fma(An[l * lds + j], Ac[min(l, j) * lds + max(l, j)], l_);
+      nrm[j] = 1.0 / sqrt(1.0 + g);
+      lam[j] = l_;
+    } else if (!(fabs(g) <= PDSDP_JAC_PERTURB_ORTH)) {
+      bad = 1;
     }
-    nrm[j] = 1.0 / sqrt(s2);
-    lam[j] = l;
   }
-  __syncthreads();
+  if (__syncthreads_or(bad)) return false;
   for (int e = tid; e < b * b; e += nt) {
     const int i = e / b, j = e - (e / b) * b;
     double acc = Qc[i * lds + j];
@@ -786,8 +228,12 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
 }
 
 // Parallel-order cyclic Jacobi for the b x b (b <= 64) projected matrix,
-// block-wide.  Same contract and rotations as jacobi_eig2, restructured for
-// latency: per round, thread p (< b) writes the row coefficients (a0, a1) of
+// block-wide: two-sided rotations in round-robin order from a pairing table
+// (tab: >= (bb-1) * bb ints of scratch), ping-pong buffers; on return *Aout /
+// *Qout point at the buffers holding the diagonalised matrix and the
+// eigenvectors, sflag[0] = sweeps.  Pairs touching an index < nimp are rotated
+// down to PDSDP_JAC_TOL_IMP * ||A||_F, the others to PDSDP_JAC_TOL_GUARD.
+// Structured for latency: per round, thread p (< b) writes the row coefficients (a0, a1) of
 // index p -- an unpaired index is its own partner with (1, 0) -- so the
 // element update  A' = J^T A J,  Q' = Q J  is branch-free; thread (i, j0)
 // owns row i and columns j0, j0+8, ... (no index division); a sweep starts
@@ -1064,115 +510,5 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
   __syncthreads();
 }
 
-// Same as jacobi_eig2, executed by warp 0 alone (warp-synchronous).
-__device__ void jacobi_eig2_warp(double* A, double* A2, double* Q, double* Q2, int b, int lds, double* cs,
-                            int* tab, int* sflag, int nimp, double** Aout, double** Qout) {
-  const int tid = threadIdx.x & 31, nt = 32;
-  double f = 0.0;
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
-    Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
-    const double v = A[i * lds + j];
-    f = fma(v, v, f);
-  }
-  f = warp_sum(f);
-  const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
-  // pairing table: tab[t * bb + i] = partner of i in round t (>= b: none)
-  for (int e = tid; e < R * bb; e += nt) {
-    const int t = e / bb, j = e % bb;
-    if (j < np) {
-      const int t0 = j, t1 = bb - 1 - j;
-      const int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + t) % R;
-      const int q = 1 + (t1 - 1 + t) % R;
-      tab[t * bb + p] = q;
-      tab[t * bb + q] = p;
-    }
-  }
-  __syncwarp();
-  const double fro = sqrt(f);
-  const double thr_imp = PDSDP_JAC_TOL_IMP * fro, thr_guard = PDSDP_JAC_TOL_GUARD * fro;
-  double *Ac = A, *An = A2, *Qc = Q, *Qn = Q2;
-  int sweeps = 0;
-  if (b > 1) {
-    for (int sweep = 0; sweep < 40; ++sweep) {
-      int any = 0;
-      for (int t = 0; t < R; ++t) {
-        const int* pt = tab + t * bb;
-        // (1) rotations, indexed by the smaller index of each pair
-        for (int p = tid; p < b; p += nt) {
-          const int q = pt[p];
-          if (p < q) {
-            double c = 1.0, sn = 0.0;
-            if (q < b) {
-              const double apq = Ac[p * lds + q];
-              if (fabs(apq) > ((p < nimp) ? thr_imp : thr_guard)) {
-                const double tau = (Ac[q * lds + q] - Ac[p * lds + p]) * fast_rcp(2.0 * apq);
-                const double at = fabs(tau);
-                double tt;
-                if (at < 1e150) {
-                  const double u = fma(tau, tau, 1.0);
-                  tt = fast_rcp(at + u * fast_rsqrt(u));
-                } else {
-                  tt = 0.5 * fast_rcp(at);
-                }
-                tt = (tau >= 0.0) ? tt : -tt;
-                if (!isfinite(tau)) tt = 0.0;
-                c = fast_rsqrt(fma(tt, tt, 1.0));
-                sn = tt * c;
-                if (sn != 0.0) any = 1;
-              }
-            }
-            cs[2 * p] = c;
-            cs[2 * p + 1] = sn;
-          }
-        }
-        __syncwarp();
-        // (2) A' = J^T A J and Q' = Q J, element-wise
-        for (int e = tid; e < 2 * b * b; e += nt) {
-          const bool isQ = e >= b * b;
-          const int ee = isQ ? e - b * b : e;
-          const int i = ee / b, j = ee % b;
-          const int pj = pt[j];
-          double b0 = 1.0, b1 = 0.0;
-          if (pj < b) {
-            const int pp = min(j, pj);
-            b0 = cs[2 * pp];
-            b1 = (j == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
-          }
-          if (isQ) {
-            double v = b0 * Qc[i * lds + j];
-            if (pj < b) v = fma(b1, Qc[i * lds + pj], v);
-            Qn[i * lds + j] = v;
-            continue;
-          }
-          const int pi = pt[i];
-          double a0 = 1.0, a1 = 0.0;
-          if (pi < b) {
-            const int pp = min(i, pi);
-            a0 = cs[2 * pp];
-            a1 = (i == pp) ? -cs[2 * pp + 1] : cs[2 * pp + 1];
-          }
-          double v = b0 * Ac[i * lds + j];
-          if (pj < b) v = fma(b1, Ac[i * lds + pj], v);
-          v *= a0;
-          if (pi < b) {
-            double w = b0 * Ac[pi * lds + j];
-            if (pj < b) w = fma(b1, Ac[pi * lds + pj], w);
-            v = fma(a1, w, v);
-            if (pi == j && cs[2 * min(i, pi) + 1] != 0.0) v = 0.0;   // annihilated pair
-          }
-          An[i * lds + j] = v;
-        }
-        __syncwarp();
-        { double* tp = Ac; Ac = An; An = tp; tp = Qc; Qc = Qn; Qn = tp; }
-      }
-      ++sweeps;
-      if (!__any_sync(0xffffffffu, any)) break;
-    }
-  }
-  *Aout = Ac; *Qout = Qc;
-  if (tid == 0) sflag[0] = sweeps;
-  __syncwarp();
-}
 
 }  // namespace pdsdp

@@ -53,3 +53,22 @@ def test_gather_summaries_two_ranks_gloo(count):
         assert full.shape == (count, len(FIELDS))
         np.testing.assert_array_equal(full[:, 0], np.arange(count))
         np.testing.assert_array_equal(full[:, 5], 100 + np.arange(count))
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` without a launcher re-executes itself under
+    torch.distributed.run (one process per GPU) and prints ONE JSON line with
+    n_gpus = 2 (CPU check of the launcher path: gloo, no CUDA work)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-check"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["ranks"] == [0, 1]
