@@ -49,7 +49,8 @@ enum {
   PDSDP_OUT_CORR = 9,
   PDSDP_OUT_ED2 = 10,
   PDSDP_OUT_BLOCK = 11,  /* eigen block size b                              */
-  PDSDP_OUT_DONE = 12    /* 1 if the step executed (pdsdp_iterate_many)      */
+  PDSDP_OUT_DONE = 12,   /* 1 if the step executed (pdsdp_iterate_many)      */
+  PDSDP_OUT_ERR = 13     /* 1 if the step needs an eigen block above PDSDP_BLOCK_MAX (continue in dense mode) */
 };
 
 /* One SDP in the reference's general form (problem.py:73-105). */
@@ -108,6 +109,24 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
                        const int32_t* ypar0, const int32_t* flags, int32_t maxpass, int32_t K,
                        const double* conv_thr, const double* stall_thr, double* out,
                        int32_t* steps_done);
+
+/* Dense-iterate mode: the same iteration with X_k held as a dense n x n matrix
+ * and the projection done by a FULL eigendecomposition on the device
+ * (one-sided Jacobi) -- the replacement of the reference's dense fallback
+ * `full_eigen` / `np.linalg.eigh` (symmat.py:158-161), taken by
+ * `truncated_eigen` for n <= 32, 2(r+1) > n or an ARPACK failure
+ * (symmat.py:181-185,200-207) and by `proj_psd` of the exact solver
+ * (symmat.py:223-226, pdhg.py:166-174).  pdsdp_iterate_many leaves a step
+ * unfinished (slot 13 of its outputs set, steps_done excludes it, X_k / y_k
+ * intact) when the projection argument has more positive eigenvalues than an
+ * eigen block of PDSDP_BLOCK_MAX holds; pdsdp_dense_begin(from_factored = 1)
+ * then expands X_k = F diag(lam) F^T and the solve continues with
+ * pdsdp_iterate_dense (one iteration per call, any r <= n; same output slots;
+ * slot 4 = Jacobi sweeps).  from_factored = 0 starts from X_0 = 0
+ * (solve_pd_sdp with n > PDSDP_BLOCK_MAX, op-level aproj_psd).  pdsdp_reset
+ * leaves dense mode.  pdsdp_objective / pdsdp_download_x follow the mode. */
+int pdsdp_dense_begin(pdsdp_batch* b, int inst, int from_factored);
+int pdsdp_iterate_dense(pdsdp_batch* b, int inst, int32_t r, int32_t ypar, double* out);
 
 /* tr(C X) (lowrank.py:159,168,191) for X = the newest iterate (which = 0)
  * or the previous one (which = 1). */

@@ -350,8 +350,10 @@ __device__ __forceinline__ void bulk_multicast(void* dst_smem, const void* src_g
                " [%0], [%1], %2, [%3], %4;"
                ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(mb)), "h"(mask) : "memory");
 }
-__device__ __forceinline__ void cluster_sync_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+// Cluster barrier with release / acquire semantics: this CTA's reads of its
+// staging buffer happen-before the other CTAs' next multicast writes into it.
+__device__ __forceinline__ void cluster_sync_relacq() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
@@ -758,10 +760,11 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     else own_gather<false, NI>(zcol, zval, ys, R0, R1, cq, ys_, ep, ee, zacc);
     g0 = g1;
     prof_tick(pf, 22);
-    // the staging buffer is reused by the next group: an execution barrier
-    // only (nothing written since the step's barrier needs publishing), so
-    // the arrive is relaxed -- no release fence draining this SM's stores
-    if (g0 < C) cluster_sync_relaxed();
+    // the staging buffer is reused by the next group: the arrive must have
+    // release semantics so that this CTA's shared-memory reads of the group
+    // are ordered before the other CTAs' multicast writes of the next one
+    // (a relaxed arrive orders nothing: write-after-read race)
+    if (g0 < C) cluster_sync_relacq();
     prof_mark(pf, 3);
   }
   if ((cq >> 2) & 1) {        // own_gather kept this thread's chunk halves swapped

@@ -17,6 +17,7 @@
 
 #include "../../include/pdsdp_b200.h"
 #include "common.cuh"
+#include "dense_path.cuh"
 #include "iterate.cuh"
 #include "opnorm.cuh"
 #include "residual.cuh"
@@ -82,6 +83,12 @@ struct Instance {
   double* d_packed = nullptr;   // scratch packed vector (op-level maps)
   long long zl_age = 1LL << 40;  // iterations since the last lambda_max(Z) estimate
   long long P = 0;
+  // dense-iterate mode (dense_path.cuh): X_k as a dense n x n matrix, full eigendecomposition
+  int dense_mode = 0;
+  int dcur = 0;                  // dd.X[dcur] holds X_k
+  void* dense_mem = nullptr;
+  DenseDev dd{};
+  double* d_rowt = nullptr;      // per-row scratch of the dense kernels
 };
 
 }  // namespace
@@ -516,6 +523,44 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds, int step0, int nsteps) {
   return PDSDP_OK;
 }
 
+
+// ---- dense-iterate mode (dense_path.cuh) ----
+#define DENSE_GRID 512
+
+int dense_alloc(Instance* I) {
+  if (I->dense_mem) return PDSDP_OK;
+  const size_t n = I->n, nn = n * n;
+  if (2 * n * sizeof(double) > 220 * 1024)
+    return fail(PDSDP_ENOMEM, "dense eigensolver stages two matrix rows in shared memory: n <= 14080");
+  const size_t rowt = std::max<size_t>(std::max<size_t>(3 * (size_t)I->mp, 2 * n), 2 * (size_t)PDSDP_NDMAX * n) + 16;
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += (b + 255) & ~size_t(255); };
+  add(nn * 8); add(nn * 8); add(nn * 8); add(n * 8); add(n * 8); add(n * 4); add(n * 8);
+  add(4 * DENSE_PART_MAX * 8); add(DENSE_SCAL * 8); add(64); add(rowt * 8);
+  CK(cudaMalloc(&I->dense_mem, bytes + 4096));
+  CK(cudaMemset(I->dense_mem, 0, bytes + 4096));
+  Arena a{(char*)I->dense_mem, 0, bytes + 4096};
+  DenseDev& D = I->dd;
+  D.n = I->n;
+  D.X[0] = a.take<double>(nn - 2); D.X[1] = a.take<double>(nn - 2); D.W = a.take<double>(nn - 2);
+  D.lam = a.take<double>(n); D.lams = a.take<double>(n); D.idx = a.take<int>(n); D.rowsum = a.take<double>(n);
+  D.part = a.take<double>(4 * DENSE_PART_MAX); D.scal = a.take<double>(DENSE_SCAL);
+  D.rot = a.take<unsigned>(4);
+  I->d_rowt = a.take<double>(rowt - 2);
+  return PDSDP_OK;
+}
+
+int dense_objective(pdsdp_batch* b, Instance* I, int which, double* out) {
+  const DenseDev& D = I->dd;
+  dense_objective_kernel<<<DENSE_GRID, 256, 0, b->stream>>>(I->n, (int)I->nz, I->desc.zrow, I->desc.zcol, I->desc.cval,
+                                                           D.X[which ? (I->dcur ^ 1) : I->dcur], D.part);
+  reduce_sum_kernel<<<1, 256, 0, b->stream>>>(D.part, DENSE_GRID, D.scal + DS_DENSE);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, D.scal + DS_DENSE, sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return PDSDP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -608,6 +653,7 @@ int pdsdp_batch_destroy(pdsdp_batch* b) {
   if (b->stream) cudaStreamSynchronize(b->stream);
   for (Instance* I : b->inst) {
     if (I->dmem) cudaFree(I->dmem);
+    if (I->dense_mem) cudaFree(I->dense_mem);
     delete I;
   }
   if (b->h_out) cudaFreeHost(b->h_out);
@@ -705,6 +751,7 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed) {
   Instance* I = b->inst[inst];
   I->bmax = 0;
   I->zl_age = 1LL << 40;
+  I->dense_mode = 0;
   CK(cudaMemsetAsync(I->desc.st, 0, sizeof(State), b->stream));
   CK(cudaMemsetAsync(I->desc.V, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
   CK(cudaMemsetAsync(I->desc.F, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
@@ -810,10 +857,12 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     for (int j = 0; j < K; ++j) {
       const double* src = b->h_out + ((size_t)insts[a] * PDSDP_KMAX + j) * PDSDP_OUT_LEN;
       memcpy(out + ((size_t)a * K + j) * PDSDP_OUT_LEN, src, PDSDP_OUT_LEN * sizeof(double));
+      // a step whose projection argument has more positive eigenvalues than an
+      // eigen block holds did not complete (O_ERR set, X_k / y_k intact): the
+      // steps before it count, the caller continues in dense mode
+      // (pdsdp_dense_begin / pdsdp_iterate_dense)
+      if (src[O_ERR] != 0.0) break;
       if (src[O_DONE] == 1.0) done = j + 1;
-      if (src[O_ERR] != 0.0)
-        return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + ": S has more positive eigenvalues than an eigen block of " +
-                                     std::to_string(PDSDP_BMAX) + " holds (PDSDP_BMAX)");
     }
     if (steps_done) steps_done[a] = done;
     b->inst[insts[a]]->zl_age += done;
@@ -879,6 +928,7 @@ int pdsdp_objective(pdsdp_batch* b, int inst, int which, double* out) {
   int rc = check_inst(b, inst);
   if (rc) return rc;
   if (!out) return fail(PDSDP_EINVAL, "out is NULL");
+  if (b->inst[inst]->dense_mode) return dense_objective(b, b->inst[inst], which, out);
   b->h_active[0] = inst;
   CK(cudaMemcpyAsync(b->d_active, b->h_active, sizeof(int), cudaMemcpyHostToDevice, b->stream));
   objective_kernel<<<dim3(148, 1), 256, 0, b->stream>>>(b->d_insts, b->d_active, which ? 1 : 0, b->d_objpart,
@@ -896,6 +946,10 @@ int pdsdp_download_x(pdsdp_batch* b, int inst, int which, double* packed_out) {
   Instance* I = b->inst[inst];
   const long long P = I->P;
   const int grid = (int)std::min<long long>(148 * 8, (P + 255) / 256);
+  if (I->dense_mode)
+    dense_pack_kernel<<<dim3(std::max(1, std::min(8, (I->n + 255) / 256)), I->n), 256, 0, b->stream>>>(
+        I->n, I->dd.X[which ? (I->dcur ^ 1) : I->dcur], I->d_packed);
+  else
   pack_kernel<<<std::max(grid, 1), 256, 0, b->stream>>>(b->d_insts, inst, which ? 1 : 0, I->d_packed);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(packed_out, I->d_packed, P * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
@@ -967,6 +1021,123 @@ int pdsdp_apply_M_adjoint(pdsdp_batch* b, int inst, const double* y, double* out
   return PDSDP_OK;
 }
 
+int pdsdp_dense_begin(pdsdp_batch* b, int inst, int from_factored) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  Instance* I = b->inst[inst];
+  if ((rc = dense_alloc(I))) return rc;
+  DenseDev& D = I->dd;
+  const size_t nn = (size_t)I->n * I->n;
+  I->dcur = 0;
+  if (from_factored) {
+    // X_k = F diag(lamF) F^T of the last (possibly unfinished) cluster iteration
+    State h;
+    CK(cudaMemcpyAsync(&h, I->desc.st, sizeof(State), cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+    const int nt = (I->n + RECON_TILE - 1) / RECON_TILE;
+    recon_kernel<<<nt * (nt + 1) / 2, 256, 0, b->stream>>>(I->n, I->desc.F, 1, I->desc.ld, nullptr,
+                                                          I->desc.st->lamF, nullptr, h.rF_used, D.X[0]);
+    CK(cudaGetLastError());
+  } else {
+    CK(cudaMemsetAsync(D.X[0], 0, nn * sizeof(double), b->stream));
+  }
+  CK(cudaMemsetAsync(D.X[1], 0, nn * sizeof(double), b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  I->dense_mode = 1;
+  return PDSDP_OK;
+}
+
+int pdsdp_iterate_dense(pdsdp_batch* b, int inst, int32_t r, int32_t ypar, double* out) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  Instance* I = b->inst[inst];
+  if (!I->dense_mode) return fail(PDSDP_EINVAL, "instance is not in dense mode (pdsdp_dense_begin)");
+  if (!out) return fail(PDSDP_EINVAL, "out is NULL");
+  const int n = I->n, mp = I->mp;
+  if (r < 1 || r > n) return fail(PDSDP_EINVAL, "rank r=" + std::to_string(r) + " outside [1, " + std::to_string(n) + "]");
+  DenseDev& D = I->dd;
+  Inst d = I->desc;
+  cudaStream_t s = b->stream;
+  const double* Xo = D.X[I->dcur];
+  double* Xn = D.X[I->dcur ^ 1];
+  const double* yk = (ypar & 1) ? d.ybuf1 : d.ybuf0;
+  double* yn = (ypar & 1) ? d.ybuf0 : d.ybuf1;
+  const double* zv = (ypar & 1) ? d.zbuf1 : d.zbuf0;
+  double* zvn = (ypar & 1) ? d.zbuf0 : d.zbuf1;
+  const int gx = std::max(1, std::min(8, (n + 255) / 256));
+  // S = X_k - alpha (C + M^T y_k), shifted to SPD
+  dense_arg_kernel<<<dim3(gx, n), 256, 0, s>>>(n, Xo, D.W, d.alpha, d.nd, d.du, yk, d);
+  if (d.nz) dense_arg_sparse_kernel<<<std::max(1, std::min(4096, (d.nz + 255) / 256)), 256, 0, s>>>(n, d.nz, d.zrow, d.zcol, zv, D.W, d.alpha);
+  dense_rowabs_kernel<<<(n + 7) / 8, 256, 0, s>>>(n, D.W, D.rowsum);
+  dense_shift_kernel<<<1, 256, 0, s>>>(n, D.W, D.rowsum, D.scal);
+  CK(cudaGetLastError());
+  // full eigendecomposition: one-sided Jacobi sweeps until no rotation is applied
+  const int nn = n + (n & 1);
+  const size_t jsm = (size_t)2 * n * sizeof(double);
+  CK(cudaFuncSetAttribute(jacobi_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(jsm, 1024)));
+  const double tol = std::max(1e-15, 2.0 * 2.220446049250313e-16 * std::sqrt((double)n));
+  int sweeps = 0, conv = (n == 1) ? 1 : 0;
+  for (; n > 1 && sweeps < 60 && !conv; ++sweeps) {
+    CK(cudaMemsetAsync(D.rot, 0, sizeof(unsigned), s));
+    for (int t = 0; t < nn - 1; ++t) jacobi_round_kernel<<<nn / 2, DENSE_THREADS, jsm, s>>>(n, D.W, t, tol, D.rot);
+    CK(cudaGetLastError());
+    unsigned rot = 0;
+    CK(cudaMemcpyAsync(&rot, D.rot, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    b->n_launch += nn - 1;
+    if (rot == 0) conv = 1;
+  }
+  eig_finalize_kernel<<<n, 256, 0, s>>>(n, D.W, D.scal, D.lam);
+  eig_sort_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, D.lam, D.idx, D.lams);
+  eig_select_kernel<<<1, 32, 0, s>>>(n, r, D.lams, D.scal);
+  // X+ = sum of the kept positive pairs (symmat.py:212-220)
+  const int nt = (n + RECON_TILE - 1) / RECON_TILE;
+  recon_kernel<<<nt * (nt + 1) / 2, 256, 0, s>>>(n, D.W, n, 1, D.idx, D.lams, D.scal, 0, Xn);
+  CK(cudaGetLastError());
+  // dual step, adjoint, residuals
+  double* rowt = I->d_rowt;
+  CK(cudaMemsetAsync(D.scal + DS_ED2, 0, 5 * sizeof(double), s));
+  if (d.nd > 0) {
+    dense_quad_kernel<<<n, 256, 0, s>>>(n, Xn, Xo, d.nd, d.du, rowt);
+    for (int q = 0; q < d.nd; ++q) {
+      reduce_sum_kernel<<<1, 256, 0, s>>>(rowt + (size_t)(2 * q) * n, n, D.scal + DS_QN + q);
+      reduce_sum_kernel<<<1, 256, 0, s>>>(rowt + (size_t)(2 * q + 1) * n, n, D.scal + DS_QD + q);
+    }
+  }
+  if (mp > 0) {
+    dense_dual_kernel<<<std::max(1, std::min(2048, (mp + 255) / 256)), 256, 0, s>>>(d, Xn, Xo, yk, yn, D.scal, rowt);
+    reduce_sum_kernel<<<1, 256, 0, s>>>(rowt, mp, D.scal + DS_ED2);
+    reduce_sum_kernel<<<1, 256, 0, s>>>(rowt + mp, mp, D.scal + DS_DYSD);
+    reduce_sum_kernel<<<1, 256, 0, s>>>(rowt + 2 * (size_t)mp, mp, D.scal + DS_FIN);
+    dense_adjoint_kernel<<<DENSE_GRID, 256, 0, s>>>(d, Xn, Xo, yn, zvn, D.part);
+    reduce_sum_kernel<<<1, 256, 0, s>>>(D.part, DENSE_GRID, D.scal + DS_CORR);
+  }
+  dense_presid_kernel<<<n, 256, 0, s>>>(d, Xn, Xo, rowt);
+  reduce_sum_kernel<<<1, 256, 0, s>>>(rowt, n, D.scal + DS_DENSE);
+  reduce_sum_kernel<<<1, 256, 0, s>>>(rowt + n, n, D.scal + DS_ROT);
+  CK(cudaGetLastError());
+  double h[DENSE_SCAL];
+  CK(cudaMemcpyAsync(h, D.scal, DENSE_SCAL * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  b->n_launch += 16;
+  I->dcur ^= 1;
+  for (int k = 0; k < PDSDP_OUT_LEN; ++k) out[k] = 0.0;
+  const double fin = (h[DS_FIN] == 0.0 && h[DS_ROT] == 0.0 && h[DS_XFIN] == 1.0) ? 1.0 : 0.0;
+  out[O_EPS_P] = std::sqrt(std::max(h[DS_DENSE] + h[DS_CORR], 0.0));
+  out[O_EPS_D] = std::sqrt(std::max(h[DS_ED2], 0.0));
+  out[O_LAM] = h[DS_LAMK];
+  out[O_FIN] = fin;
+  out[O_PASSES] = sweeps;
+  out[O_EIGCONV] = conv;
+  out[O_DENSE] = h[DS_DENSE];
+  out[O_CORR] = h[DS_CORR];
+  out[O_ED2] = h[DS_ED2];
+  out[O_BLK] = n;
+  out[O_DONE] = 1.0;
+  out[O_DENSE_EXACT] = NAN;
+  return PDSDP_OK;
+}
+
 int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_packed_out, double* lambda_out) {
   if (n < 1 || !S_packed || !P_packed_out) return fail(PDSDP_EINVAL, "bad aproj arguments");
   if (r < 1 || r > n) return fail(PDSDP_EINVAL, "rank r=" + std::to_string(r) + " outside [1, " + std::to_string(n) + "]");
@@ -984,7 +1155,15 @@ int pdsdp_aproj_psd(int32_t n, const double* S_packed, int32_t r, double* P_pack
   double out[PDSDP_OUT_LEN];
   rc = pdsdp_set_alpha(b, 0, 1.0);
   if (!rc) rc = pdsdp_reset(b, 0, 0.0);
-  if (!rc) rc = pdsdp_iterate(b, 1, &inst, &rr, &yp, &fl, 200, out);
+  // the top r+1 pairs fit an eigen block: subspace iteration in one cluster;
+  // otherwise the full eigendecomposition (the reference switches to dense
+  // eigh for 2 (r+1) > n, symmat.py:181-185)
+  if (std::min(r + 1, n) <= PDSDP_BMAX) {
+    if (!rc) rc = pdsdp_iterate(b, 1, &inst, &rr, &yp, &fl, 200, out);
+  } else {
+    if (!rc) rc = pdsdp_dense_begin(b, 0, 0);
+    if (!rc) rc = pdsdp_iterate_dense(b, 0, rr, yp, out);
+  }
   if (!rc) rc = pdsdp_download_x(b, 0, 0, P_packed_out);
   if (!rc && lambda_out) *lambda_out = out[PDSDP_OUT_LAMBDA];
   std::string e = g_err;

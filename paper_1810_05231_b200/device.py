@@ -23,6 +23,7 @@ OUT_EPS_P, OUT_EPS_D, OUT_LAMBDA, OUT_FINITE = 0, 1, 2, 3
 OUT_PASSES, OUT_MATVECS, OUT_EIGCONV, OUT_EIGRES = 4, 5, 6, 7
 OUT_BLOCK = 11
 OUT_DONE = 12
+OUT_ERR = 13
 OUT_DENSE = 8
 OUT_DENSE_EXACT = 14
 BLOCK_MAX = 64
@@ -37,6 +38,7 @@ EXPORTED = (
     "pdsdp_apply_M", "pdsdp_apply_M_adjoint", "pdsdp_aproj_psd", "pdsdp_strerror",
     "pdsdp_last_error", "pdsdp_version", "pdsdp_set_timing", "pdsdp_kernel_times",
     "pdsdp_debug", "pdsdp_iterate_many", "pdsdp_set_verify_residual",
+    "pdsdp_dense_begin", "pdsdp_iterate_dense",
 )
 
 
@@ -88,6 +90,8 @@ def load_library(path: str = LIB_PATH):
             "pdsdp_set_verify_residual": (ct.c_int, [P, ct.c_int]),
             "pdsdp_debug": (ct.c_int, [P, ct.c_int, P]),
             "pdsdp_iterate_many": (ct.c_int, [P, ct.c_int, P, P, P, P, I32, I32, P, P, P, P]),
+            "pdsdp_dense_begin": (ct.c_int, [P, ct.c_int, ct.c_int]),
+            "pdsdp_iterate_dense": (ct.c_int, [P, ct.c_int, I32, I32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -228,6 +232,16 @@ class DeviceBatch:
                                            _ptr(fl), int(maxpass), int(K), _ptr(conv), _ptr(stall),
                                            _ptr(out), _ptr(done)))
         return out, done
+
+    def dense_begin(self, inst: int, from_factored: bool):
+        """Switch an instance to the dense-iterate path (full device
+        eigendecomposition): X_k expanded from its factors, or X_0 = 0."""
+        _check(self.lib.pdsdp_dense_begin(self.h, inst, 1 if from_factored else 0))
+
+    def iterate_dense(self, inst: int, r: int, ypar: int) -> np.ndarray:
+        out = np.zeros(OUT_LEN)
+        _check(self.lib.pdsdp_iterate_dense(self.h, inst, int(r), int(ypar), _ptr(out)))
+        return out
 
     def objective(self, inst: int, which: int = 0) -> float:
         v = np.zeros(1)

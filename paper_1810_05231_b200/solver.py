@@ -33,8 +33,8 @@ from .config import (
     update_rank,
 )
 from .device import (
-    KMAX, OUT_EIGCONV, OUT_EPS_D, OUT_EPS_P, OUT_FINITE, OUT_LAMBDA, OUT_MATVECS, OUT_PASSES,
-    DeviceBatch,
+    BLOCK_MAX, KMAX, OUT_EIGCONV, OUT_EPS_D, OUT_EPS_P, OUT_ERR, OUT_FINITE, OUT_LAMBDA, OUT_MATVECS,
+    OUT_PASSES, DeviceBatch,
 )
 from .layout import SymMatrix, approx_error_bound
 from .model import SdpProblem, as_problem
@@ -179,6 +179,36 @@ class _InstanceRun:
         self.scale = 1.0
         self.k = 1
         self.eig_passes = self.eig_matvecs = self.eig_unconverged = 0
+        self.dense = False     # dense-iterate mode (full device eigendecomposition)
+        self.dense_from = None
+
+    def enter_dense(self) -> None:
+        """The projection argument has more positive eigenvalues than an eigen
+        block holds (the unfinished step left X_k, y_k intact): continue with
+        the full eigendecomposition, as the reference's dense fallback does
+        (``symmat.py:181-185``)."""
+        logger.info("k=%d (r=%d): eigen block limit reached, continuing with the dense device eigensolver",
+                    self.k, self.controller.r)
+        self.batch.dense_begin(self.inst, True)
+        self.dense = True
+        self.dense_from = self.k
+
+    def step(self, chunk: int) -> None:
+        """Run the next chunk of iterations of this instance alone."""
+        if self.dense:
+            out = self.batch.iterate_dense(self.inst, self.controller.r, self.it.ypar)
+            self.consume([out], 1)
+        else:
+            K = self.max_chunk(chunk)
+            conv, stall = self.thresholds(K)
+            outs, done = self.batch.iterate_many([self.inst], [self.controller.r], [self.it.ypar], K, [conv], stall)
+            self.after_chunk(outs[0], int(done[0]), K)
+        self.check_time()
+
+    def after_chunk(self, outs, done: int, K: int) -> None:
+        self.consume(outs, done)
+        if self.status is None and done < K and outs[done][OUT_ERR] != 0.0:
+            self.enter_dense()
 
     def max_chunk(self, chunk: int) -> int:
         """Steps the device may run before the host must look: the first
@@ -208,12 +238,14 @@ class _InstanceRun:
             if out[OUT_FINITE] == 1.0:
                 ec = float(out[OUT_EPS_P]) + float(out[OUT_EPS_D])
                 sc = (1.0 + ec) if (self.k == 1 and c.relative_residuals) else self.scale
-                if ec <= c.eps_tol * sc:
+                if ec <= c.eps_tol * sc and not self.dense:
                     # checkpoint iteration: the certificate needs lambda_{r+1} to the
                     # reference's accuracy; re-run this iteration from the same
                     # (X_k, y_k) with the certificate eigenpair converged too
                     assert j == done - 1, "device chunk ran past a checkpoint"
                     out = self.batch.iterate([self.inst], [ctl.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
+                    if out[OUT_ERR] != 0.0:
+                        raise RuntimeError("certificate re-run exceeded the eigen block limit")
                     self.eig_passes += int(out[OUT_PASSES])
                     self.eig_matvecs += int(out[OUT_MATVECS])
             if out[OUT_EIGCONV] == 0:
@@ -280,11 +312,7 @@ def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverC
     run = _InstanceRun(batch, inst, prob, config, alpha, callback,
                        time.perf_counter() if t0 is None else t0)
     while run.status is None:
-        K = run.max_chunk(chunk)
-        conv, stall = run.thresholds(K)
-        outs, done = batch.iterate_many([inst], [run.controller.r], [run.it.ypar], K, [conv], stall)
-        run.consume(outs[0], int(done[0]))
-        run.check_time()
+        run.step(chunk)
     return run.outcome()
 
 
@@ -297,8 +325,13 @@ def run_lr_batch(batch: DeviceBatch, insts, config: SolverConfig, alphas,
     t0 = time.perf_counter() if t0 is None else t0
     runs = [_InstanceRun(batch, i, batch.problems[i], config, a, None, t0) for i, a in zip(insts, alphas)]
     while True:
-        live = [r for r in runs if r.status is None]
+        for r in runs:                     # instances on the dense path step alone
+            if r.status is None and r.dense:
+                r.step(chunk)
+        live = [r for r in runs if r.status is None and not r.dense]
         if not live:
+            if any(r.status is None for r in runs):
+                continue
             break
         K = min(r.max_chunk(chunk) for r in live)
         convs, stalls = [], []
@@ -309,7 +342,7 @@ def run_lr_batch(batch: DeviceBatch, insts, config: SolverConfig, alphas,
         outs, done = batch.iterate_many([r.inst for r in live], [r.controller.r for r in live],
                                         [r.it.ypar for r in live], K, convs, np.concatenate(stalls))
         for a, r in enumerate(live):
-            r.consume(outs[a], int(done[a]))
+            r.after_chunk(outs[a], int(done[a]), K)
             r.check_time()
     return [r.outcome() for r in runs]
 
@@ -369,11 +402,11 @@ def solve_lr_pd_sdp_batch(problems, config: SolverConfig | None = None) -> list:
 
 # ---------------------------------------------------------------------------
 # Exact PD-SDP (reference pdhg.py:221-288) with the full PSD projection
-# (symmat.py:223-226).  On the device the full projection is the eigen block
-# covering all of R^n (r = n: the Rayleigh-Ritz step is then the complete
-# eigendecomposition), so it is available for n <= PDSDP_BLOCK_MAX; larger n
-# need a full dense eigensolver (not built).
-EXACT_N_MAX = 64
+# (symmat.py:223-226).  For n <= PDSDP_BLOCK_MAX the full projection is the
+# eigen block covering all of R^n (r = n: the Rayleigh-Ritz step is then the
+# complete eigendecomposition, one cluster kernel per iteration); larger n run
+# on the dense-iterate path (csrc/dense_path.cuh: dense X_k in HBM, full
+# one-sided-Jacobi eigendecomposition per iteration).
 
 
 def solve_pd_sdp(
@@ -389,14 +422,14 @@ def solve_pd_sdp(
     config.validate()
     prob = as_problem(prob)
     n = prob.n
-    if n > EXACT_N_MAX:
-        raise ValueError(f"exact projection on the device supports n <= {EXACT_N_MAX} (n={n}); "
-                         "use solve_lr_pd_sdp")
     t0 = time.perf_counter()
     alpha = step_size(prob, config)
     batch = _device_batch(prob)
     batch.set_alpha(0, alpha)
     batch.reset(0, 0.0)
+    dense = n > BLOCK_MAX
+    if dense:
+        batch.dense_begin(0, False)
     it = _DeviceIterate(batch, 0)
     status, res, scale, k = None, (math.nan, math.nan, math.nan), 1.0, 1
     while status is None and k <= config.max_iter:
@@ -404,7 +437,10 @@ def solve_pd_sdp(
         if callback is not None and k > 1:
             K = min(K, config.progress_every - (k - 1) % config.progress_every)
         conv = config.eps_tol * scale if k > 1 else -1.0
-        outs, done = batch.iterate_many([0], [n], [it.ypar], K, [conv], np.full(K, np.inf))
+        if dense:
+            outs, done = [[batch.iterate_dense(0, n, it.ypar)]], [1]
+        else:
+            outs, done = batch.iterate_many([0], [n], [it.ypar], K, [conv], np.full(K, np.inf))
         for j in range(int(done[0])):
             out = outs[0][j]
             if out[OUT_FINITE] != 1.0:                   # pdhg.py:251-253

@@ -44,3 +44,15 @@ def problem_from_golden(d, prefix="") -> SdpProblem:
 @pytest.fixture
 def rng():
     return np.random.default_rng(12345)
+
+
+def dense_case_matrix(n, seed):
+    """Seeded symmetric test matrix of the dense-eigensolver fixtures
+    (tests/golden/make_golden.py make_dense builds the same one): random
+    symmetric plus a few planted large eigenvalues, so kept / clipped /
+    certificate pairs are all present."""
+    rng = np.random.default_rng(seed)
+    R = rng.standard_normal((n, n))
+    S = 0.5 * (R + R.T) / np.sqrt(n)
+    U = rng.standard_normal((n, 5))
+    return S + (U * np.array([4.0, 3.0, 2.5, -3.5, 2.0])) @ U.T / n

@@ -51,6 +51,8 @@ from pdsdp import SdpProblem as RProblem, SparseRow as RRow, SymMatrix as RSym  
 from scipy.sparse.linalg import ArpackError  # noqa: E402
 
 from paper_1810_05231_b200 import workloads  # noqa: E402
+sys.path.insert(0, os.path.dirname(HERE))
+from conftest import dense_case_matrix  # noqa: E402  (seeded matrices shared with the GPU tests)
 
 SKETCH_SEED = 777
 
@@ -366,6 +368,69 @@ def make_pd_small(path):
     np.savez_compressed(path, **out)
 
 
+def make_dense(path):
+    """Reference outputs where its dense eigh path runs (symmat.py:158-161,
+    181-185, 223-226) -- what the device's full eigensolver (dense_path.cuh)
+    is checked against:
+      * aproj_psd at n = 100 / 300 with 2 (r+1) > n or r + 1 above the eigen block;
+      * exact PD-SDP (full projection each iteration) on an n = 100 Max-Cut;
+      * an LR-PD-SDP run whose rank doubling crosses the eigen block limit
+        with more positive eigenvalues than a block holds (equipartition n = 150)."""
+    out = {}
+    zs = np.random.default_rng(SKETCH_SEED).standard_normal((300, 4))
+    for (n, seed, ranks) in ((100, 11, (60, 80, 100)), (300, 12, (100, 200, 300))):
+        S = dense_case_matrix(n, seed)
+        Sp = pdsdp.SymMatrix.from_dense(S)
+        for r in ranks:
+            P, lam = pdsdp.aproj_psd(Sp, r)
+            pre = f"ap_n{n}_r{r}_"
+            Pd = P.to_dense()
+            out[pre + "lam"] = lam
+            out[pre + "fro"] = np.linalg.norm(Pd)
+            out[pre + "diag"] = np.diag(Pd).copy()
+            out[pre + "Pz"] = Pd @ zs[:n]
+            if n == 100:
+                out[pre + "P"] = P.data
+    prob = to_ref(workloads.maxcut_problem(100, 0.1, 0, signed=False))
+    flatten_problem("pd_", prob, out)
+    for K in (1, 10, 50):
+        res = pdsdp.solve_pd_sdp(prob, pdsdp.SolverConfig(eps_tol=1e-4, max_iter=K, time_limit_s=1e9))
+        out[f"pd_X{K}"] = res.X.data
+        out[f"pd_y{K}"] = res.y
+        out[f"pd_res{K}"] = np.array(res.final_residuals)
+    res = pdsdp.solve_pd_sdp(prob, pdsdp.SolverConfig(eps_tol=1e-4, max_iter=5000, time_limit_s=1e9))
+    out["pd_status"] = res.status.value
+    out["pd_iters"] = res.iterations
+    out["pd_X"] = res.X.data
+    out["pd_y"] = res.y
+    out["pd_pobj"] = res.primal_objective
+    out["pd_dobj"] = res.dual_objective
+    out["pd_res"] = np.array(res.final_residuals)
+    print("dense pd", res.status, res.iterations, res.primal_objective)
+    prob = to_ref(workloads.equipartition_problem(150, 0.05, 2))
+    cfg = pdsdp.SolverConfig(eps_tol=1e-4, max_iter=300, initial_rank=70, window_ell=50, time_limit_s=1e9)
+    with LambdaRecorder() as rec:
+        res = pdsdp.solve_lr_pd_sdp(prob, cfg)
+    out["lr_status"] = res.status.value
+    out["lr_iters"] = res.iterations
+    out["lr_X"] = res.X.data
+    out["lr_y"] = res.y
+    out["lr_res"] = np.array(res.final_residuals)
+    out["lr_rank_path"] = np.array(res.rank_path)
+    out["lr_lam"] = np.array(rec.values)
+    out["lr_pobj"] = res.primal_objective
+    w = np.linalg.eigvalsh(res.X.to_dense())
+    out["lr_npos"] = int(np.sum(w > 1e-9 * w.max()))
+    print("dense lr", res.status, res.iterations, res.rank_path, out["lr_npos"])
+    # a Max-Cut whose first projection argument has ~n positive eigenvalues
+    prob = to_ref(workloads.maxcut_problem(200, 0.1, 0, signed=False))
+    res = pdsdp.solve_lr_pd_sdp(prob, pdsdp.SolverConfig(initial_rank=80, max_iter=2, time_limit_s=1e9))
+    out["mc_X"] = res.X.data
+    out["mc_y"] = res.y
+    out["mc_res"] = np.array(res.final_residuals)
+    np.savez_compressed(path, **out)
+
+
 def make_mimo(path):
     """LR-PD-SDP on MIMO relaxations (reference instances.gen_mimo): n+1
     diagonal pins and the box -1 <= X_ij <= 1 as 2 n (n+1) / 2 inequality
@@ -512,6 +577,7 @@ if __name__ == "__main__":
         "cfg1": lambda: make_cfg1(os.path.join(HERE, "cfg1.npz")),
         "pd_small": lambda: make_pd_small(os.path.join(HERE, "pd_small.npz")),
         "mimo": lambda: make_mimo(os.path.join(HERE, "mimo.npz")),
+        "dense": lambda: make_dense(os.path.join(HERE, "dense.npz")),
         "check": lambda: make_check(os.path.join(HERE, "check.npz")),
         "io": lambda: make_io(os.path.join(HERE, "io.npz")),
     }

@@ -80,14 +80,3 @@ def test_packed_layout_round_trip(rng):
         assert A.inner(A) == pytest.approx(np.trace(S @ S))
     with pytest.raises(ValueError, match="not symmetric"):
         svec(np.array([[1.0, 2.0], [0.0, 1.0]]))
-
-
-def test_exact_solver_size_limit_is_loud():
-    """solve_pd_sdp's full projection runs as one eigen block on the device:
-    above the block limit it raises instead of silently falling back."""
-    import pytest
-    import paper_1810_05231_b200 as pk
-    from paper_1810_05231_b200 import workloads
-    prob = workloads.maxcut_problem(80, 0.1, 1, signed=False)
-    with pytest.raises(ValueError, match="n <= 64"):
-        pk.solve_pd_sdp(prob)

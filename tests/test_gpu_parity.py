@@ -280,18 +280,84 @@ def test_target_rank_above_block_uses_positive_part():
         np.testing.assert_allclose(res.final_residuals, ref.final_residuals, rtol=1e-7)
 
 
-def test_rank_above_block_limit_fails_loudly():
-    # S_1 = alpha L / 4 has ~n positive eigenvalues: more than one block holds
-    prob = workloads.maxcut_problem(200, 0.1, 0, signed=False)
-    with pytest.raises(ValueError, match="eigen block"):
-        pk.solve_lr_pd_sdp(prob, SolverConfig(initial_rank=80, max_iter=2))
-    # the same run continued past 62 positive eigenpairs (reference: dense eigh)
+def _unpack(n, v):
+    iu, ju = np.triu_indices(n)
+    w = np.array(v, dtype=float)
+    w[iu != ju] /= np.sqrt(2.0)
+    S = np.zeros((n, n))
+    S[iu, ju] = w
+    S[ju, iu] = w
+    return S
+
+
+@pytest.mark.parametrize("n,seed,ranks", [(100, 11, (60, 80, 100)), (300, 12, (100, 200, 300))])
+def test_dense_eigensolver_aproj_matches_reference(n, seed, ranks):
+    """aproj_psd where the reference takes dense eigh (2 (r+1) > n,
+    symmat.py:181-185) or r + 1 exceeds the in-cluster eigen block: the device
+    runs its full eigendecomposition (dense_path.cuh, one-sided Jacobi).
+    Reference outputs: tests/golden/dense.npz (make_golden.py make_dense)."""
+    from conftest import dense_case_matrix
+    d = load_golden("dense.npz")
+    S = pk.SymMatrix.from_dense(dense_case_matrix(n, seed))
+    zs = np.random.default_rng(777).standard_normal((300, 4))[:n]
+    for r in ranks:
+        pre = f"ap_n{n}_r{r}_"
+        P, lam = pk.aproj_psd(S, r)
+        Pd = _unpack(n, P.data)
+        assert lam == pytest.approx(float(d[pre + "lam"]), abs=1e-10)
+        assert abs(np.linalg.norm(Pd) - float(d[pre + "fro"])) <= 1e-9 * float(d[pre + "fro"])
+        assert rel(np.diag(Pd), d[pre + "diag"]) <= ITER_TOL
+        assert rel(Pd @ zs, d[pre + "Pz"]) <= ITER_TOL
+        if n == 100:
+            assert rel(P.data, d[pre + "P"]) <= ITER_TOL
+
+
+def test_exact_solver_above_block_limit_matches_reference():
+    """solve_pd_sdp with n = 100 > PDSDP_BLOCK_MAX: every iteration is a full
+    projection on the dense-iterate path (reference pdhg.py:221-288 with
+    symmat.py:223-226); iterates at K = 1, 10, 50 and the solve to tolerance."""
+    d = load_golden("dense.npz")
+    prob = problem_from_golden(d, "pd_")
+    for K in (1, 10, 50):
+        res = pk.solve_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=K, time_limit_s=1e9))
+        assert res.iterations == K
+        assert rel(res.X.data, d[f"pd_X{K}"]) <= ITER_TOL
+        assert rel(res.y, d[f"pd_y{K}"]) <= ITER_TOL
+        np.testing.assert_allclose(res.final_residuals, d[f"pd_res{K}"], rtol=1e-6)
+    res = pk.solve_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=5000, time_limit_s=1e9))
+    assert res.status.value == str(d["pd_status"]) == "optimal"
+    assert res.iterations == int(d["pd_iters"])
+    assert res.rank_path == [(0, 100)]
+    assert res.primal_objective == pytest.approx(float(d["pd_pobj"]), rel=OBJ_TOL)
+    assert res.dual_objective == pytest.approx(float(d["pd_dobj"]), rel=OBJ_TOL)
+    assert rel(res.X.data, d["pd_X"]) <= 1e-6
+
+
+def test_rank_above_block_limit_continues_on_dense_path():
+    """An LR run whose projection argument has more positive eigenvalues than
+    an eigen block holds (the reference runs dense eigh there,
+    symmat.py:181-185): the cluster kernel leaves that step unfinished and the
+    solve continues on the dense-iterate path from the same (X_k, y_k)."""
+    d = load_golden("dense.npz")
+    # equipartition n = 150, r0 = 70: rank doubles to 140 / 150, X reaches 84 positive eigenpairs
     prob = workloads.equipartition_problem(150, 0.05, 2)
-    with pytest.raises(ValueError, match="eigen block"):
-        pk.solve_lr_pd_sdp(prob, SolverConfig(eps_tol=1e-4, max_iter=300, initial_rank=70, window_ell=50))
-    # op level: aproj_psd needs lambda_{r+1} itself, so r + 1 must fit the block
-    with pytest.raises(ValueError, match="eigen block"):
-        pk.aproj_psd(pk.SymMatrix.from_dense(np.eye(100)), 80)
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=300, initial_rank=70, window_ell=50, time_limit_s=1e9)
+    res = pk.solve_lr_pd_sdp(prob, cfg)
+    assert res.status.value == str(d["lr_status"])
+    assert res.iterations == int(d["lr_iters"])
+    assert res.rank_path == [tuple(int(v) for v in row) for row in d["lr_rank_path"]]
+    assert int(d["lr_npos"]) > 64
+    assert rel(res.X.data, d["lr_X"]) <= ITER_TOL
+    assert rel(res.y, d["lr_y"]) <= ITER_TOL
+    np.testing.assert_allclose(res.final_residuals, d["lr_res"], rtol=1e-6)
+    assert res.primal_objective == pytest.approx(float(d["lr_pobj"]), rel=OBJ_TOL)
+    # Max-Cut n = 200, r0 = 80: S_1 = alpha L / 4 has ~n positive eigenvalues at the first step
+    prob = workloads.maxcut_problem(200, 0.1, 0, signed=False)
+    res = pk.solve_lr_pd_sdp(prob, SolverConfig(initial_rank=80, max_iter=2, time_limit_s=1e9))
+    assert res.iterations == 2
+    assert rel(res.X.data, d["mc_X"]) <= ITER_TOL
+    assert rel(res.y, d["mc_y"]) <= ITER_TOL
+    np.testing.assert_allclose(res.final_residuals, d["mc_res"], rtol=1e-6)
 
 
 def test_time_limit_and_max_iter_status():
