@@ -33,7 +33,7 @@ extern "C" {
 
 #define PDSDP_BLOCK_MAX 64
 #define PDSDP_OUT_LEN 16
-#define PDSDP_KMAX 64
+#define PDSDP_KMAX 128
 
 /* Output slots of one iteration (doubles, PDSDP_OUT_LEN per instance). */
 enum {
@@ -109,6 +109,22 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
                        const int32_t* ypar0, const int32_t* flags, int32_t maxpass, int32_t K,
                        const double* conv_thr, const double* stall_thr, double* out,
                        int32_t* steps_done);
+
+/* Asynchronous per-instance chunks: the multi-instance analogue of the
+ * reference's sequential bench rows (cli.py:284-329), scheduled on the device.
+ * pdsdp_slots creates (once) as many streams as clusters of the iteration
+ * kernel can be resident and returns that count; pdsdp_chunk_launch enqueues
+ * up to K iterations of ONE instance on a slot (same arguments and pause rules
+ * as pdsdp_iterate_many, stall_thr[K]) and returns at once; pdsdp_chunk_poll
+ * returns 1 when the slot's chunk has finished (0 while running);
+ * pdsdp_chunk_collect waits for it and copies the K * PDSDP_OUT_LEN outputs.
+ * Chunks of different instances run side by side, each pausing at its own
+ * events, so a batch finishes in about the time of its longest solve. */
+int pdsdp_slots(pdsdp_batch* b, int32_t* nslots_out);
+int pdsdp_chunk_launch(pdsdp_batch* b, int32_t slot, int32_t inst, int32_t rank, int32_t ypar0, int32_t flags,
+                       int32_t maxpass, int32_t K, double conv_thr, const double* stall_thr);
+int pdsdp_chunk_poll(pdsdp_batch* b, int32_t slot);
+int pdsdp_chunk_collect(pdsdp_batch* b, int32_t slot, int32_t inst, int32_t K, double* out, int32_t* steps_done);
 
 /* Dense-iterate mode: the same iteration with X_k held as a dense n x n matrix
  * and the projection done by a FULL eigendecomposition on the device

@@ -25,7 +25,7 @@
 #endif
 #define PDSDP_RED_MAX (2 * PDSDP_BMAX * PDSDP_BMAX + 64)
 #define PDSDP_OUT_LEN 16       // doubles per instance and step in the host-mapped output
-#define PDSDP_KMAX 64          // iterations per pdsdp_iterate_many call
+#define PDSDP_KMAX 128         // iterations per pdsdp_iterate_many call
 #define PDSDP_NDMAX 2          // dense rank-one constraint rows handled as vectors
 
 // Eigen block for k = r+1 wanted pairs: k plus max(GUARD_MIN, k / GUARD_DIV)

@@ -64,6 +64,9 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
   // sentinel of an effective-rank block: only its sign matters -- the
   // eigenvalue within its residual must be negative (with margin)
   if (i == r && cert_tol < 0.0) return th < 0.0 && ri <= 0.1 * -th;
+  // op-level aproj_psd returns lambda_{r+1} itself (symmat.py:242-245): the
+  // tight certificate is held to the kept-pair residual whatever its sign
+  if (i == r && cert_tol > 0.0 && cert_tol < PDSDP_TOL_CERT) return ri <= cert_tol * scale;
   // clipped / certificate passes -- only trusted once the pair is nearly
   // invariant (a Ritz value of an unconverged block can sit far below the
   // eigenvalue it will converge to)

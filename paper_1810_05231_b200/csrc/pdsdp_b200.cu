@@ -119,6 +119,10 @@ struct pdsdp_batch {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0, n_launch = 0.0;
   cudaEvent_t tev[PDSDP_KMAX + 1] = {};
+  // asynchronous per-instance chunks (pdsdp_chunk_*): one stream + event per slot
+  std::vector<cudaStream_t> slot_stream;
+  std::vector<cudaEvent_t> slot_event;
+  int* d_ident = nullptr;    // d_ident[i] = i: the active list of a one-instance launch
 };
 
 namespace {
@@ -381,7 +385,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   add(nseg * 4 + 4); add(nseg * 4 + 4); add((I.mp + 1) * 4); add(I.o_mcol.size() * 4 + 4);
   add(I.o_mval.size() * 8 + 8); add(I.o_tptr.size() * 4 + 4); add(I.o_trow.size() * 4 + 4);
   add(I.o_tval.size() * 8 + 8); add(I.tpos.size() * 8 + 8); add(I.mp * 8 + 8); add(nseg * 8 + 8);
-  add(NORM_BLOCKS * 8); add(64); add(4096 * 8);
+  add(2 * NORM_BLOCKS * 8); add(64); add(4096 * 8);
   add((size_t)I.P * 8);
   add(I.du.size() * 8 + 8);
   add((size_t)C * 2 * PDSDP_TRACE_CTA * 8);
@@ -469,7 +473,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   o.x = a.take<double>(I.tpos.size() + 1);
   o.y = a.take<double>(I.mp + 1);
   o.seg_part = a.take<double>(nseg + 1);
-  o.norm_part = a.take<double>(NORM_BLOCKS);
+  o.norm_part = a.take<double>(2 * NORM_BLOCKS);
   o.scal = a.take<double>(8);
   o.s_hist = a.take<double>(4096);
   I.d_packed = a.take<double>((size_t)I.P);
@@ -486,7 +490,8 @@ int check_inst(pdsdp_batch* b, int inst) {
   return PDSDP_OK;
 }
 
-int launch_iterate(pdsdp_batch* b, int nact, int lds, int step0, int nsteps) {
+int launch_iterate(pdsdp_batch* b, int nact, int lds, int step0, int nsteps, cudaStream_t stream = nullptr,
+                   const int* d_active = nullptr) {
   // shared memory plan beyond the fixed workspaces, in priority order:
   // (1) the CTA's Z rows (all-or-nothing; they feed every sparse product),
   // (2) own rows of F, Y_j, Y_{j-1} (smem-resident filter recurrence),
@@ -510,7 +515,7 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds, int step0, int nsteps) {
   cfg.gridDim = dim3(nact * b->C);
   cfg.blockDim = dim3(PDSDP_NTHR);
   cfg.dynamicSmemBytes = iterate_smem_bytes(lds, zcap, ycap, owncap, nlmax);
-  cfg.stream = b->stream;
+  cfg.stream = stream ? stream : b->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = b->C;
@@ -519,7 +524,61 @@ int launch_iterate(pdsdp_batch* b, int nact, int lds, int step0, int nsteps) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, lrpdhg_iterate_kernel, (const Inst*)b->d_insts, (const Ctl*)b->d_ctl,
-                        (const int*)b->d_active, step0, nsteps, lds, zcap, ycap, owncap, nlmax));
+                        d_active ? d_active : (const int*)b->d_active, step0, nsteps, lds, zcap, ycap, owncap, nlmax));
+  return PDSDP_OK;
+}
+
+// Resident clusters of the iteration kernel on this device (cluster size C,
+// one CTA per SM): the number of per-instance chunks that can run side by side.
+int max_active_clusters(pdsdp_batch* b, int* out) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(b->C);
+  cfg.blockDim = dim3(PDSDP_NTHR);
+  cfg.dynamicSmemBytes = b->smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = b->C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  CK(cudaOccupancyMaxActiveClusters(&n, lrpdhg_iterate_kernel, &cfg));
+  *out = std::max(1, n);
+  return PDSDP_OK;
+}
+
+// Fill the control block of one instance's next K steps (host side).
+void fill_ctl(pdsdp_batch* b, int k, int rank, int ypar0, int flags, int maxpass, int K, double conv_thr,
+              const double* stall_thr) {
+  for (int j = 0; j < K; ++j) {
+    Ctl& c = b->h_ctl[(size_t)k * PDSDP_KMAX + j];
+    c.r = rank;
+    c.ypar = (ypar0 ^ j) & 1;
+    c.flags = flags;
+    c.maxpass = maxpass;
+    c.conv_thr = conv_thr;
+    c.stall_thr = stall_thr ? stall_thr[j] : HUGE_VAL;
+    double* o = b->h_out + ((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN;
+    o[O_DONE] = 0.0;
+    o[O_DENSE_EXACT] = NAN;
+    o[O_ERR] = 0.0;
+  }
+}
+
+// The lambda_max(Z) refresh of one instance on `stream`, when due (zbound.cuh).
+int maybe_zlanczos(pdsdp_batch* b, int k, int ypar, cudaStream_t stream) {
+  Instance* I = b->inst[k];
+  if (I->zl_age < PDSDP_ZL_EVERY || I->n > PDSDP_ZL_NMAX) return PDSDP_OK;
+  b->h_zl[2 * k] = k;
+  b->h_zl[2 * k + 1] = ypar & 1;
+  I->zl_age = 0;
+  CK(cudaMemcpyAsync(b->d_zl + 2 * k, b->h_zl + 2 * k, 2 * sizeof(int), cudaMemcpyHostToDevice, stream));
+  const size_t zsm = (size_t)3 * std::max(2, I->n) * sizeof(double);
+  CK(cudaFuncSetAttribute(zlanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
+  zlanczos_kernel<<<1, PDSDP_ZL_THREADS, zsm, stream>>>(b->d_insts, b->d_zl + 2 * k);
+  CK(cudaGetLastError());
+  b->n_launch += 1;
   return PDSDP_OK;
 }
 
@@ -667,6 +726,9 @@ int pdsdp_batch_destroy(pdsdp_batch* b) {
   if (b->d_objres) cudaFree(b->d_objres);
   if (b->d_stop) cudaFree(b->d_stop);
   if (b->d_zl) cudaFree(b->d_zl);
+  if (b->d_ident) cudaFree(b->d_ident);
+  for (cudaStream_t st : b->slot_stream) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
+  for (cudaEvent_t ev : b->slot_event) cudaEventDestroy(ev);
   delete[] b->h_zl;
   for (int k = 0; k < 3; ++k) if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   for (int k = 0; k <= PDSDP_KMAX; ++k) if (b->tev[k]) cudaEventDestroy(b->tev[k]);
@@ -694,20 +756,19 @@ int pdsdp_opnorm_positions(pdsdp_batch* b, int inst, int64_t* pos_out, int64_t* 
   return PDSDP_OK;
 }
 
-static int opnorm_step(pdsdp_batch* b, Instance* I, double* hist, int idx) {
-  OpnormDev& o = I->od;
-  cudaStream_t s = b->stream;
-  // y = M x ; s = |y|
-  seg_dot_kernel<<<o.nseg, 256, 0, s>>>(o);
-  seg_final_kernel<<<std::max(1, std::min(1024, (o.mp + 255) / 256)), 256, 0, s>>>(o);
-  sumsq_kernel<<<NORM_BLOCKS, 256, 0, s>>>(o.y, o.mp, o.norm_part);
-  norm_final_kernel<<<1, 32, 0, s>>>(o.norm_part, NORM_BLOCKS, o.scal, hist, idx);
-  // x = M^T y / |M^T y|
-  adjT_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, s>>>(o);
-  sumsq_kernel<<<NORM_BLOCKS, 256, 0, s>>>(o.x, o.nT, o.norm_part);
-  norm_final_kernel<<<1, 32, 0, s>>>(o.norm_part, NORM_BLOCKS, o.scal + 1, nullptr, 0);
-  inv_scale_kernel<<<std::max(1, std::min(4096, (o.nT + 255) / 256)), 256, 0, s>>>(o.x, o.nT, o.scal + 1);
-  CK(cudaGetLastError());
+// One cooperative launch for `iters` power iterations (opnorm.cuh).
+static int opnorm_chunk(pdsdp_batch* b, Instance* I, int iters) {
+  OpnormDev o = I->od;
+  int dev = 0, sms = 148, per_sm = 1;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, opnorm_power_kernel, 256, 0));
+  const long long want = std::max<long long>(std::max<long long>(o.nseg, ((long long)std::max(o.nT, o.mp) + 255) / 256), 1);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((long long)sms * std::max(per_sm, 1), want));
+  double* hist = o.s_hist;
+  void* args[] = {(void*)&o, (void*)&iters, (void*)&hist};
+  CK(cudaLaunchCooperativeKernel((void*)opnorm_power_kernel, dim3(grid), dim3(256), args, 0, b->stream));
+  b->n_launch += 1;
   return PDSDP_OK;
 }
 
@@ -718,8 +779,7 @@ int pdsdp_opnorm_run(pdsdp_batch* b, int inst, const double* x0, int iters, doub
   Instance* I = b->inst[inst];
   if (I->od.nT == 0 || I->o_mval.empty()) return fail(PDSDP_EINVAL, "all constraint rows are zero; operator norm is 0");
   if (x0) CK(cudaMemcpyAsync(I->od.x, x0, I->tpos.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
-  for (int it = 0; it < iters; ++it)
-    if ((rc = opnorm_step(b, I, I->od.s_hist, it))) return rc;
+  if ((rc = opnorm_chunk(b, I, iters))) return rc;
   CK(cudaMemcpyAsync(s_out, I->od.s_hist, iters * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
   return PDSDP_OK;
@@ -782,27 +842,27 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     if (flags && (flags[a] & 8) && std::min(rank[a] + 1, I->n) > PDSDP_BMAX)
       return fail(PDSDP_ERANK, "rank r=" + std::to_string(rank[a]) + " needs an eigen block above 64");
     const int kk = std::min(std::min(rank[a] + 1, I->n), PDSDP_BMAX);
-    for (int j = 0; j < K; ++j) {
-      Ctl& c = b->h_ctl[(size_t)k * PDSDP_KMAX + j];
-      c.r = rank[a];
-      c.ypar = (ypar0[a] ^ j) & 1;
-      c.flags = flags ? flags[a] : 0;
-      c.maxpass = maxpass;
-      c.conv_thr = conv_thr ? conv_thr[a] : -1.0;
-      c.stall_thr = stall_thr ? stall_thr[(size_t)a * K + j] : HUGE_VAL;
-      b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_DONE] = 0.0;
-      b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_DENSE_EXACT] = NAN;
-      b->h_out[((size_t)k * PDSDP_KMAX + j) * PDSDP_OUT_LEN + O_ERR] = 0.0;
-    }
+    fill_ctl(b, k, rank[a], ypar0[a], flags ? flags[a] : 0, maxpass, K, conv_thr ? conv_thr[a] : -1.0,
+             stall_thr ? stall_thr + (size_t)a * K : nullptr);
     b->h_active[a] = k;
     const int bb = block_for(kk, I->n);
     I->bmax = std::max(I->bmax, bb);
     lds = std::max(lds, I->bmax);
     maxr = std::max(maxr, (int)rank[a]);
   }
-  CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, (size_t)N * PDSDP_KMAX * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
+  // only the listed instances' control blocks and stop flags are touched:
+  // other instances may have chunks in flight on the slot streams
+  if (nact == N && b->slot_stream.empty()) {
+    CK(cudaMemcpyAsync(b->d_ctl, b->h_ctl, (size_t)N * PDSDP_KMAX * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
+    CK(cudaMemsetAsync(b->d_stop, 0, (size_t)N * sizeof(int), b->stream));
+  } else {
+    for (int a = 0; a < nact; ++a) {
+      const size_t o = (size_t)insts[a] * PDSDP_KMAX;
+      CK(cudaMemcpyAsync(b->d_ctl + o, b->h_ctl + o, (size_t)K * sizeof(Ctl), cudaMemcpyHostToDevice, b->stream));
+      CK(cudaMemsetAsync(b->d_stop + insts[a], 0, sizeof(int), b->stream));
+    }
+  }
   CK(cudaMemcpyAsync(b->d_active, b->h_active, nact * sizeof(int), cudaMemcpyHostToDevice, b->stream));
-  CK(cudaMemsetAsync(b->d_stop, 0, (size_t)N * sizeof(int), b->stream));
   const int kp = std::min(RES_KMAX, (2 * std::min(maxr, PDSDP_BMAX) + 3) & ~3);
   const size_t rsm = (size_t)2 * RES_TILE * (kp + 1) * sizeof(double);
   // timing: one event before the chunk and one after every iteration launch,
@@ -812,27 +872,9 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
   // entry-wise residual kernel, so it launches step by step
   // refresh the lambda_max(Z) estimate of the Chebyshev interval every
   // PDSDP_ZL_EVERY iterations (Z_k drifts slowly with y; zbound.cuh)
-  {
-    int nz = 0;
-    for (int a = 0; a < nact; ++a) {
-      Instance* I = b->inst[insts[a]];
-      if (I->zl_age >= PDSDP_ZL_EVERY && I->n <= PDSDP_ZL_NMAX) {
-        b->h_zl[2 * nz] = insts[a];
-        b->h_zl[2 * nz + 1] = ypar0[a] & 1;
-        ++nz;
-        I->zl_age = 0;
-      }
-    }
-    if (nz > 0) {
-      int nmax = 2;
-      for (int a = 0; a < nz; ++a) nmax = std::max(nmax, b->inst[b->h_zl[2 * a]]->n);
-      CK(cudaMemcpyAsync(b->d_zl, b->h_zl, (size_t)2 * nz * sizeof(int), cudaMemcpyHostToDevice, b->stream));
-      const size_t zsm = (size_t)3 * nmax * sizeof(double);
-      CK(cudaFuncSetAttribute(zlanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
-      zlanczos_kernel<<<nz, PDSDP_ZL_THREADS, zsm, b->stream>>>(b->d_insts, b->d_zl);
-      CK(cudaGetLastError());
-      b->n_launch += 1;
-    }
+  for (int a = 0; a < nact; ++a) {
+    int rc = maybe_zlanczos(b, insts[a], ypar0[a], b->stream);
+    if (rc) return rc;
   }
   if (b->timing) CK(cudaEventRecord(b->tev[0], b->stream));
   if (!b->verify_residual) {
@@ -873,6 +915,80 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     CK(cudaEventElapsedTime(&t1, b->tev[0], b->tev[b->verify_residual ? done_max : 1]));
     b->t_iter += t1; b->n_iter += done_max;
   }
+  return PDSDP_OK;
+}
+
+int pdsdp_slots(pdsdp_batch* b, int32_t* nslots_out) {
+  if (!b || !nslots_out) return fail(PDSDP_EINVAL, "bad arguments");
+  if (b->slot_stream.empty()) {
+    int n = 1;
+    int rc = max_active_clusters(b, &n);
+    if (rc) return rc;
+    n = std::min(n, (int)b->inst.size());
+    const int N = (int)b->inst.size();
+    std::vector<int> ident(N);
+    for (int i = 0; i < N; ++i) ident[i] = i;
+    CK(cudaMalloc(&b->d_ident, (size_t)N * sizeof(int)));
+    CK(cudaMemcpy(b->d_ident, ident.data(), (size_t)N * sizeof(int), cudaMemcpyHostToDevice));
+    for (int k = 0; k < n; ++k) {
+      cudaStream_t st; cudaEvent_t ev;
+      CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      b->slot_stream.push_back(st);
+      b->slot_event.push_back(ev);
+    }
+  }
+  *nslots_out = (int)b->slot_stream.size();
+  return PDSDP_OK;
+}
+
+int pdsdp_chunk_launch(pdsdp_batch* b, int32_t slot, int32_t inst, int32_t rank, int32_t ypar0, int32_t flags,
+                       int32_t maxpass, int32_t K, double conv_thr, const double* stall_thr) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (slot < 0 || slot >= (int)b->slot_stream.size()) return fail(PDSDP_EINVAL, "slot out of range (pdsdp_slots)");
+  if (K < 1 || K > PDSDP_KMAX) return fail(PDSDP_EINVAL, "K must lie in [1, PDSDP_KMAX]");
+  Instance* I = b->inst[inst];
+  if (I->dense_mode) return fail(PDSDP_EINVAL, "instance is in dense mode");
+  if (rank < 1 || rank > I->n)
+    return fail(PDSDP_EINVAL, "rank r=" + std::to_string(rank) + " outside [1, " + std::to_string(I->n) + "]");
+  cudaStream_t st = b->slot_stream[slot];
+  fill_ctl(b, inst, rank, ypar0, flags, maxpass, K, conv_thr, stall_thr);
+  const int kk = std::min(std::min(rank + 1, I->n), PDSDP_BMAX);
+  I->bmax = std::max(I->bmax, block_for(kk, I->n));
+  const size_t o = (size_t)inst * PDSDP_KMAX;
+  CK(cudaMemcpyAsync(b->d_ctl + o, b->h_ctl + o, (size_t)K * sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(b->d_stop + inst, 0, sizeof(int), st));
+  if ((rc = maybe_zlanczos(b, inst, ypar0, st))) return rc;
+  if ((rc = launch_iterate(b, 1, std::max(4, I->bmax), 0, K, st, b->d_ident + inst))) return rc;
+  CK(cudaEventRecord(b->slot_event[slot], st));
+  b->n_launch += 1;
+  return PDSDP_OK;
+}
+
+int pdsdp_chunk_poll(pdsdp_batch* b, int32_t slot) {
+  if (!b || slot < 0 || slot >= (int)b->slot_stream.size()) return fail(PDSDP_EINVAL, "slot out of range");
+  cudaError_t e = cudaEventQuery(b->slot_event[slot]);
+  if (e == cudaSuccess) return 1;
+  if (e == cudaErrorNotReady) return 0;
+  return fail(PDSDP_ECUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(e));
+}
+
+int pdsdp_chunk_collect(pdsdp_batch* b, int32_t slot, int32_t inst, int32_t K, double* out, int32_t* steps_done) {
+  int rc = check_inst(b, inst);
+  if (rc) return rc;
+  if (slot < 0 || slot >= (int)b->slot_stream.size() || !out || K < 1 || K > PDSDP_KMAX)
+    return fail(PDSDP_EINVAL, "bad collect arguments");
+  CK(cudaEventSynchronize(b->slot_event[slot]));
+  int done = 0;
+  for (int j = 0; j < K; ++j) {
+    const double* src = b->h_out + ((size_t)inst * PDSDP_KMAX + j) * PDSDP_OUT_LEN;
+    memcpy(out + (size_t)j * PDSDP_OUT_LEN, src, PDSDP_OUT_LEN * sizeof(double));
+    if (src[O_ERR] != 0.0) break;
+    if (src[O_DONE] == 1.0) done = j + 1;
+  }
+  if (steps_done) *steps_done = done;
+  b->inst[inst]->zl_age += done;
   return PDSDP_OK;
 }
 

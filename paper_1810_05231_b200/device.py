@@ -27,7 +27,7 @@ OUT_ERR = 13
 OUT_DENSE = 8
 OUT_DENSE_EXACT = 14
 BLOCK_MAX = 64
-KMAX = 64
+KMAX = 128
 
 EINVAL, ECUDA, ENOMEM, ERANK = -1, -2, -3, -4
 
@@ -39,6 +39,7 @@ EXPORTED = (
     "pdsdp_last_error", "pdsdp_version", "pdsdp_set_timing", "pdsdp_kernel_times",
     "pdsdp_debug", "pdsdp_iterate_many", "pdsdp_set_verify_residual",
     "pdsdp_dense_begin", "pdsdp_iterate_dense",
+    "pdsdp_slots", "pdsdp_chunk_launch", "pdsdp_chunk_poll", "pdsdp_chunk_collect",
 )
 
 
@@ -90,6 +91,10 @@ def load_library(path: str = LIB_PATH):
             "pdsdp_set_verify_residual": (ct.c_int, [P, ct.c_int]),
             "pdsdp_debug": (ct.c_int, [P, ct.c_int, P]),
             "pdsdp_iterate_many": (ct.c_int, [P, ct.c_int, P, P, P, P, I32, I32, P, P, P, P]),
+            "pdsdp_slots": (ct.c_int, [P, P]),
+            "pdsdp_chunk_launch": (ct.c_int, [P, I32, I32, I32, I32, I32, I32, I32, D, P]),
+            "pdsdp_chunk_poll": (ct.c_int, [P, I32]),
+            "pdsdp_chunk_collect": (ct.c_int, [P, I32, I32, I32, P, P]),
             "pdsdp_dense_begin": (ct.c_int, [P, ct.c_int, ct.c_int]),
             "pdsdp_iterate_dense": (ct.c_int, [P, ct.c_int, I32, I32, P]),
         }
@@ -232,6 +237,31 @@ class DeviceBatch:
                                            _ptr(fl), int(maxpass), int(K), _ptr(conv), _ptr(stall),
                                            _ptr(out), _ptr(done)))
         return out, done
+
+    # ---- asynchronous per-instance chunks (one stream per resident cluster) ----
+    def slots(self) -> int:
+        n = ct.c_int32()
+        _check(self.lib.pdsdp_slots(self.h, ct.byref(n)))
+        return int(n.value)
+
+    def chunk_launch(self, slot: int, inst: int, rank: int, ypar0: int, K: int, conv_thr: float,
+                     stall_thr, flags: int = 0, maxpass: int = 60):
+        stall = np.ascontiguousarray(stall_thr, dtype=np.float64)
+        assert stall.size == K
+        _check(self.lib.pdsdp_chunk_launch(self.h, slot, inst, int(rank), int(ypar0), int(flags),
+                                           int(maxpass), int(K), float(conv_thr), _ptr(stall)))
+
+    def chunk_poll(self, slot: int) -> bool:
+        rc = self.lib.pdsdp_chunk_poll(self.h, slot)
+        if rc < 0:
+            _check(rc)
+        return rc == 1
+
+    def chunk_collect(self, slot: int, inst: int, K: int):
+        out = np.zeros((K, OUT_LEN))
+        done = ct.c_int32()
+        _check(self.lib.pdsdp_chunk_collect(self.h, slot, inst, int(K), _ptr(out), ct.byref(done)))
+        return out, int(done.value)
 
     def dense_begin(self, inst: int, from_factored: bool):
         """Switch an instance to the dense-iterate path (full device

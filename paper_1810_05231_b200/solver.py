@@ -229,9 +229,50 @@ class _InstanceRun:
 
     def consume(self, outs, done: int) -> None:
         """Apply the reference's per-iteration control logic to the executed
-        steps, in order (lowrank.py:141-188)."""
+        steps, in order (lowrank.py:141-188).  The device pauses a chunk at the
+        first step where that logic can act, so every step but the last is
+        uneventful (finite, above the convergence threshold, below its stall
+        threshold, no callback due): those are folded in at once after
+        checking exactly that; anything else takes the step-by-step path."""
+        nb = done - 1
+        if nb >= 1 and self.k > 1 and self._bulk_ok(outs, nb):
+            o = np.asarray(outs[:nb])
+            self.eig_passes += int(o[:, OUT_PASSES].sum())
+            self.eig_matvecs += int(o[:, OUT_MATVECS].sum())
+            self.eig_unconverged += int(np.count_nonzero(o[:, OUT_EIGCONV] == 0))
+            ep, ed = o[:, OUT_EPS_P], o[:, OUT_EPS_D]
+            ec = ep + ed
+            it, ctl = self.it, self.controller
+            it.k = self.k + nb - 1
+            it.ypar ^= nb & 1
+            it.which = 0
+            ctl.last_lambda_r = float(o[nb - 1, OUT_LAMBDA])
+            self.res = (float(ep[-1]), float(ed[-1]), float(ec[-1]))
+            ctl.history.extend(ec.tolist())
+            self.k += nb
+            self._consume_steps(outs, nb, done)
+        else:
+            self._consume_steps(outs, 0, done)
+
+    def _bulk_ok(self, outs, nb: int) -> bool:
+        c, ctl = self.config, self.controller
+        o = np.asarray(outs[:nb])
+        if not np.all(o[:, OUT_FINITE] == 1.0):
+            return False
+        ec = o[:, OUT_EPS_P] + o[:, OUT_EPS_D]
+        if np.any(ec <= c.eps_tol * self.scale):
+            return False
+        if np.any(ec >= _stall_thresholds(ctl, self.n, nb)):
+            return False
+        if self.callback is not None:
+            ks = self.k + np.arange(nb)
+            if np.any(ks % c.progress_every == 0):
+                return False
+        return True
+
+    def _consume_steps(self, outs, j0: int, done: int) -> None:
         c, ctl, it, n = self.config, self.controller, self.it, self.n
-        for j in range(done):
+        for j in range(j0, done):
             out = outs[j]
             self.eig_passes += int(out[OUT_PASSES])
             self.eig_matvecs += int(out[OUT_MATVECS])
@@ -318,32 +359,51 @@ def run_lr_loop(batch: DeviceBatch, inst: int, prob: SdpProblem, config: SolverC
 
 def run_lr_batch(batch: DeviceBatch, insts, config: SolverConfig, alphas,
                  chunk: int = KMAX, t0: float | None = None) -> list:
-    """Algorithm 2 on many resident instances at once: every chunk launches
-    all still-running instances together (one cluster per instance); each
-    instance pauses on the device at its own events and keeps its own host
-    controller, exactly as in run_lr_loop."""
+    """Algorithm 2 on many resident instances at once (the multi-instance
+    analogue of the reference's sequential bench rows, ``cli.py:284-329``).
+
+    Device-side scheduling: as many per-instance chunks as clusters of the
+    iteration kernel fit on the GPU run side by side, one stream ("slot")
+    each.  A chunk pauses on the device at its instance's own events; the host
+    polls the slots, applies that instance's control logic (exactly as
+    run_lr_loop does) and hands the freed slot to the next waiting instance, so
+    no instance waits for another one's chunk and the batch takes about as long
+    as its longest solve."""
+    from collections import deque
     t0 = time.perf_counter() if t0 is None else t0
     runs = [_InstanceRun(batch, i, batch.problems[i], config, a, None, t0) for i, a in zip(insts, alphas)]
-    while True:
-        for r in runs:                     # instances on the dense path step alone
-            if r.status is None and r.dense:
-                r.step(chunk)
-        live = [r for r in runs if r.status is None and not r.dense]
-        if not live:
-            if any(r.status is None for r in runs):
+    nslots = batch.slots()
+    free = list(range(nslots))
+    inflight = {}
+    queue = deque(runs)
+    while queue or inflight:
+        while free and queue:
+            r = queue.popleft()
+            if r.status is not None:
                 continue
-            break
-        K = min(r.max_chunk(chunk) for r in live)
-        convs, stalls = [], []
-        for r in live:
-            cthr, sthr = r.thresholds(K)
-            convs.append(cthr)
-            stalls.append(sthr)
-        outs, done = batch.iterate_many([r.inst for r in live], [r.controller.r for r in live],
-                                        [r.it.ypar for r in live], K, convs, np.concatenate(stalls))
-        for a, r in enumerate(live):
-            r.after_chunk(outs[a], int(done[a]), K)
-            r.check_time()
+            if r.dense:                    # dense-path instances step alone, synchronously
+                r.step(chunk)
+                if r.status is None:
+                    queue.append(r)
+                continue
+            K = r.max_chunk(chunk)
+            conv, stall = r.thresholds(K)
+            slot = free.pop()
+            batch.chunk_launch(slot, r.inst, r.controller.r, r.it.ypar, K, conv, stall)
+            inflight[slot] = (r, K)
+        progressed = False
+        for slot in list(inflight):
+            if batch.chunk_poll(slot):
+                r, K = inflight.pop(slot)
+                outs, done = batch.chunk_collect(slot, r.inst, K)
+                r.after_chunk(outs, done, K)
+                r.check_time()
+                free.append(slot)
+                if r.status is None:
+                    queue.append(r)
+                progressed = True
+        if not progressed and inflight:
+            time.sleep(0)
     return [r.outcome() for r in runs]
 
 

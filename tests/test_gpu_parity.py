@@ -100,6 +100,29 @@ def test_aproj_clustered_spectrum_vs_oracle(rng):
         assert lm == pytest.approx(lr, rel=1e-8, abs=1e-10)
 
 
+def test_aproj_triple_clusters_vs_oracle(rng):
+    """Three or more nearly equal kept eigenvalues (relative gaps 1e-10 ..
+    1e-12): the Jacobi second-order finish U = I + K loses orthogonality by
+    K^T K there, so it must be rejected in favour of the sweeps; X+ is the
+    projector-weighted sum and is basis-independent within each cluster."""
+    for n, r in ((96, 9), (200, 12), (320, 20)):
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = -rng.random(n)
+        top = np.concatenate([[7.0, 7.0 * (1 + 1e-10), 7.0 * (1 - 3e-12), 7.0 * (1 + 2e-11),
+                               3.0, 3.0 * (1 + 1e-11), 3.0 * (1 - 1e-12), 1.5, 1.5 * (1 + 1e-10)],
+                              0.5 + 0.4 * rng.random(r)])[:r]
+        lam[:r] = top
+        D = (Q * lam) @ Q.T
+        S = orc.pack(0.5 * (D + D.T))
+        P, lm = pk.aproj_psd(pk.SymMatrix(n, S), r)
+        Pr, lr = orc.aproj_psd(S, n, r)
+        assert rel(P.data, Pr) <= ITER_TOL
+        assert lm == pytest.approx(lr, rel=1e-8, abs=1e-10)
+        # X+ = Q_r diag(top) Q_r^T exactly (the construction), to the same tolerance
+        exact = orc.pack((Q[:, :r] * top) @ Q[:, :r].T)
+        assert rel(P.data, exact) <= ITER_TOL
+
+
 # ---------------------------------------------------------------- full solves
 
 @pytest.mark.parametrize("ci", range(5))
