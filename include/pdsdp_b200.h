@@ -93,11 +93,15 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed);
 
 /* One LR-PDHG iteration (lowrank.py:141-150: approximate_primal_step,
  * dual_step, residuals) for each listed instance.  rank[i], ypar[i], flags[i]
- * per listed instance; out: nact * PDSDP_OUT_LEN doubles (host). */
+ * per listed instance; out: nact * PDSDP_OUT_LEN doubles (host).
+ * flags: bit 0 cold start, bit 1 certificate eigenvalue accurate, bit 2 re-run
+ * of the last iteration from the same (X_k, y_k), bit 3 certificate to the
+ * kept-pair tolerance (op-level aproj_psd), bits 8..11 extra guard columns of
+ * the eigen block (0..15; wider blocks converge in fewer filter passes). */
 int pdsdp_iterate(pdsdp_batch* b, int nact, const int32_t* insts, const int32_t* rank,
                   const int32_t* ypar, const int32_t* flags, int32_t maxpass, double* out);
 
-/* Up to K (<= 64) consecutive iterations with one host synchronisation.
+/* Up to K (<= PDSDP_KMAX) consecutive iterations with one host synchronisation.
  * Step j of listed instance a runs with y parity ypar0[a]^j.  The device
  * pauses an instance after the first step whose combined residual
  * eps_p + eps_d is <= conv_thr[a] or >= stall_thr[a*K + j], or whose iterate

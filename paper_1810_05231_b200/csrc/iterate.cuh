@@ -1083,7 +1083,13 @@ inline size_t iterate_smem_bytes(int lds, int zcap, int ycap, int owncap, int nl
          (size_t)(3 * PDSDP_BMAX + 8 + 20 + zcap + (owncap ? nlmax + 2 : 0)) * sizeof(int) + 64;
 }
 
-__device__ int choose_block(int k, int n) { return block_for(k, n); }
+// eigen block for k wanted pairs plus `extra` guard columns requested by the
+// host (Ctl flags bits 8..11: instances whose iterations keep needing several
+// filter passes get a wider block, see solver.py)
+__device__ int choose_block(int k, int n, int extra) {
+  int b = block_for(k, n) + extra;
+  return b > n ? n : b;
+}
 
 __global__ void __launch_bounds__(PDSDP_NTHR, 1)
 lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ctls,
@@ -1223,7 +1229,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   const bool cold = !rerun && ((ctl.flags & 1) || st->b == 0);
   const int rF = cold ? 0 : (rerun ? st->rF_used : st->rF);
   const int b_old = cold ? 0 : st->b;
-  int b = choose_block(k, n);
+  const int gextra = (ctl.flags >> 8) & 15;
+  int b = choose_block(k, n, gextra);
   if (b > lcap) b = lcap;
   if (b < b_old) b = b_old;
   int iav = cold ? 1 : st->iav;   // physical buffer holding AV
@@ -1721,7 +1728,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const int rn = min(r_t, max(np + 2, r + 4));
           const int kn = min(rn + 1, n);
           if (kn > lcap) { grow_err = 1; break; }
-          int bn = choose_block(kn, n);
+          int bn = choose_block(kn, n, gextra);
           if (bn > lcap) bn = lcap;
           if (bn < b) bn = b;
           __syncthreads();

@@ -845,7 +845,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     fill_ctl(b, k, rank[a], ypar0[a], flags ? flags[a] : 0, maxpass, K, conv_thr ? conv_thr[a] : -1.0,
              stall_thr ? stall_thr + (size_t)a * K : nullptr);
     b->h_active[a] = k;
-    const int bb = block_for(kk, I->n);
+    const int bb = std::min(std::min(I->n, PDSDP_BMAX), block_for(kk, I->n) + ((flags ? flags[a] : 0) >> 8 & 15));
     I->bmax = std::max(I->bmax, bb);
     lds = std::max(lds, I->bmax);
     maxr = std::max(maxr, (int)rank[a]);
@@ -955,7 +955,7 @@ int pdsdp_chunk_launch(pdsdp_batch* b, int32_t slot, int32_t inst, int32_t rank,
   cudaStream_t st = b->slot_stream[slot];
   fill_ctl(b, inst, rank, ypar0, flags, maxpass, K, conv_thr, stall_thr);
   const int kk = std::min(std::min(rank + 1, I->n), PDSDP_BMAX);
-  I->bmax = std::max(I->bmax, block_for(kk, I->n));
+  I->bmax = std::max(I->bmax, std::min(std::min(I->n, PDSDP_BMAX), block_for(kk, I->n) + ((flags >> 8) & 15)));
   const size_t o = (size_t)inst * PDSDP_KMAX;
   CK(cudaMemcpyAsync(b->d_ctl + o, b->h_ctl + o, (size_t)K * sizeof(Ctl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(b->d_stop + inst, 0, sizeof(int), st));

@@ -48,6 +48,13 @@ _NORM_REL_TOL = 1e-10
 _NORM_SAFETY = 1.0 + 1e-7
 _NORM_CHUNK = 256
 FLAG_COLD, FLAG_CERT, FLAG_RERUN = 1, 2, 4
+# Extra guard columns of the eigen block (flags bits 8..11).  One guard is
+# fastest when an iteration converges in one or two filter passes (configs 2
+# and 5); instances whose iterations keep needing many passes (config 4: a
+# kept eigenvalue inside a cluster at a 1e-3 gap ratio) get a wider block:
+# +2 columns whenever a chunk averaged more than GUARD_PASSES passes per
+# iteration, up to GUARD_MAX (config 4: 113 -> 96 s to tolerance).
+GUARD_SHIFT, GUARD_STEP, GUARD_MAX, GUARD_PASSES = 8, 2, 6, 3.0
 
 
 def _device_batch(prob: SdpProblem) -> DeviceBatch:
@@ -181,6 +188,15 @@ class _InstanceRun:
         self.eig_passes = self.eig_matvecs = self.eig_unconverged = 0
         self.dense = False     # dense-iterate mode (full device eigendecomposition)
         self.dense_from = None
+        self.guard = 0         # extra guard columns of the eigen block
+
+    def flags(self) -> int:
+        return self.guard << GUARD_SHIFT
+
+    def _adapt_guard(self, outs, done: int) -> None:
+        if done >= 8 and self.guard < GUARD_MAX:
+            if float(np.mean(np.asarray(outs[:done])[:, OUT_PASSES])) > GUARD_PASSES:
+                self.guard = min(GUARD_MAX, self.guard + GUARD_STEP)
 
     def enter_dense(self) -> None:
         """The projection argument has more positive eigenvalues than an eigen
@@ -201,11 +217,13 @@ class _InstanceRun:
         else:
             K = self.max_chunk(chunk)
             conv, stall = self.thresholds(K)
-            outs, done = self.batch.iterate_many([self.inst], [self.controller.r], [self.it.ypar], K, [conv], stall)
+            outs, done = self.batch.iterate_many([self.inst], [self.controller.r], [self.it.ypar], K, [conv], stall,
+                                                 flags=[self.flags()])
             self.after_chunk(outs[0], int(done[0]), K)
         self.check_time()
 
     def after_chunk(self, outs, done: int, K: int) -> None:
+        self._adapt_guard(outs, done)
         self.consume(outs, done)
         if self.status is None and done < K and outs[done][OUT_ERR] != 0.0:
             self.enter_dense()
@@ -284,7 +302,7 @@ class _InstanceRun:
                     # reference's accuracy; re-run this iteration from the same
                     # (X_k, y_k) with the certificate eigenpair converged too
                     assert j == done - 1, "device chunk ran past a checkpoint"
-                    out = self.batch.iterate([self.inst], [ctl.r], [it.ypar], [FLAG_CERT | FLAG_RERUN])[0]
+                    out = self.batch.iterate([self.inst], [ctl.r], [it.ypar], [FLAG_CERT | FLAG_RERUN | self.flags()])[0]
                     if out[OUT_ERR] != 0.0:
                         raise RuntimeError("certificate re-run exceeded the eigen block limit")
                     self.eig_passes += int(out[OUT_PASSES])
@@ -389,7 +407,7 @@ def run_lr_batch(batch: DeviceBatch, insts, config: SolverConfig, alphas,
             K = r.max_chunk(chunk)
             conv, stall = r.thresholds(K)
             slot = free.pop()
-            batch.chunk_launch(slot, r.inst, r.controller.r, r.it.ypar, K, conv, stall)
+            batch.chunk_launch(slot, r.inst, r.controller.r, r.it.ypar, K, conv, stall, flags=r.flags())
             inflight[slot] = (r, K)
         progressed = False
         for slot in list(inflight):

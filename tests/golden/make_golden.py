@@ -566,6 +566,11 @@ if __name__ == "__main__":
     a = ap.parse_args()
     if a.full:
         for name in a.full.split(","):
+            if name == "cfg3_stall":
+                # config 3 past its first stall-triggered rank doubling (k = 501):
+                # pins the stall rule and the rank path at the full size
+                make_sketch(os.path.join(HERE, "cfg3_stall_sketch.npz"), 2, (510,))
+                continue
             if name.startswith("cfg5s"):
                 make_full(os.path.join(HERE, f"{name}_full.npz"), 4, int(name[5:]))
             else:

@@ -383,6 +383,57 @@ def test_rank_above_block_limit_continues_on_dense_path():
     np.testing.assert_allclose(res.final_residuals, d["mc_res"], rtol=1e-6)
 
 
+# ------------------------------------------------- solves to tolerance, full size
+
+FULL_CASES = [("cfg2_full.npz", 1, 0), ("cfg5s0_full.npz", 4, 0), ("cfg5s1_full.npz", 4, 1),
+              ("cfg4_full.npz", 3, 0)]
+
+
+@pytest.mark.parametrize("fname,idx,seed", FULL_CASES)
+def test_solve_to_tolerance_matches_reference(fname, idx, seed, capsys):
+    """BASELINE configs 2, 4, 5 solved to the 1e-4 rule on the GPU against the
+    UNMODIFIED reference run to tolerance on the same seeded input
+    (tests/golden/make_golden.py --full: status, stop iteration, rank path,
+    checkpoints, objectives, final residuals, final X as eigen-factors).
+    North-star bar: objective within 1e-5 relative, the same 1e-4 stopping
+    rule met.  Long solves are chaotic in the stall-triggered rank-doubling
+    times (eigensolver differences at ARPACK's own 1e-12 move them), so the
+    iteration counts are compared with a tolerance and the delta is printed;
+    the sequence of ranks must be identical."""
+    d = load_golden(fname)
+    prob, cfg = workloads.config(idx, seed)
+    res = pk.solve_lr_pd_sdp(prob, cfg)
+    assert res.status.value == str(d["status"]) == "optimal"
+    ref_iters = int(d["iters"])
+    ref_path = [tuple(int(v) for v in row) for row in d["rank_path"]]
+    assert [r for _, r in res.rank_path] == [r for _, r in ref_path]
+    assert res.residual_scale == pytest.approx(float(d["scale"]), rel=1e-9)
+    # the same stopping rule met by both (lowrank.py:153-161)
+    assert res.final_residuals[2] <= cfg.eps_tol * res.residual_scale
+    assert float(d["res_final"][2]) <= cfg.eps_tol * float(d["scale"])
+    assert res.primal_objective == pytest.approx(float(d["pobj"]), rel=OBJ_TOL)
+    assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
+    assert len(res.checkpoints) == len(d["checkpoints"])
+    for c, (rk, obj) in zip(res.checkpoints, d["checkpoints"]):
+        assert c.rank == int(rk) and c.objective == pytest.approx(obj, rel=1e-4)
+    assert abs(res.iterations - ref_iters) <= 0.05 * ref_iters
+    # exact rel-Frobenius distance of the final iterates (reference X = V diag(lam) V^T)
+    V, lam = d["X_V"], d["X_lam"]
+    Xg = res.X.to_dense()
+    err = np.linalg.norm(Xg - (V * lam) @ V.T) / float(d["X_fro"])
+    yerr = rel(res.y, d["y_final"])
+    same_path = res.rank_path == ref_path
+    with capsys.disabled():
+        print(f"\n[{fname}] iterations {res.iterations} vs reference {ref_iters} (delta {res.iterations - ref_iters}), "
+              f"rank path {res.rank_path} vs {ref_path}, pobj rel diff "
+              f"{abs(res.primal_objective - float(d['pobj'])) / abs(float(d['pobj'])):.2e}, "
+              f"final X rel-Frobenius diff {err:.2e}, y rel diff {yerr:.2e}")
+    if same_path and res.iterations == ref_iters:
+        assert err <= 1e-6 and yerr <= 1e-6      # same trajectory: only eigensolver-level differences
+    else:
+        assert err <= 5e-3                       # both within the 1e-4 rule of the same optimum
+
+
 def test_time_limit_and_max_iter_status():
     prob, cfg = workloads.config(0)
     res = pk.solve_lr_pd_sdp(prob, with_iters(cfg, 7))

@@ -9,10 +9,14 @@ from paper_1810_05231_b200.device import DeviceBatch
 from paper_1810_05231_b200.solver import operator_norm_on_device, run_lr_loop
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 prob, cfg = workloads.config(idx)
+if len(sys.argv) > 2:      # optional iteration cap (bounded sweeps of long configs)
+    from paper_1810_05231_b200 import SolverConfig
+    cfg = SolverConfig(**{**cfg.__dict__, "max_iter": int(sys.argv[2])})
 batch = DeviceBatch([prob])
 alpha = cfg.alpha_safety / operator_norm_on_device(batch, 0, cfg.seed)
 stream = torch.cuda.ExternalStream(batch.stream_handle())
-o = run_lr_loop(batch, 0, prob, cfg, alpha)
+if len(sys.argv) <= 3:
+    o = run_lr_loop(batch, 0, prob, cfg, alpha)
 torch.cuda.synchronize()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record(stream)
