@@ -23,8 +23,16 @@
 #include "residual.cuh"
 #include "zbound.cuh"
 
+// Iterations between lambda_max(Z) estimates: Z = C + M^T y drifts quickly
+// while y builds up and ever more slowly afterwards, so the refresh interval
+// grows with the iteration count, k / 8 clamped to [ZL_EVERY, ZL_EVERY_MAX]
+// (a stale estimate costs filter efficiency, never accuracy: zbound.cuh;
+// config 2: fixed 256 -> 7.56 s, 1024 -> 7.42 s, 4096 -> 7.37 s to tolerance).
 #ifndef PDSDP_ZL_EVERY
-#define PDSDP_ZL_EVERY 256   // iterations between lambda_max(Z) estimates
+#define PDSDP_ZL_EVERY 256
+#endif
+#ifndef PDSDP_ZL_EVERY_MAX
+#define PDSDP_ZL_EVERY_MAX 4096
 #endif
 
 using namespace pdsdp;
@@ -82,6 +90,7 @@ struct Instance {
   OpnormDev od{};
   double* d_packed = nullptr;   // scratch packed vector (op-level maps)
   long long zl_age = 1LL << 40;  // iterations since the last lambda_max(Z) estimate
+  long long iters_total = 0;     // iterations since the last reset
   long long P = 0;
   // dense-iterate mode (dense_path.cuh): X_k as a dense n x n matrix, full eigendecomposition
   int dense_mode = 0;
@@ -569,7 +578,8 @@ void fill_ctl(pdsdp_batch* b, int k, int rank, int ypar0, int flags, int maxpass
 // The lambda_max(Z) refresh of one instance on `stream`, when due (zbound.cuh).
 int maybe_zlanczos(pdsdp_batch* b, int k, int ypar, cudaStream_t stream) {
   Instance* I = b->inst[k];
-  if (I->zl_age < PDSDP_ZL_EVERY || I->n > PDSDP_ZL_NMAX) return PDSDP_OK;
+  const long long every = std::min<long long>(PDSDP_ZL_EVERY_MAX, std::max<long long>(PDSDP_ZL_EVERY, I->iters_total / 8));
+  if (I->zl_age < every || I->n > PDSDP_ZL_NMAX) return PDSDP_OK;
   b->h_zl[2 * k] = k;
   b->h_zl[2 * k + 1] = ypar & 1;
   I->zl_age = 0;
@@ -811,6 +821,7 @@ int pdsdp_reset(pdsdp_batch* b, int inst, double seed) {
   Instance* I = b->inst[inst];
   I->bmax = 0;
   I->zl_age = 1LL << 40;
+  I->iters_total = 0;
   I->dense_mode = 0;
   CK(cudaMemsetAsync(I->desc.st, 0, sizeof(State), b->stream));
   CK(cudaMemsetAsync(I->desc.V, 0, (size_t)I->n * I->ld * sizeof(double), b->stream));
@@ -908,6 +919,7 @@ int pdsdp_iterate_many(pdsdp_batch* b, int nact, const int32_t* insts, const int
     }
     if (steps_done) steps_done[a] = done;
     b->inst[insts[a]]->zl_age += done;
+    b->inst[insts[a]]->iters_total += done;
     done_max = std::max(done_max, done);
   }
   if (b->timing && done_max > 0) {
@@ -989,6 +1001,7 @@ int pdsdp_chunk_collect(pdsdp_batch* b, int32_t slot, int32_t inst, int32_t K, d
   }
   if (steps_done) *steps_done = done;
   b->inst[inst]->zl_age += done;
+  b->inst[inst]->iters_total += done;
   return PDSDP_OK;
 }
 

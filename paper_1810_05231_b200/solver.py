@@ -52,8 +52,9 @@ FLAG_COLD, FLAG_CERT, FLAG_RERUN = 1, 2, 4
 # fastest when an iteration converges in one or two filter passes (configs 2
 # and 5); instances whose iterations keep needing many passes (config 4: a
 # kept eigenvalue inside a cluster at a 1e-3 gap ratio) get a wider block:
-# +2 columns whenever a chunk averaged more than GUARD_PASSES passes per
-# iteration, up to GUARD_MAX (config 4: 113 -> 96 s to tolerance).
+# +2 columns at a rank change (where the block is rebuilt anyway) if the rank
+# phase that just ended averaged more than GUARD_PASSES passes per iteration,
+# up to GUARD_MAX.
 GUARD_SHIFT, GUARD_STEP, GUARD_MAX, GUARD_PASSES = 8, 2, 6, 3.0
 
 
@@ -189,14 +190,21 @@ class _InstanceRun:
         self.dense = False     # dense-iterate mode (full device eigendecomposition)
         self.dense_from = None
         self.guard = 0         # extra guard columns of the eigen block
+        self.phase_passes, self.phase_steps = 0.0, 0
 
     def flags(self) -> int:
         return self.guard << GUARD_SHIFT
 
     def _adapt_guard(self, outs, done: int) -> None:
-        if done >= 8 and self.guard < GUARD_MAX:
-            if float(np.mean(np.asarray(outs[:done])[:, OUT_PASSES])) > GUARD_PASSES:
-                self.guard = min(GUARD_MAX, self.guard + GUARD_STEP)
+        """Filter passes of the current rank phase (for the guard policy)."""
+        if done > 0:
+            self.phase_passes += float(np.asarray(outs[:done])[:, OUT_PASSES].sum())
+            self.phase_steps += done
+
+    def _rank_changed(self) -> None:
+        if self.phase_steps >= 8 and self.phase_passes > GUARD_PASSES * self.phase_steps:
+            self.guard = min(GUARD_MAX, self.guard + GUARD_STEP)
+        self.phase_passes, self.phase_steps = 0.0, 0
 
     def enter_dense(self) -> None:
         """The projection argument has more positive eigenvalues than an eigen
@@ -338,11 +346,13 @@ class _InstanceRun:
                              ctl.r, approx_error_bound(n, ctl.r, lambda_r), self.eps_lambda)
                 update_rank(ctl, n)
                 self.rank_path.append((k, ctl.r))
+                self._rank_changed()
                 assert j == done - 1, "device chunk ran past a rank change"
             elif ctl.r < n and stall_detected(ctl.history, ctl.ell):
                 logger.debug("stalled at rank %d after %d iterations; doubling", ctl.r, k)
                 update_rank(ctl, n)
                 self.rank_path.append((k, ctl.r))
+                self._rank_changed()
                 assert j == done - 1, "device chunk ran past a stall"
 
     def check_time(self) -> None:

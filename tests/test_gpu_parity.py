@@ -386,7 +386,7 @@ def test_rank_above_block_limit_continues_on_dense_path():
 # ------------------------------------------------- solves to tolerance, full size
 
 FULL_CASES = [("cfg2_full.npz", 1, 0), ("cfg5s0_full.npz", 4, 0), ("cfg5s1_full.npz", 4, 1),
-              ("cfg4_full.npz", 3, 0)]
+              ("cfg5s2_full.npz", 4, 2), ("cfg5s3_full.npz", 4, 3), ("cfg4_full.npz", 3, 0)]
 
 
 @pytest.mark.parametrize("fname,idx,seed", FULL_CASES)
