@@ -124,12 +124,19 @@ def cpu_model() -> str:
 # Share of a config-2 solve's iterations spent at each target rank (rank path
 # [(0, 10), (k1, 20)] of the solve to tolerance; tests/golden/cfg2_full.npz when
 # the reference-to-tolerance fixture is present, else the GPU solve's own path).
+# rank paths of the solves to tolerance measured on the B200 (used by the
+# reference arm when the reference-to-tolerance fixture is not in the tree)
+MEASURED_RANK_PATHS = {1: ([(0, 10), (24118, 20)], 30920)}
+
+
 def rank_shares(idx: int, fallback=None):
     path = os.path.join(ROOT, "tests", "golden", f"cfg{idx + 1}_full.npz")
     try:
         d = np.load(path)
         rp, iters = d["rank_path"], int(d["iters"])
     except (OSError, KeyError, ValueError):
+        if fallback is None:
+            fallback = MEASURED_RANK_PATHS.get(idx)
         if fallback is None:
             return None
         rp, iters = np.asarray(fallback[0]), int(fallback[1])
@@ -217,7 +224,7 @@ def run_reference(args, rank, world):
     for q, r in enumerate(ranks):
         b = burn if q == 0 else max(args.warmup * per_step, args.ref_burn_in // 5)
         dt = oracle_stamps(prob, cfg, b + args.steps * per_step, initial_rank=r)
-        t_rank[r] = float(np.sum(dt[b:])) / (args.steps * per_step)
+        t_rank[r] = float(np.median(dt[b:]))
     s_per_it = sum(shares[r] * t_rank[r] for r in ranks)
     value = 1.0 / s_per_it
     cores = os.cpu_count()
@@ -233,9 +240,9 @@ def run_reference(args, rank, world):
                    "s_per_iteration_by_rank": {str(r): t_rank[r] for r in ranks},
                    "rank_shares": {str(r): shares[r] for r in ranks}},
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores, "kind": "port",
-                         "sample": f"{its} timed LR-PDHG iterations per rank (after {burn} burn-in iterations at the "
-                                   f"initial rank) of {wname} with numpy/scipy (OpenBLAS, ARPACK) on all host "
-                                   f"threads, weighted by the solve's iteration share at each rank"},
+                         "sample": f"median s/iteration over {its} timed LR-PDHG iterations per rank (after {burn} burn-in "
+                                   f"iterations at the initial rank) of {wname} with numpy/scipy (OpenBLAS, ARPACK) on "
+                                   f"all host threads, weighted by the solve's iteration share at each rank"},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -386,9 +393,14 @@ def run_ours(args, rank, world, local_rank):
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        shares = rank_shares(idx, fallback=(o.rank_path, o.it.k))
-        cpu = cpu_reference(prob, cfg, shares, alpha=alpha, span=(100, 100 + args.cpu_iters),
-                            span_hi=(20, 20 + max(10, args.cpu_iters // 3)))
+        # in a fresh interpreter (no CUDA context, no torch thread pools): the
+        # same environment as the --impl reference arm
+        leg = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-leg", "--workload", args.workload,
+                              "--cpu-iters", str(args.cpu_iters)], capture_output=True, text=True)
+        try:
+            cpu = json.loads([ln for ln in leg.stdout.splitlines() if ln.startswith("{")][-1])
+        except (IndexError, ValueError):
+            cpu = {"error": (leg.stderr or leg.stdout)[-400:]}
     # ---- BASELINE config 5 as one batch over the ranks, measured once ----
     batch.close()
     brec = None
@@ -571,12 +583,20 @@ def main():
     ap.add_argument("--batch-instances", type=int, default=32,
                     help="config-5 instances of the once-per-run batch record (0 = skip)")
     ap.add_argument("--launcher-check", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--instances", type=int, default=256, help="cfg5: number of instances")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
         return spawn_ranks(args.gpus)
+    if args.cpu_leg:      # the cpu_baseline leg of the GPU arm, in its own process
+        from paper_1810_05231_b200 import workloads
+        idx, _ = WORKLOADS[args.workload]
+        prob, cfg = workloads.config(idx, seed=0)
+        print(json.dumps(cpu_reference(prob, cfg, rank_shares(idx), span=(100, 100 + args.cpu_iters),
+                                       span_hi=(20, 20 + max(10, args.cpu_iters // 3)))), flush=True)
+        return 0
     rank, world, local_rank = env_rank()
     if args.launcher_check:
         return launcher_check(rank, world)
