@@ -160,15 +160,7 @@ def test_config1_end_to_end_matches_reference():
     assert [tuple(x) for x in res.rank_path] == [tuple(x) for x in d["rank_path"].tolist()]
     assert rel(res.X.data, d["X_final"]) <= ITER_TOL
     assert res.primal_objective == pytest.approx(float(d["pobj"]), rel=OBJ_TOL)
-    same_path = res.rank_path == ref_path
-    if same_path:
-        assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
-    else:
-        # different rank-doubling times = a different trajectory to the same
-        # optimum: the dual objective of either run is only as accurate as its
-        # duality gap at the 1e-4 stop (config 4: gap 1.0e-3, difference 1.3e-4)
-        gap = abs(float(d["pobj"]) - float(d["dobj"]))
-        assert abs(res.dual_objective - float(d["dobj"])) <= gap
+    assert res.dual_objective == pytest.approx(float(d["dobj"]), rel=OBJ_TOL)
     assert len(res.checkpoints) == len(d["checkpoints"])
     for c, (rk, obj) in zip(res.checkpoints, d["checkpoints"]):
         assert c.rank == int(rk) and c.objective == pytest.approx(obj, rel=OBJ_TOL)
@@ -178,7 +170,8 @@ def test_config1_end_to_end_matches_reference():
 
 
 @pytest.mark.parametrize("idx,fname", [(4, "cfg5_sketch.npz"), (3, "cfg4_sketch.npz"),
-                                       (1, "cfg2_sketch.npz"), (2, "cfg3_sketch.npz")])
+                                       (1, "cfg2_sketch.npz"), (2, "cfg3_sketch.npz"),
+                                       (2, "cfg3_stall_sketch.npz")])
 def test_large_configs_fixed_K_sketches(idx, fname):
     """Configs 2-5 at the reference's full sizes, fixed K: y, diag(X), the
     sketch X z for a seeded z, ||X||_F, tr(CX) and the residuals."""
