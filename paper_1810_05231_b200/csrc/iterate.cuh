@@ -1276,14 +1276,39 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     const int nzl = d.zptr[x.r1] - s.zoff;
     for (int e = tid; e < nzl; e += blockDim.x) const_cast<double*>(static_cast<const double*>(s.zvs))[e] = zv[s.zoff + e];
   }
-  for (int it = tid; it < (x.r1 - x.r0) * b; it += blockDim.x) {
-    const int lq_ = fdiv(it, b);
-    const int rho = x.r0 + lq_, j = it - lq_ * b;
-    double* Vr = d.V + (size_t)rho * ld;
-    if (!rerun && j < rF) d.F[(size_t)rho * ld + j] = (s.lamF[j] != 0.0) ? Vr[j] : 0.0;
-    if (s.own && j < rF) s.SF[(size_t)(rho - x.r0) * s.sld + j] = rerun ? d.F[(size_t)rho * ld + j] : ((s.lamF[j] != 0.0) ? Vr[j] : 0.0);
-    if (j >= b_old) Vr[j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
+  // F <- V[:, :rF] masked by the clip (own rows; also into shared memory).
+  // Four loads are issued before their stores: a plain copy loop pays one L2
+  // round trip per trip (the stores may alias the loads for the compiler).
+  if (rF > 0) {
+    const int tot = (x.r1 - x.r0) * rF;
+    const double* srcm = rerun ? d.F : d.V;
+    for (int it0 = tid; it0 < tot; it0 += 4 * blockDim.x) {
+      double v[4];
+      int lr_[4], j_[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int it = it0 + u * blockDim.x;
+        lr_[u] = fdiv(min(it, tot - 1), rF);
+        j_[u] = min(it, tot - 1) - lr_[u] * rF;
+        v[u] = __ldcg(srcm + (size_t)(x.r0 + lr_[u]) * ld + j_[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int it = it0 + u * blockDim.x;
+        if (it < tot) {
+          const double f = (rerun || s.lamF[j_[u]] != 0.0) ? v[u] : 0.0;
+          if (!rerun) d.F[(size_t)(x.r0 + lr_[u]) * ld + j_[u]] = f;
+          if (s.own) s.SF[(size_t)lr_[u] * s.sld + j_[u]] = f;
+        }
+      }
+    }
   }
+  if (b > b_old)      // fresh block columns (cold start, rank change)
+    for (int it = tid; it < (x.r1 - x.r0) * (b - b_old); it += blockDim.x) {
+      const int lq_ = fdiv(it, b - b_old);
+      const int rho = x.r0 + lq_, j = b_old + it - lq_ * (b - b_old);
+      d.V[(size_t)rho * ld + j] = hash_uniform(0x5EEDull + (uint64_t)st->seed, (uint64_t)rho, (uint64_t)j);
+    }
   for (int it = tid; it < (x.r1 - x.r0) * d.nd; it += blockDim.x) {
     const int rho = x.r0 + it / d.nd, q = it % d.nd;
     const double u = d.du[(size_t)q * n + rho];
