@@ -1818,6 +1818,32 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   const double* yk = ctl.ypar ? d.ybuf1 : d.ybuf0;
   double* yn = ctl.ypar ? d.ybuf0 : d.ybuf1;
   const int rN = (r < b) ? r : b;
+  // Own rows of V (= X_k+1's factor) into shared memory for the residual
+  // algebra below (P = V^T F, F_perp = F - V P, G = F_perp^T F_perp): the
+  // staging area is idle after the eigensolver, and Gram products / row
+  // updates fed from L2 wait one round trip per step.  Four loads in flight.
+  const int nlo = x.r1 - x.r0;
+  const bool tsm = s.own && 3 * nlmax * lcap <= ycap;
+  double* SV = s.A + 4 * (size_t)lcap * lds;      // nlo x rN
+  double* SFp = SV + (size_t)nlo * lcap;          // nlo x rF
+  if (tsm) {
+    const int tot = nlo * rN;
+    for (int it0 = tid; it0 < tot; it0 += 4 * blockDim.x) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int it = min(it0 + u * (int)blockDim.x, tot - 1);
+        const int lr = fdiv(it, rN);
+        v[u] = __ldcg(d.V + (size_t)(x.r0 + lr) * ld + (it - lr * rN));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int it = it0 + u * blockDim.x;
+        if (it < tot) SV[it] = v[u];
+      }
+    }
+    // visible to the Gram product after the dual step's barrier
+  }
   // dense rank-one rows: <D, X> = sig u^T X u from p = V^T u (X+) and q = F^T u (X_k)
   __shared__ double dsum_sm[2 * PDSDP_NDMAX];   // [2q]: sig u^T(2X+ - X)u, [2q+1]: sig u^T(X+ - X)u
   if (d.nd > 0) {
@@ -1901,7 +1927,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     // P = V^T F (own rows) rides along: the dense part of the primal residual
     // is evaluated in factored form (see dense_residual_lowrank)
     prof_tick(pf, 50);
-    gram_mma(d.V, rN, d.F, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 2, s.gsc);
+    if (tsm) gram_mma2<true, true>(SV, rN, rN, s.SF, s.sld, rF, 0, nlo, red_slot(d, x, x.c) + 2, s.gsc);
+    else gram_mma(d.V, rN, d.F, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 2, s.gsc);
     prof_tick(pf, 51);
     if (tid == 0) {
       double a = 0.0, a2 = 0.0, ff = 1.0;
@@ -1923,13 +1950,23 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   for (int i = tid; i < rN * rF; i += blockDim.x) Pm[i] = s.red1[2 + i];
   double* Fp = buf_free_after_passes(d, iav);
   __syncthreads();
-  for (int it = tid; it < (x.r1 - x.r0) * rF; it += blockDim.x) {
-    const int lq_ = fdiv(it, rF);
-    const int rho = x.r0 + lq_, j = it - lq_ * rF;
-    const double* Vr = d.V + (size_t)rho * ld;
-    double a = d.F[(size_t)rho * ld + j];
-    for (int l = 0; l < rN; ++l) a = fma(-Vr[l], Pm[l * rF + j], a);
-    Fp[(size_t)rho * ld + j] = a;
+  if (tsm) {
+    for (int it = tid; it < nlo * rF; it += blockDim.x) {
+      const int lr = fdiv(it, rF), j = it - lr * rF;
+      const double* Vr = SV + (size_t)lr * rN;
+      double a = s.SF[(size_t)lr * s.sld + j];
+      for (int l = 0; l < rN; ++l) a = fma(-Vr[l], Pm[l * rF + j], a);
+      SFp[it] = a;
+    }
+  } else {
+    for (int it = tid; it < (x.r1 - x.r0) * rF; it += blockDim.x) {
+      const int lq_ = fdiv(it, rF);
+      const int rho = x.r0 + lq_, j = it - lq_ * rF;
+      const double* Vr = d.V + (size_t)rho * ld;
+      double a = d.F[(size_t)rho * ld + j];
+      for (int l = 0; l < rN; ++l) a = fma(-Vr[l], Pm[l * rF + j], a);
+      Fp[(size_t)rho * ld + j] = a;
+    }
   }
   __syncthreads();
   prof_tick(pf, 53);
@@ -1993,7 +2030,8 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     }
     __syncthreads();
     prof_tick(pf, 54);
-    gram_mma(Fp, rF, Fp, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 1 + d.nd, s.gsc);
+    if (tsm) gram_mma2<true, true>(SFp, rF, rF, SFp, rF, rF, 0, nlo, red_slot(d, x, x.c) + 1 + d.nd, s.gsc);
+    else gram_mma(Fp, rF, Fp, rF, ld, x.r0, x.r1, red_slot(d, x, x.c) + 1 + d.nd, s.gsc);
     prof_tick(pf, 55);
     if (tid == 0) {
       double a = 0.0, gg = 0.0;
