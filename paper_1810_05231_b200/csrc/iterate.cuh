@@ -1157,6 +1157,10 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     s.scr = p; p += PDSDP_NTHR;
     s.theta = p; p += PDSDP_BMAX; s.res = p; p += PDSDP_BMAX; s.lamF = p; p += PDSDP_BMAX;
     s.lamN = p; p += PDSDP_BMAX; s.dsc = p; p += PDSDP_BMAX; s.cs = p; p += 4 * PDSDP_BMAX;
+    // red1 receives cluster reductions of up to 3 + r^2 values: beyond 4 BMAX
+    // doubles it runs on into gsc (and, above r ~ 57, into the Rayleigh-Ritz
+    // workspaces), all of which are idle between a reduction and the reads of
+    // its result in the residual phase -- keep red1, gsc, A.. in this order
     s.red1 = p; p += 4 * PDSDP_BMAX;
     s.gsc = p; p += PDSDP_GRAM_SCR;
     // A, Q, L, M are Rayleigh-Ritz workspaces: dead while the filter runs, so
