@@ -160,6 +160,79 @@ jacobi_round_kernel(int n, double* __restrict__ W, int t, double tol, unsigned i
   if (threadIdx.x == 0) atomicAdd(rot, 1u);
 }
 
+// The same round with both rows moved by TMA bulk copies (cp.async.bulk,
+// SASS UBLKCP): one thread issues the two row loads against an mbarrier, so a
+// CTA has its whole 16 n bytes in flight at once instead of one 8-byte load
+// per thread; the rotated rows go back with bulk stores from shared memory.
+// Needs 16-byte aligned rows: n even.  Dynamic shared memory: 2 n doubles.
+__device__ __forceinline__ unsigned dp_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(DENSE_THREADS)
+jacobi_round_tma_kernel(int n, double* __restrict__ W, int t, double tol, unsigned int* __restrict__ rot) {
+  extern __shared__ __align__(16) double jsm[];
+  __shared__ double sh[3][DENSE_THREADS / 32];
+  __shared__ __align__(8) unsigned long long mbar;
+  const int nn = n + (n & 1);
+  int p, q;
+  rr_pair(blockIdx.x, t, nn, p, q);
+  if (q >= n) return;
+  double* rp = jsm;
+  double* rq = jsm + n;
+  double* gp = W + (size_t)p * n;
+  double* gq = W + (size_t)q * n;
+  const unsigned bytes = (unsigned)n * 8u;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dp_smem_u32(&mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dp_smem_u32(&mbar)), "r"(2u * bytes) : "memory");
+    for (unsigned off = 0; off < bytes; off += 65536u) {
+      const unsigned piece = min(65536u, bytes - off);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dp_smem_u32(rp) + off), "l"(reinterpret_cast<const char*>(gp) + off), "r"(piece),
+                     "r"(dp_smem_u32(&mbar)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dp_smem_u32(rq) + off), "l"(reinterpret_cast<const char*>(gq) + off), "r"(piece),
+                     "r"(dp_smem_u32(&mbar)) : "memory");
+    }
+  }
+  __syncthreads();       // the barrier is initialised before anyone waits on it
+  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra WAIT_%=;\n\t}"
+               ::"r"(dp_smem_u32(&mbar)) : "memory");
+  double a = 0.0, b = 0.0, d = 0.0;
+  for (int k = threadIdx.x; k < n; k += DENSE_THREADS) {
+    const double x = rp[k], y = rq[k];
+    a = fma(x, x, a); b = fma(y, y, b); d = fma(x, y, d);
+  }
+  a = warp_sum(a); b = warp_sum(b); d = warp_sum(d);
+  if ((threadIdx.x & 31) == 0) { sh[0][threadIdx.x >> 5] = a; sh[1][threadIdx.x >> 5] = b; sh[2][threadIdx.x >> 5] = d; }
+  __syncthreads();
+  a = b = d = 0.0;
+  for (int k = 0; k < DENSE_THREADS / 32; ++k) { a += sh[0][k]; b += sh[1][k]; d += sh[2][k]; }
+  if (!(fabs(d) > tol * sqrt(a * b))) return;
+  const double zeta = (b - a) / (2.0 * d);
+  const double tt = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+  for (int k = threadIdx.x; k < n; k += DENSE_THREADS) {
+    const double x = rp[k], y = rq[k];
+    rp[k] = c * x - s * y;
+    rq[k] = s * x + c * y;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes visible to the bulk stores
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(rot, 1u);
+    for (unsigned off = 0; off < bytes; off += 65536u) {
+      const unsigned piece = min(65536u, bytes - off);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(reinterpret_cast<char*>(gp) + off), "r"(dp_smem_u32(rp) + off), "r"(piece) : "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(reinterpret_cast<char*>(gq) + off), "r"(dp_smem_u32(rq) + off), "r"(piece) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");     // shared memory is released when the CTA exits
+  }
+}
+
 // lam[j] = ||row_j|| - c ; row_j <- row_j / ||row_j||   (one block per row)
 __global__ void eig_finalize_kernel(int n, double* __restrict__ W, const double* __restrict__ scal,
                                     double* __restrict__ lam) {
