@@ -336,6 +336,22 @@ def test_dense_eigensolver_aproj_matches_reference(n, seed, ranks):
             assert rel(P.data, d[pre + "P"]) <= ITER_TOL
 
 
+def test_dense_eigensolver_large_even_n_bulk_copy_rounds():
+    """n = 3072 takes the Jacobi rounds whose rows move by TMA bulk copies
+    (even n >= 3072); the full projection is checked against numpy's eigh, the
+    reference's own dense method (symmat.py:158-161, 223-226)."""
+    n = 3072
+    rng = np.random.default_rng(31)
+    R = rng.standard_normal((n, n))
+    Sd = 0.5 * (R + R.T) / np.sqrt(n)
+    P, lam = pk.aproj_psd(pk.SymMatrix.from_dense(Sd), n)
+    w, V = np.linalg.eigh(Sd)
+    assert lam == pytest.approx(w[0], abs=1e-9)
+    keep = w > 0
+    ref = (V[:, keep] * w[keep]) @ V[:, keep].T
+    assert rel(_unpack(n, P.data), ref) <= ITER_TOL
+
+
 def test_exact_solver_above_block_limit_matches_reference():
     """solve_pd_sdp with n = 100 > PDSDP_BLOCK_MAX: every iteration is a full
     projection on the dense-iterate path (reference pdhg.py:221-288 with
