@@ -127,6 +127,8 @@ struct pdsdp_batch {
   int timing = 0;
   int verify_residual = 0;   // also run residual_kernel (exact dense term) after each step
   int dense_no_tma = 0;      // PDSDP_DENSE_NO_TMA=1: plain-load Jacobi rounds (A/B of the bulk-copy kernel)
+  int dense_no_block = 0;    // PDSDP_DENSE_NO_BLOCK=1: scalar-rotation rounds for every n (A/B of the blocked kernel)
+  int bj_nmin = PDSDP_BJ_NMIN;   // smallest n taking the blocked rounds (PDSDP_DENSE_BLOCK_NMIN overrides: tests)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   double t_iter = 0.0, n_iter = 0.0, t_res = 0.0, n_res = 0.0, n_launch = 0.0;
   cudaEvent_t tev[PDSDP_KMAX + 1] = {};
@@ -607,7 +609,7 @@ int dense_alloc(Instance* I) {
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += (b + 255) & ~size_t(255); };
   add(nn * 8); add(nn * 8); add(nn * 8); add(n * 8); add(n * 8); add(n * 4); add(n * 8);
-  add(4 * DENSE_PART_MAX * 8); add(DENSE_SCAL * 8); add(64); add(rowt * 8);
+  add(4 * DENSE_PART_MAX * 8); add(DENSE_SCAL * 8); add(64); add(64); add(rowt * 8);
   CK(cudaMalloc(&I->dense_mem, bytes + 4096));
   CK(cudaMemset(I->dense_mem, 0, bytes + 4096));
   Arena a{(char*)I->dense_mem, 0, bytes + 4096};
@@ -617,6 +619,7 @@ int dense_alloc(Instance* I) {
   D.lam = a.take<double>(n); D.lams = a.take<double>(n); D.idx = a.take<int>(n); D.rowsum = a.take<double>(n);
   D.part = a.take<double>(4 * DENSE_PART_MAX); D.scal = a.take<double>(DENSE_SCAL);
   D.rot = a.take<unsigned>(4);
+  D.maxoff = a.take<unsigned long long>(2);
   I->d_rowt = a.take<double>(rowt - 2);
   return PDSDP_OK;
 }
@@ -658,6 +661,8 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
   CK(cudaGetDevice(&dev));
   pdsdp_batch* b = new pdsdp_batch();
   if (const char* e = getenv("PDSDP_DENSE_NO_TMA")) b->dense_no_tma = atoi(e);
+  if (const char* e = getenv("PDSDP_DENSE_NO_BLOCK")) b->dense_no_block = atoi(e);
+  if (const char* e = getenv("PDSDP_DENSE_BLOCK_NMIN")) b->bj_nmin = std::max(BJ_B2, atoi(e));
   int maxn = 0;
   for (int k = 0; k < count; ++k) maxn = std::max(maxn, (int)problems[k].n);
   int C = 1;
@@ -1213,6 +1218,28 @@ int pdsdp_iterate_dense(pdsdp_batch* b, int inst, int32_t r, int32_t ypar, doubl
   const bool tma = (n % 2 == 0) && n >= 3072 && !b->dense_no_tma;
   const double tol = std::max(1e-15, 2.0 * 2.220446049250313e-16 * std::sqrt((double)n));
   int sweeps = 0, conv = (n == 1) ? 1 : 0;
+  if (n >= b->bj_nmin && !b->dense_no_block) {
+    // blocked rounds: one CTA per pair of 16-row blocks (dense_path.cuh)
+    const int nbk = (n + BJ_BS - 1) / BJ_BS, nbe = nbk + (nbk & 1);
+    const size_t bsm = block_jacobi_smem_bytes();
+    CK(cudaFuncSetAttribute(block_jacobi_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+    // the in-CTA eigensolve leaves rows orthogonal to ~1e-14 ||G||_F / g_ii (its rotation
+    // threshold), a few 1e-14 relative: the sweep test sits above that floor
+    const double tolb = std::max(2e-13, 16.0 * 2.220446049250313e-16 * std::sqrt((double)n));
+    for (; sweeps < 60 && !conv; ++sweeps) {
+      CK(cudaMemsetAsync(D.maxoff, 0, sizeof(unsigned long long), s));
+      for (int t = 0; t < nbe - 1; ++t)
+        block_jacobi_round_kernel<<<nbe / 2, BJ_THREADS, bsm, s>>>(n, D.W, t, nbk, tolb, D.maxoff);
+      CK(cudaGetLastError());
+      unsigned long long bits = 0;
+      CK(cudaMemcpyAsync(&bits, D.maxoff, sizeof(bits), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      b->n_launch += nbe - 1;
+      double mo;
+      memcpy(&mo, &bits, sizeof(mo));
+      if (!(mo > tolb)) conv = 1;
+    }
+  } else
   for (; n > 1 && sweeps < 60 && !conv; ++sweeps) {
     CK(cudaMemsetAsync(D.rot, 0, sizeof(unsigned), s));
     for (int t = 0; t < nn - 1; ++t) {

@@ -352,6 +352,30 @@ def test_dense_eigensolver_large_even_n_bulk_copy_rounds():
     assert rel(_unpack(n, P.data), ref) <= ITER_TOL
 
 
+def test_dense_eigensolver_blocked_rounds(monkeypatch):
+    """The blocked Jacobi rounds (16-row blocks, in-CTA Gram eigensolve; taken
+    for n >= 4096) forced at n = 300 / 515 (odd block count, ragged last
+    block) against the reference's dense-path outputs and numpy eigh."""
+    monkeypatch.setenv("PDSDP_DENSE_BLOCK_NMIN", "32")
+    from conftest import dense_case_matrix
+    d = load_golden("dense.npz")
+    S = pk.SymMatrix.from_dense(dense_case_matrix(300, 12))
+    zs = np.random.default_rng(777).standard_normal((300, 4))
+    for r in (200, 300):
+        P, lam = pk.aproj_psd(S, r)
+        Pd = _unpack(300, P.data)
+        assert lam == pytest.approx(float(d[f"ap_n300_r{r}_lam"]), abs=1e-10)
+        assert rel(Pd @ zs, d[f"ap_n300_r{r}_Pz"]) <= ITER_TOL
+    n = 515
+    rng = np.random.default_rng(41)
+    R = rng.standard_normal((n, n))
+    Sd = 0.5 * (R + R.T) / np.sqrt(n)
+    P, lam = pk.aproj_psd(pk.SymMatrix.from_dense(Sd), n)
+    w, V = np.linalg.eigh(Sd)
+    assert lam == pytest.approx(w[0], abs=1e-10)
+    assert rel(_unpack(n, P.data), (V[:, w > 0] * w[w > 0]) @ V[:, w > 0].T) <= ITER_TOL
+
+
 def test_exact_solver_above_block_limit_matches_reference():
     """solve_pd_sdp with n = 100 > PDSDP_BLOCK_MAX: every iteration is a full
     projection on the dense-iterate path (reference pdhg.py:221-288 with
