@@ -86,3 +86,51 @@ def test_rank_shares_from_rank_path():
     assert sh == {10: 0.75, 20: 0.25}
     sh = bench.rank_shares(1)                            # fixture or the measured path of config 2
     assert abs(sum(sh.values()) - 1.0) < 1e-12 and set(sh) == {10, 20}
+
+
+def test_unfinished_step_switches_the_instance_to_the_dense_path():
+    """A chunk that reports a step needing more than an eigen block (output slot
+    13) counts the steps before it and continues on the dense path from the
+    same (X_k, y_k) -- the reference's dense fallback, symmat.py:181-185."""
+    from paper_1810_05231_b200.device import OUT_ERR
+
+    class Stub(_StubBatch):
+        def __init__(self, prob):
+            super().__init__(prob)
+            self.dense_calls = []
+
+        def dense_begin(self, inst, from_factored):
+            self.dense_calls.append((inst, from_factored))
+
+    prob = workloads.maxcut_problem(40, 0.2, 1, signed=True)
+    cfg = SolverConfig(eps_tol=1e-9, initial_rank=2, window_ell=50, max_iter=10_000)
+    rng = np.random.default_rng(7)
+    batch = Stub(prob)
+    run = _InstanceRun(batch, 0, prob, cfg, 0.5, None, 0.0)
+    run.after_chunk(_chunk(rng, 1, 5.0), 1, 1)
+    out = _chunk(rng, 16, 4.0)
+    out[9, OUT_ERR] = 1.0                     # step 9 did not complete
+    run.after_chunk(out, 9, 16)
+    assert run.k == 1 + 1 + 9 - 1 + 1 and run.it.k == 10
+    assert run.dense and batch.dense_calls == [(0, True)] and run.dense_from == run.k
+
+
+def test_guard_columns_grow_at_rank_changes_of_many_pass_phases():
+    prob = workloads.maxcut_problem(40, 0.2, 1, signed=True)
+    cfg = SolverConfig(eps_tol=1e-9, initial_rank=2, window_ell=12, max_iter=10_000)
+    rng = np.random.default_rng(8)
+    run = _InstanceRun(_StubBatch(prob), 0, prob, cfg, 0.5, None, 0.0)
+    run.after_chunk(_chunk(rng, 1, 5.0), 1, 1)
+    many = _chunk(rng, 12, 4.0)
+    many[:, OUT_PASSES] = 5                   # a phase that keeps needing five passes
+    run.after_chunk(many, 12, 12)
+    assert run.guard == 0 and run.flags() == 0
+    bump = _chunk(rng, 12, 3.5, stall_at=11)  # the stall rule doubles the rank here
+    bump[:, OUT_PASSES] = 5
+    run.after_chunk(bump, 12, 12)
+    assert run.controller.r == 4 and run.guard == 2 and run.flags() == 2 << 8
+    calm = _chunk(rng, 12, 3.0, stall_at=11)  # one-pass phase: no further growth
+    calm[:, OUT_PASSES] = 1
+    run.after_chunk(_chunk(rng, 12, 3.2), 12, 12)
+    run.after_chunk(calm, 12, 12)
+    assert run.controller.r == 8 and run.guard == 2
