@@ -579,11 +579,20 @@ __device__ __forceinline__ void operator_step(const Inst& d, Cta& x, const Sm& s
 #define PDSDP_OWN_ITEMS 3      // (row, 4-column chunk) items per thread
 #endif
 __device__ __forceinline__ int own_stride(int bc) { return (bc + 3) & ~3; }
-// row stride of the compact operand block: an odd number of 16-byte units,
-// so the 16-byte loads of different rows at the same column chunk fall in
-// different shared-memory bank groups (a multiple of 128 bytes put them all
-// in the same group: 2-way conflicts on every operand load)
-__device__ __forceinline__ int own_ystr(int bc) { return own_stride(bc) + 2; }
+// row stride of the compact operand block: the smallest odd number of 16-byte
+// units that holds the bc columns, so the 16-byte loads of different rows at
+// the same column chunk fall in different shared-memory bank groups (a
+// multiple of 128 bytes put them all in the same group: 2-way conflicts on
+// every operand load).  It may be shorter than the 4-column chunks' span
+// (bc = 22: 22 doubles for 6 chunks): the last chunk's upper load then reads
+// the next row's first two entries, which only feed discarded columns.  A
+// tighter stride is fewer multicast bytes and more rows per staging group
+// (n = 2000, rank 20: 3 row groups per operator step instead of 4).
+__device__ __forceinline__ int own_ystr(int bc) {
+  int u = (bc + 1) >> 1;
+  if (!(u & 1)) ++u;
+  return 2 * u;
+}
 // the locked pairs' own rows are copied next to F's in shared memory when
 // they fit the row stride of SF
 __device__ __forceinline__ bool own_lock_sm(int rFx, int nlock, int sl) { return nlock > 0 && rFx + nlock <= sl; }
@@ -883,7 +892,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
       const int lr = lr0 + u * rps;
       if (!tact || lr >= nl) break;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) yo[(size_t)lr * ys_ + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
+      for (int v = 0; v < 4; ++v)
+        if (4 * cq + v < ys_) yo[(size_t)lr * ys_ + 4 * cq + v] = (4 * cq + v < bc) ? zacc[u][v] : 0.0;
     }
     __syncthreads();
     prof_tick(pf, 27);
@@ -1186,7 +1196,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     {
       const int nl = x.r1 - x.r0, sp = own_ystr(lcap);
       s.own = (owncap > 0 && nl * lcap <= owncap && nl <= nlmax && nl * sp <= s.ycap &&
-               nl <= PDSDP_OWN_ITEMS * (PDSDP_NTHR / (sp / 4))) ? 1 : 0;
+               nl <= PDSDP_OWN_ITEMS * (PDSDP_NTHR / (own_stride(lcap) / 4))) ? 1 : 0;
     }
   }
   __shared__ __align__(8) unsigned long long mbar_sm;   // completion barrier of the operand all-gather
