@@ -439,13 +439,27 @@ __device__ __forceinline__ void rotate_rows(const Inst& d, const Cta& x, const d
   }
 }
 
-// rows [0, nl) of a b-column block, global (stride ld) -> shared (stride b)
+// rows [0, nl) of a b-column block, global (stride ld) -> shared (stride b).
+// With an even b (rows and dst 16-byte aligned) the copy is issued as 16-byte
+// cp.async (global -> shared without a register stage): every transfer of the
+// block is in flight at once, where a plain copy loop pays one L2 round trip
+// per trip -- and holding several loads in registers instead spills in the
+// Rayleigh-Ritz section.  The caller's copies are completed by copy_rows_wait().
 __device__ __forceinline__ void copy_rows_in(const double* __restrict__ src, int ld, double* dst, int nl, int b) {
+  if ((b & 1) == 0 && (ld & 1) == 0) {
+    const int hp = b >> 1, tot = nl * hp;
+    for (int it = threadIdx.x; it < tot; it += blockDim.x) {
+      const int lr = fdiv(it, hp), j2 = it - lr * hp;
+      cp_async16(dst + 2 * it, src + (size_t)lr * ld + 2 * j2);
+    }
+    return;
+  }
   for (int it = threadIdx.x; it < nl * b; it += blockDim.x) {
     const int lr = fdiv(it, b), j = it - lr * b;
     dst[it] = src[(size_t)lr * ld + j];
   }
 }
+__device__ __forceinline__ void copy_rows_wait() { cp_async_wait_all(); }
 
 // out (nl x b) = In (nl x b, shared memory) * Msm (b x b, shared memory) on
 // FP64 tensor cores (mma.sync.m8n8k4.f64): one warp per 8-row tile, all
@@ -694,8 +708,8 @@ __device__ __forceinline__ void operator_step_own(const Inst& d, Cta& x, const S
     double* yo = s.ys;
     {
       const double* src = Ycur + (size_t)x.r0 * ys_;
-      for (int i = tid; i < nl * ys_ / 2; i += blockDim.x)
-        reinterpret_cast<double2*>(yo)[i] = __ldcg(reinterpret_cast<const double2*>(src) + i);
+      for (int i = tid; i < nl * ys_ / 2; i += blockDim.x) cp_async16(yo + 2 * i, src + 2 * i);   // all in flight, no register stage
+      cp_async_wait_all();
     }
     __syncthreads();
     double* slot = red_slot(d, x, x.c);
@@ -1606,6 +1620,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       prof_mark(pf, 5);
       copy_rows_in(buf(iy) + (size_t)x.r0 * ld, ld, S1, nlr, b);
       copy_rows_in(buf(iw) + (size_t)x.r0 * ld, ld, S2, nlr, b);
+      copy_rows_wait();
       __syncthreads();
       gram_mma2<true, true>(S1, b, b, S2, b, b, 0, nlr, red_slot(d, x, x.c), s.gsc);   // H0 = Y^T W
       prof_mark(pf, 4);
@@ -1621,9 +1636,11 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
     prof_mark(pf, 5);
     if (rsm) {
       copy_rows_in(buf(iy) + (size_t)x.r0 * ld, ld, S0, nlr, b);
+      copy_rows_wait();
       __syncthreads();
       rot_mma(S0, b, nullptr, 0, s.M, lds, S1, b, nullptr, 0, nlr, b, nullptr, nullptr, nullptr);
       copy_rows_in(buf(iw) + (size_t)x.r0 * ld, ld, S0, nlr, b);
+      copy_rows_wait();
       __syncthreads();
       rot_mma(S0, b, nullptr, 0, s.M, lds, S2, b, nullptr, 0, nlr, b, nullptr, nullptr, nullptr);
     } else {
