@@ -1428,9 +1428,26 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const size_t nld = (size_t)n * (ld + 4);
       int ycp = 0;
       bool gram_ready = false;
-      for (int it = tid; it < nl * bc; it += blockDim.x) {
-        const int lr = fdiv(it, bc), jj = it - lr * bc;
-        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = d.V[(size_t)(x.r0 + lr) * ld + c0 + jj];
+      if (((bc | c0) & 1) == 0) {
+        // bounce through the (idle) staging buffer: cp.async in, 16-byte stores out
+        double* yb_ = s.ys;
+        const int hp = bc >> 1;
+        for (int it = tid; it < nl * hp; it += blockDim.x) {
+          const int lr = fdiv(it, hp), j2 = it - lr * hp;
+          cp_async16(yb_ + (size_t)lr * bcp + 2 * j2, d.V + (size_t)(x.r0 + lr) * ld + c0 + 2 * j2);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        for (int it = tid; it < nl * hp; it += blockDim.x) {
+          const int lr = fdiv(it, hp), j2 = it - lr * hp;
+          *reinterpret_cast<double2*>(d.Yc + (size_t)(x.r0 + lr) * bcp + 2 * j2) =
+              *reinterpret_cast<const double2*>(yb_ + (size_t)lr * bcp + 2 * j2);
+        }
+      } else {
+        for (int it = tid; it < nl * bc; it += blockDim.x) {
+          const int lr = fdiv(it, bc), jj = it - lr * bc;
+          d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = d.V[(size_t)(x.r0 + lr) * ld + c0 + jj];
+        }
       }
       if (own_lock_sm(rFx, nlock, s.sld))
         for (int it = tid; it < nl * nlock; it += blockDim.x) {
@@ -1531,11 +1548,29 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const int nl = x.r1 - x.r0, bcp = own_ystr(b);   // compact row stride
       prof_mark(pf, 1);
       double* yo = s.ys;   // own rows for the G1 product (staging buffer idle until the step's barrier)
-      for (int it = tid; it < nl * b; it += blockDim.x) {
-        const int lr = fdiv(it, b), jj = it - lr * b;
-        const double v = buf(iy)[(size_t)(x.r0 + lr) * ld + jj];
-        d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
-        yo[(size_t)lr * bcp + jj] = v;
+      if ((b & 1) == 0) {
+        // global -> shared by cp.async (every transfer in flight, no registers), then
+        // shared -> the compact multicast source; a copy loop through registers
+        // waits for one L2 round trip per trip
+        const int hp = b >> 1;
+        for (int it = tid; it < nl * hp; it += blockDim.x) {
+          const int lr = fdiv(it, hp), j2 = it - lr * hp;
+          cp_async16(yo + (size_t)lr * bcp + 2 * j2, buf(iy) + (size_t)(x.r0 + lr) * ld + 2 * j2);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        for (int it = tid; it < nl * hp; it += blockDim.x) {
+          const int lr = fdiv(it, hp), j2 = it - lr * hp;
+          *reinterpret_cast<double2*>(d.Yc + (size_t)(x.r0 + lr) * bcp + 2 * j2) =
+              *reinterpret_cast<const double2*>(yo + (size_t)lr * bcp + 2 * j2);
+        }
+      } else {
+        for (int it = tid; it < nl * b; it += blockDim.x) {
+          const int lr = fdiv(it, b), jj = it - lr * b;
+          const double v = buf(iy)[(size_t)(x.r0 + lr) * ld + jj];
+          d.Yc[(size_t)(x.r0 + lr) * bcp + jj] = v;
+          yo[(size_t)lr * bcp + jj] = v;
+        }
       }
       fence_proxy_async();
       __syncthreads();
