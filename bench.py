@@ -51,7 +51,7 @@ WORKLOADS = {
 FP64_DMMA_TFLOPS = 37.1   # measured on this pool's B200 (profiles/r01_fp64_cluster_probe.txt)
 # dram__bytes_read.sum + dram__bytes_write.sum of one iteration at rank 20 from the
 # last committed `ncu --set full` capture of the iteration kernel (archived, per commit)
-ARCHIVED_TRAFFIC = (2867712, "profiles/r02_iterate_kernel_ncu_raw_r20.csv (archived capture)")
+ARCHIVED_TRAFFIC = (2874624, "profiles/r02_iterate_kernel_ncu_raw_r20.csv (archived capture)")
 
 
 def env_rank():
@@ -376,7 +376,7 @@ def run_ours(args, rank, world, local_rank):
     roof = {"kernel": "lrpdhg_iterate_kernel (one launch = one PDHG iteration, residuals included)",
             "bound": "hbm", "achieved": achieved, "peak": B / 1e9, "unit": "GB/s", "frac": achieved / (B / 1e9),
             # dram__bytes_read.sum + dram__bytes_write.sum of one iteration-kernel
-            # launch = one iteration at the final rank (ncu --set full; 2060800 at
+            # launch = one iteration at the final rank (ncu --set full; 2067456 at
             # rank 10): the iterate stays L2-resident, the kernel is latency-bound
             # archived figure of that capture (not re-measured by this run)
             "traffic": ARCHIVED_TRAFFIC[0], "traffic_source": ARCHIVED_TRAFFIC[1],
