@@ -25,6 +25,15 @@ records, for seeded inputs built with ``paper_1810_05231_b200.workloads``:
   residuals, tr(CX), ||X||_F and the sketch X @ z for a seeded z (sketches
   keep the fixtures small while pinning the full n x n iterate).
 
+* ``dense.npz``       — where the reference runs dense eigh: aproj_psd at n = 100 /
+  300 with large r, exact PD-SDP at n = 100, an LR run whose rank crosses 64;
+* ``cfgN_full.npz`` / ``cfg5sK_full.npz`` (``--full cfg2,cfg4,cfg5s0,...``; hours of
+  CPU each) — the UNMODIFIED reference run to tolerance: status, stop iteration,
+  rank path, checkpoints, objectives, residuals, y, the final X as eigen-factors,
+  the progress history every 100 iterations;
+* ``cfg3_stall_sketch.npz`` (``--full cfg3_stall``) — config 3 at K = 510, past its
+  first stall-triggered rank doubling.
+
 The reference crashes on config 4 iteration 1 (ArpackError -9, SURVEY.md §8c
 quirk 1); for that config only the harness wraps ``truncated_eigen`` with the
 reference's own dense fallback (``symmat.py:200-207``).
