@@ -515,6 +515,24 @@ def test_batched_solve_matches_single_instance_solves():
         assert rel(rb.X.data, ro.X) <= ITER_TOL
 
 
+def test_batch_with_instance_switching_to_dense_path():
+    """A batch in which one instance leaves the cluster kernel for the
+    dense-iterate path mid-run (more positive eigenvalues than an eigen block
+    holds) while the others stay on it: every instance matches its own
+    single-instance solve, so the slot scheduler does not mix the two modes."""
+    probs = [workloads.maxcut_problem(60, 0.15, 3, signed=True),
+             workloads.equipartition_problem(150, 0.05, 2),
+             workloads.maxcut_problem(80, 0.1, 4, signed=True)]
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=300, initial_rank=70, window_ell=50, time_limit_s=1e9)
+    batch = pk.solve_lr_pd_sdp_batch(probs, cfg)     # initial_rank is clipped to n per problem
+    for p, rb in zip(probs, batch):
+        rs = pk.solve_lr_pd_sdp(p, cfg)
+        assert rb.status == rs.status and rb.iterations == rs.iterations
+        assert rb.rank_path == rs.rank_path
+        assert rel(rb.X.data, rs.X.data) <= 1e-12
+        assert rel(rb.y, rs.y) <= 1e-12
+
+
 # ------------------------------------------- factored vs entrywise residual
 
 @pytest.mark.parametrize("ci,K,r", [(0, 300, 5), (1, 40, 10), (3, 30, 1), (4, 40, 1)])
