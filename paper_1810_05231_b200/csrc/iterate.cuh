@@ -23,8 +23,12 @@ namespace cg = cooperative_groups;
 namespace pdsdp {
 
 // tolerances of the eigensolver (relative to the spectral scale)
+#ifndef PDSDP_TOL_KEEP
 #define PDSDP_TOL_KEEP 1e-12   // ARPACK's tol in the reference (symmat.py:33), relative to the spectral scale
+#endif
+#ifndef PDSDP_TOL_X
 #define PDSDP_TOL_X 1e-12      // admissible per-iteration error of X+ (relative to ||X+||_F)
+#endif
 #define PDSDP_TOL_CERT 1e-8
 #define PDSDP_TOL_CLIP 1e-6
 #ifndef PDSDP_MMAX
