@@ -62,7 +62,7 @@ struct State {
   int rF_used;      // columns of F (= X_k) used by the last iteration
   int r_cur;        // columns of V (= X_k+1) produced by the last iteration
   int npos;         // positive kept Ritz values of the last iteration (effective-rank hint)
-  int pad1;
+  int fvalid;       // leading columns of F holding eigenvectors of the iteration before (not clipped to zero)
   double theta[PDSDP_BMAX];
   double res[PDSDP_BMAX];
   double lamF[PDSDP_BMAX];   // eigenvalues of X_k   (clipped)

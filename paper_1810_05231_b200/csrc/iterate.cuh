@@ -46,6 +46,11 @@ namespace pdsdp {
 #ifndef PDSDP_STALE_EPS
 #define PDSDP_STALE_EPS 1e-3
 #endif
+// the same after an extrapolated start (PDSDP_EXTRAP below): the kept columns
+// are then ~1e-8 from their targets and the trailing ones ~1e-5
+#ifndef PDSDP_STALE_EPS_X
+#define PDSDP_STALE_EPS_X 1e-3
+#endif
 #ifndef PDSDP_ONEPASS_RR
 #define PDSDP_ONEPASS_RR 1
 #endif
@@ -54,6 +59,18 @@ namespace pdsdp {
 #endif
 #ifndef PDSDP_ONEPASS_ETA
 #define PDSDP_ONEPASS_ETA 0.5   // entrywise bound b * max|E| of the one-pass test (cond <= (1+eta)/(1-eta))
+#endif
+// Start block of the eigensolver: the eigenvectors move smoothly from one
+// iteration to the next (|V_k+1 - 2 V_k + V_k-1| ~ 1e-4 |V_k+1 - V_k| on
+// config 2, tools/gpu_warmstart_extrapolation.py), so the kept columns start
+// from the linear extrapolation 2 V_k - V_k-1 (V_k-1 is still in F when the
+// iteration begins) instead of V_k.  Only the starting point changes; the
+// block is iterated to the same tolerances.
+#ifndef PDSDP_EXTRAP
+#define PDSDP_EXTRAP 1
+#endif
+#ifndef PDSDP_HINT_MIN
+#define PDSDP_HINT_MIN 2        // smallest first-pass filter degree
 #endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
@@ -1311,11 +1328,13 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   // F <- V[:, :rF] masked by the clip (own rows; also into shared memory).
   // Four loads are issued before their stores: a plain copy loop pays one L2
   // round trip per trip (the stores may alias the loads for the compiler).
+  // columns [0, nex) of F still hold V_k-1: their start is 2 V_k - V_k-1
+  const int nex = (PDSDP_EXTRAP && !cold && !rerun && b == b_old && st->theta_valid) ? min(st->fvalid, rF) : 0;
   if (rF > 0) {
     const int tot = (x.r1 - x.r0) * rF;
     const double* srcm = rerun ? d.F : d.V;
     for (int it0 = tid; it0 < tot; it0 += 4 * blockDim.x) {
-      double v[4];
+      double v[4], fo[4];
       int lr_[4], j_[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1323,6 +1342,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         lr_[u] = fdiv(min(it, tot - 1), rF);
         j_[u] = min(it, tot - 1) - lr_[u] * rF;
         v[u] = __ldcg(srcm + (size_t)(x.r0 + lr_[u]) * ld + j_[u]);
+        fo[u] = (j_[u] < nex) ? __ldcg(d.F + (size_t)(x.r0 + lr_[u]) * ld + j_[u]) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1331,6 +1351,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
           const double f = (rerun || s.lamF[j_[u]] != 0.0) ? v[u] : 0.0;
           if (!rerun) d.F[(size_t)(x.r0 + lr_[u]) * ld + j_[u]] = f;
           if (s.own) s.SF[(size_t)lr_[u] * s.sld + j_[u]] = f;
+          if (j_[u] < nex) d.V[(size_t)(x.r0 + lr_[u]) * ld + j_[u]] = 2.0 * v[u] - fo[u];
         }
       }
     }
@@ -1370,7 +1391,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       const double xnorm = kept_norm_w(s.theta, r, b);
       const Assess as = assess_w(s.theta, s.res, r, b, k, scale, xnorm, cert_tol);
       const bool stale = (pass == 0 && !rerun);   // residuals belong to the previous S
-      const double eps_rel = fmax(as.maxres, stale ? PDSDP_STALE_EPS : 0.0);
+      const double eps_rel = fmax(as.maxres, stale ? (nex > 0 ? PDSDP_STALE_EPS_X : PDSDP_STALE_EPS) : 0.0);
       int mcap = PDSDP_MMAX;
       // leading pairs already converged to the kept tolerance: deflate them
       // and filter the rest of the block (a small spread admits the degree the
@@ -2162,12 +2183,17 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
       for (int i = 0; i < rN; ++i) np += (s.theta[i] > 0.0) ? 1 : 0;
       st->npos = np;
       st->theta_valid = theta_valid ? 1 : 0;
+      {   // leading columns of F (this iteration's X_k factor) that were not clipped
+        int fv = 0;
+        while (fv < rF && s.lamF[fv] != 0.0) ++fv;
+        st->fvalid = fv;
+      }
       // degree hint for the next iteration's first pass: after a single-pass
       // convergence drop the measured slack (less a safety degree), else the
       // total degree this iteration needed
       if (!rerun && msucc > 0)
         st->mhint = (passes == 1 && converged == 1 && fails == 0)
-                        ? max(2, msucc - max(0, slack - PDSDP_HINT_SAFETY))
+                        ? max(PDSDP_HINT_MIN, msucc - max(0, slack - PDSDP_HINT_SAFETY))
                         : msucc;
       st->iav = iav;
       st->ed2 = ed2_tot;
