@@ -63,6 +63,8 @@ struct State {
   int r_cur;        // columns of V (= X_k+1) produced by the last iteration
   int npos;         // positive kept Ritz values of the last iteration (effective-rank hint)
   int fvalid;       // leading columns of F holding eigenvectors of the iteration before (not clipped to zero)
+  int pvalid;       // leading columns of Vp holding the eigenvectors of two iterations before
+  int pad2;
   double theta[PDSDP_BMAX];
   double res[PDSDP_BMAX];
   double lamF[PDSDP_BMAX];   // eigenvalues of X_k   (clipped)
@@ -73,6 +75,9 @@ struct State {
   double finite;    // 1 when y+ and theta are finite
   double seed;
   double mhint;     // total filter degree used by the previous iteration
+  double mfloor;    // first-pass degree below which a probe of the hint failed recently
+  double mfloor_age;  // iterations since that failure
+  double q_age;     // iterations since an order-2 extrapolated start last needed a second pass (or since the reset)
   double dbg[32][8];  // per pass: m, worst rel residual, slow column, theta, t, lo, cut, xnorm
   double prof[16];    // SM cycles of CTA 0 per phase in the last launch
   double hdump[PDSDP_BMAX * PDSDP_BMAX + 8];  // diagnostic: last projected matrix H' (flag bit4)
@@ -190,6 +195,7 @@ struct Inst {
   double* Y1;
   double* Y2;
   double* F;
+  double* Vp;          // eigenvector block of two iterations before (start-block extrapolation)
   double* Yc;          // 2 x compact (stride = active width) copies of the filter block (TMA multicast sources)
   double* ybuf0;
   double* ybuf1;

@@ -61,16 +61,29 @@ namespace pdsdp {
 #define PDSDP_ONEPASS_ETA 0.5   // entrywise bound b * max|E| of the one-pass test (cond <= (1+eta)/(1-eta))
 #endif
 // Start block of the eigensolver: the eigenvectors move smoothly from one
-// iteration to the next (|V_k+1 - 2 V_k + V_k-1| ~ 1e-4 |V_k+1 - V_k| on
-// config 2, tools/gpu_warmstart_extrapolation.py), so the kept columns start
-// from the linear extrapolation 2 V_k - V_k-1 (V_k-1 is still in F when the
-// iteration begins) instead of V_k.  Only the starting point changes; the
-// block is iterated to the same tolerances.
+// iteration to the next (on config 2 the second difference of V_k is ~1e-4
+// and the third ~1e-7..1e-8 of the first, tools/gpu_warmstart_extrapolation.py),
+// so the kept columns start from an extrapolation of the last blocks instead
+// of V_k: 2 V_k - V_k-1 (order 1; V_k-1 is still in F when the iteration
+// begins) or 3 V_k - 3 V_k-1 + V_k-2 (order 2; V_k-2 kept in Vp).  Only the
+// starting point changes; the block is iterated to the same tolerances.
 #ifndef PDSDP_EXTRAP
-#define PDSDP_EXTRAP 1
+#define PDSDP_EXTRAP 2
+#endif
+#ifndef PDSDP_QRETRY
+#define PDSDP_QRETRY 128        // iterations at order 1 after an order-2 start needed a second pass
+#endif
+#ifndef PDSDP_QTOL
+#define PDSDP_QTOL 0.1          // kept-pair tolerance factor of an iteration that starts at order 2
+#endif
+#ifndef PDSDP_EXTRAP_WHOLE
+#define PDSDP_EXTRAP_WHOLE 1    // after an order-2 start the first pass filters the whole block (guards included)
 #endif
 #ifndef PDSDP_HINT_MIN
-#define PDSDP_HINT_MIN 2        // smallest first-pass filter degree
+#define PDSDP_HINT_MIN 1        // smallest first-pass filter degree
+#endif
+#ifndef PDSDP_PROBE_AGE
+#define PDSDP_PROBE_AGE 256     // iterations before a failed one-degree-down probe of the hint is retried (0: no probing)
 #endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
@@ -78,6 +91,10 @@ namespace pdsdp {
 
 // Is Ritz pair i accurate enough?  i < r: kept in X+ (clipped at 0);
 // i == r: the certificate eigenvalue lambda_{r+1} (only its value matters).
+// factor on the kept-pair tolerances of the current iteration (1, or
+// PDSDP_QTOL after an order-2 extrapolated start); block-uniform
+__shared__ double g_tolf;
+
 __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, int r, int b,
                                        double scale, double xnorm, double cert_tol) {
   const double th = theta[i];
@@ -93,12 +110,12 @@ __device__ __forceinline__ bool col_ok(int i, double ri, const double* theta, in
   // eigenvalue it will converge to)
   if (th + ri < 0.0 && ri <= PDSDP_TOL_CLIP * scale) return true;
   if (i < r) {
-    if (ri <= PDSDP_TOL_KEEP * scale) return true;
+    if (ri <= PDSDP_TOL_KEEP * g_tolf * scale) return true;
     // remaining effect on X+: |dtheta| <= ri plus rotation ~ 2 theta ri / gap (Davis-Kahan)
     const double thr = (r < b) ? theta[r] : -1.0e308;
     const double gap = th - thr;
     const double impact = ri + 2.0 * fmax(th, 0.0) * fmin(1.0, ri * fast_rcp(fmax(gap, 1e-300)));
-    return impact <= PDSDP_TOL_X * xnorm;
+    return impact <= PDSDP_TOL_X * g_tolf * xnorm;
   }
   // cert_tol < 0: sentinel column of an effective-rank block -- it must be
   // certified non-positive (the clip rule above), its value is not needed
@@ -118,6 +135,8 @@ struct Sm {
   ShPtr<const int> zc;         // staged Z columns of own rows
   ShPtr<const double> zvs;     // staged Z values of own rows
   int zoff, zstaged;
+  int pvalid;                  // leading columns of Vp valid after this iteration's prologue
+  int q_used;                  // this iteration started from the order-2 extrapolation
   ShPtr<double> scr;           // NTHR
   ShPtr<double> theta, res, lamF, lamN, dsc, cs, red1;  // BMAX each (red1: 2*BMAX)
   ShPtr<int> perm, pq, flag;
@@ -1008,7 +1027,7 @@ __device__ Assess assess_w(const double* theta, const double* res, int r, int b,
   // reciprocals by rcp.approx + two Newton steps: the software FP64 division
   // sits on the critical path of every pass (planning needs a few digits)
   const double inv_scale = fast_rcp(scale);
-  const double inv_tk = fast_rcp(fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
+  const double inv_tk = fast_rcp(g_tolf * fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm));
   int last = -1, cert = 0;
   double mr = 0.0, rk = 1.0;
   for (int i = lane; i < k; i += 32) {
@@ -1328,30 +1347,47 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
   // F <- V[:, :rF] masked by the clip (own rows; also into shared memory).
   // Four loads are issued before their stores: a plain copy loop pays one L2
   // round trip per trip (the stores may alias the loads for the compiler).
-  // columns [0, nex) of F still hold V_k-1: their start is 2 V_k - V_k-1
+  // columns [0, nex) of F still hold V_k-1 and columns [0, nex2) of Vp hold
+  // V_k-2: extrapolated start (PDSDP_EXTRAP)
   const int nex = (PDSDP_EXTRAP && !cold && !rerun && b == b_old && st->theta_valid) ? min(st->fvalid, rF) : 0;
+  // order 2 while it pays: an order-2 start that needed a second pass (its
+  // error feedback is 7x the previous errors against 3x at order 1, which
+  // some spectra turn into a period-2 cycle above the tolerance) puts the
+  // instance back to order 1 for PDSDP_QRETRY iterations
+  const int nex2 = (PDSDP_EXTRAP >= 2 && st->q_age >= (double)PDSDP_QRETRY) ? min(nex, st->pvalid) : 0;
+  if (tid == 0) {
+    s.pvalid = rerun ? st->pvalid : nex;     // Vp after this prologue (written to the state at the end)
+    s.q_used = nex2 > 0;
+    g_tolf = (nex2 > 0) ? PDSDP_QTOL : 1.0;
+  }
   if (rF > 0) {
     const int tot = (x.r1 - x.r0) * rF;
     const double* srcm = rerun ? d.F : d.V;
     for (int it0 = tid; it0 < tot; it0 += 4 * blockDim.x) {
-      double v[4], fo[4];
+      double v[4], fo[4], po[4];
       int lr_[4], j_[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int it = it0 + u * blockDim.x;
         lr_[u] = fdiv(min(it, tot - 1), rF);
         j_[u] = min(it, tot - 1) - lr_[u] * rF;
-        v[u] = __ldcg(srcm + (size_t)(x.r0 + lr_[u]) * ld + j_[u]);
-        fo[u] = (j_[u] < nex) ? __ldcg(d.F + (size_t)(x.r0 + lr_[u]) * ld + j_[u]) : 0.0;
+        const size_t o = (size_t)(x.r0 + lr_[u]) * ld + j_[u];
+        v[u] = __ldcg(srcm + o);
+        fo[u] = (j_[u] < nex) ? __ldcg(d.F + o) : 0.0;
+        po[u] = (j_[u] < nex2) ? __ldcg(d.Vp + o) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int it = it0 + u * blockDim.x;
         if (it < tot) {
+          const size_t o = (size_t)(x.r0 + lr_[u]) * ld + j_[u];
           const double f = (rerun || s.lamF[j_[u]] != 0.0) ? v[u] : 0.0;
-          if (!rerun) d.F[(size_t)(x.r0 + lr_[u]) * ld + j_[u]] = f;
+          if (!rerun) d.F[o] = f;
           if (s.own) s.SF[(size_t)lr_[u] * s.sld + j_[u]] = f;
-          if (j_[u] < nex) d.V[(size_t)(x.r0 + lr_[u]) * ld + j_[u]] = 2.0 * v[u] - fo[u];
+          if (j_[u] < nex) {
+            d.V[o] = (j_[u] < nex2) ? 3.0 * (v[u] - fo[u]) + po[u] : 2.0 * v[u] - fo[u];
+            if (PDSDP_EXTRAP >= 2) d.Vp[o] = fo[u];
+          }
         }
       }
     }
@@ -1418,7 +1454,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         const int cap2 = cheb_plan(s.theta, b, lo, s.theta[0], s.theta[b - 1], slow, as.rho_k, scale, eps_rel, m2, e2, c2, s2);
         int want2 = stale ? (hint > 0 ? hint : 4) : max(m2, 2);
         int want1 = stale ? (hint > 0 ? hint : 4) : max(m1, 2);
-        if (cap2 >= min(want2, 6)) { m = min(want2, cap2); mcap = cap2; c0 = 0; bc = b; fe = e2; fc = c2; sig1 = s2; }
+        if (cap2 >= min(want2, 6) || (PDSDP_EXTRAP_WHOLE && stale && nex2 > 0)) { m = min(want2, cap2); mcap = cap2; c0 = 0; bc = b; fe = e2; fc = c2; sig1 = s2; }
         else { m = min(want1, cap1); mcap = cap1; c0 = 0; bc = a1; fe = e1; fc = c1; sig1 = s1; }
       } else if (as.cert_bad || as.tail_bad) {
         // kept pairs converged: lock (deflate) them and filter the tail
@@ -1883,7 +1919,7 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         // each kept column's tolerance (Chebyshev gain acosh(t) per degree)
         if (m > 0 && pass == 0) {
           double sl = 1.0e300;
-          const double tol = fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
+          const double tol = g_tolf * fmax(PDSDP_TOL_KEEP * scale, PDSDP_TOL_X * xnorm);
           const double ife = fast_rcp(fe);
           for (int i = (tid & 31); i < r && i < b; i += 32) {
             const double t = (s.theta[i] - fc) * ife;
@@ -2187,14 +2223,34 @@ lrpdhg_iterate_kernel(const Inst* __restrict__ insts, const Ctl* __restrict__ ct
         int fv = 0;
         while (fv < rF && s.lamF[fv] != 0.0) ++fv;
         st->fvalid = fv;
+        st->pvalid = s.pvalid;
       }
       // degree hint for the next iteration's first pass: after a single-pass
       // convergence drop the measured slack (less a safety degree), else the
-      // total degree this iteration needed
-      if (!rerun && msucc > 0)
-        st->mhint = (passes == 1 && converged == 1 && fails == 0)
-                        ? max(PDSDP_HINT_MIN, msucc - max(0, slack - PDSDP_HINT_SAFETY))
-                        : msucc;
+      // total degree this iteration needed.  Residuals at the rounding floor
+      // (~64 eps scale; the usual case after an extrapolated start) show no
+      // slack however many degrees were surplus, so without measured slack
+      // the hint is probed one degree down; a probe that costs a second pass
+      // is not repeated for PDSDP_PROBE_AGE iterations.
+      if (!rerun && msucc > 0) {
+        const int hused = (int)st->mhint;
+        int fl = (int)st->mfloor, age = (int)st->mfloor_age + 1;
+        int h;
+        if (passes == 1 && converged == 1 && fails == 0) {
+          h = max(PDSDP_HINT_MIN, msucc - max(0, slack - PDSDP_HINT_SAFETY));
+          if (PDSDP_PROBE_AGE > 0 && h == msucc && msucc > PDSDP_HINT_MIN) {
+            if (age > PDSDP_PROBE_AGE) fl = 0;
+            if (msucc - 1 >= fl) h = msucc - 1;
+          }
+        } else {
+          h = msucc;
+          if (hused > 0) { fl = hused + 1; age = 0; }
+        }
+        st->mhint = h;
+        st->mfloor = fl;
+        st->mfloor_age = min(age, 1 << 20);
+        st->q_age = (s.q_used && (passes > 1 || fails > 0)) ? 0.0 : fmin(st->q_age + 1.0, 1048576.0);
+      }
       st->iav = iav;
       st->ed2 = ed2_tot;
       st->corr = corr_tot;

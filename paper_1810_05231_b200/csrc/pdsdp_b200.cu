@@ -389,7 +389,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   add((I.n + 1) * 4); add(I.dslot.size() * 4 + 4); add(I.n * 8 + 8);
   add((I.mp + 1) * 4); add(I.ai.size() * 4 + 4); add(I.aj.size() * 4 + 4); add(I.ag.size() * 8 + 8);
   add((C + 1) * 4); add(I.bv.size() * 8 + 8); add(I.hv.size() * 8 + 8);
-  for (int k = 0; k < 6; ++k) add(nld * 8);
+  for (int k = 0; k < 7; ++k) add(nld * 8);
   add(2 * (size_t)I.n * (I.ld + 4) * 8);
   add(I.mp * 8 + 8); add(I.mp * 8 + 8); add(I.mp * 8 + 8);
   add((size_t)2 * C * PDSDP_RED_MAX * 8);
@@ -460,6 +460,7 @@ int alloc_instance(Instance& I, int C, double* out_dev) {
   d.bv = bv; d.hv = hv;
   d.V = a.take<double>(nld); d.AV = a.take<double>(nld); d.Y0 = a.take<double>(nld);
   d.Y1 = a.take<double>(nld); d.Y2 = a.take<double>(nld); d.F = a.take<double>(nld);
+  d.Vp = a.take<double>(nld);
   d.Yc = a.take<double>(2 * (size_t)I.n * (I.ld + 4));
   d.ybuf0 = a.take<double>(I.mp + 1); d.ybuf1 = a.take<double>(I.mp + 1); d.dy = a.take<double>(I.mp + 1);
   d.red = a.take<double>((size_t)2 * C * PDSDP_RED_MAX);

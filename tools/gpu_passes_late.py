@@ -14,6 +14,11 @@ ypar = K0 & 1
 for k in range(K):
     o = b.iterate([0], [r], [ypar])[0]; ypar ^= 1
     dbg = b.debug(0)
+    if os.environ.get("COMPACT"):
+        rows = dbg["passes"][: int(o[4])]
+        print(f"it {k}: passes {o[4]:.0f} mv {o[5]:.0f} plans", [(int(row[0]), int(row[4] % 1000), f"{row[1]:.1e}") for row in rows],
+              "kept res max %.1e tail res %.1e" % (dbg["res"][:r].max(), dbg["res"][r]))
+        continue
     print(f"it {k}: passes {o[4]:.0f} mv {o[5]:.0f} conv {o[6]:.0f} blk {o[11]:.0f} lam {o[2]:.4e}")
     for row in dbg["passes"][: int(o[4]) + 1]:
         print("   m=%d maxres=%.2e last_bad=%d r=%d c0=%d b=%d bc=%d lo=%.3e cut=%.3e" % (

@@ -1,8 +1,9 @@
 """How predictable is the eigenvector block from one iteration to the next?
 Runs config idx to k0, k0+1, k0+2 (three solves, same trajectory), takes the
 kept eigenvectors V of each iterate and compares the subspace angle between
-span(V_k) and (a) span(V_{k-1}) -- the warm start the kernel uses -- with
-(b) span(2 V_{k-1} - V_{k-2}), a linear extrapolation."""
+span(V_k) and (a) span(V_{k-1}) -- the plain warm start -- with (b)
+span(2 V_{k-1} - V_{k-2}), the linear extrapolation the kernel starts from,
+and (c) the quadratic one, 3 V_{k-1} - 3 V_{k-2} + V_{k-3}."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -31,7 +32,7 @@ def sin_angle(A, B):      # largest principal angle between span(A) and span(B)
 
 for k0 in k0s:
     Vs, r = [], None
-    for k in (k0, k0 + 1, k0 + 2):
+    for k in (k0, k0 + 1, k0 + 2, k0 + 3):
         c = SolverConfig(**{**cfg.__dict__, "max_iter": k})
         res = pk.solve_lr_pd_sdp(prob, c)
         r = res.rank_path[-1][1]
@@ -39,9 +40,13 @@ for k0 in k0s:
         if Vs:
             V = V * np.sign(np.sum(V * Vs[-1], axis=0))
         Vs.append(V)
-    a = sin_angle(Vs[1], Vs[2]); b = sin_angle(2 * Vs[1] - Vs[0], Vs[2])
-    pc = [np.linalg.norm(Vs[2][:, j] - Vs[1][:, j]) for j in range(r)]
-    pe = [np.linalg.norm(Vs[2][:, j] - 2 * Vs[1][:, j] + Vs[0][:, j]) for j in range(r)]
-    print(f"k0={k0} r={r} sin(angle) warm start {a:.3e}  extrapolated {b:.3e}  ratio {a / b:.2f}")
+    npos = int(np.sum(np.linalg.norm(Vs[3] - Vs[2], axis=0) < 0.5))      # columns tracked from step to step
+    W = [V[:, :npos] for V in Vs]
+    a = sin_angle(W[2], W[3]); b = sin_angle(2 * W[2] - W[1], W[3]); c = sin_angle(3 * W[2] - 3 * W[1] + W[0], W[3])
+    pc = [np.linalg.norm(W[3][:, j] - W[2][:, j]) for j in range(npos)]
+    pe = [np.linalg.norm(W[3][:, j] - 2 * W[2][:, j] + W[1][:, j]) for j in range(npos)]
+    pq = [np.linalg.norm(W[3][:, j] - 3 * W[2][:, j] + 3 * W[1][:, j] - W[0][:, j]) for j in range(npos)]
+    print(f"k0={k0} r={r} ({npos} tracked) sin(angle) warm start {a:.3e}  linear {b:.3e}  quadratic {c:.3e}")
     print("   per column |dV|   :", " ".join(f"{x:.1e}" for x in pc))
-    print("   per column |d2V|  :", " ".join(f"{x:.1e}" for x in pe), flush=True)
+    print("   per column |d2V|  :", " ".join(f"{x:.1e}" for x in pe))
+    print("   per column |d3V|  :", " ".join(f"{x:.1e}" for x in pq), flush=True)
