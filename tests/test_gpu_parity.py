@@ -143,6 +143,23 @@ def test_small_lr_solves_match_reference(ci):
     assert res.residual_scale == pytest.approx(float(d[pre + "scale"]), rel=1e-10)
 
 
+def test_extrapolated_start_cuts_operator_applications():
+    """The eigensolver starts each iteration from an extrapolation of the last
+    eigenvector blocks (iterate.cuh, PDSDP_EXTRAP): same iterates as the
+    oracle, but far fewer operator applications than the plain warm start
+    needed on config 1 (15.9 per iteration; 8.3 measured with the
+    extrapolation) -- guards against the start silently falling back."""
+    from paper_1810_05231_b200.device import DeviceBatch
+    from paper_1810_05231_b200.solver import operator_norm_on_device, run_lr_loop
+    prob, cfg = workloads.config(0)
+    batch = DeviceBatch([prob])
+    alpha = cfg.alpha_safety / operator_norm_on_device(batch, 0, cfg.seed)
+    o = run_lr_loop(batch, 0, prob, cfg, alpha)
+    assert o.status.value == "optimal" and o.it.k == 1718
+    assert o.eig_matvecs / o.it.k < 11.0
+    batch.close()
+
+
 def test_config1_end_to_end_matches_reference():
     d = load_golden("cfg1.npz")
     prob, cfg = workloads.config(0)
