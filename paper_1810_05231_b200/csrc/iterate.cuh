@@ -71,7 +71,7 @@ namespace pdsdp {
 #define PDSDP_EXTRAP 2
 #endif
 #ifndef PDSDP_QRETRY
-#define PDSDP_QRETRY 32         // iterations at order 1 after an order-2 start needed a second pass
+#define PDSDP_QRETRY 128        // iterations at order 1 after an order-2 start needed a second pass
 #endif
 #ifndef PDSDP_QTOL
 #define PDSDP_QTOL 0.1          // kept-pair tolerance factor of an iteration that starts at order 2
@@ -83,7 +83,7 @@ namespace pdsdp {
 #define PDSDP_HINT_MIN 1        // smallest first-pass filter degree
 #endif
 #ifndef PDSDP_PROBE_AGE
-#define PDSDP_PROBE_AGE 1024    // iterations before a failed one-degree-down probe of the hint is retried (0: no probing)
+#define PDSDP_PROBE_AGE 256     // iterations before a failed one-degree-down probe of the hint is retried (0: no probing)
 #endif
 #ifndef PDSDP_HINT_SAFETY
 #define PDSDP_HINT_SAFETY 0     // degrees of slack kept when lowering the filter-degree hint
