@@ -666,8 +666,11 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
   if (const char* e = getenv("PDSDP_DENSE_BLOCK_NMIN")) b->bj_nmin = std::max(BJ_B2, atoi(e));
   int maxn = 0;
   for (int k = 0; k < count; ++k) maxn = std::max(maxn, (int)problems[k].n);
+  int cta_rows = PDSDP_CTA_ROWS;
+  const char* rows_env = getenv("PDSDP_CTA_ROWS");
+  if (rows_env) cta_rows = std::max(32, atoi(rows_env));
   int C = 1;
-  while (C < 16 && C * PDSDP_CTA_ROWS < maxn) C <<= 1;
+  while (C < 16 && C * cta_rows < maxn) C <<= 1;
   b->C = C;
   int lds = std::min(maxn, PDSDP_BMAX);
   b->lds = lds < 4 ? 4 : lds;
@@ -675,6 +678,16 @@ int pdsdp_batch_create(int count, const pdsdp_problem* problems, pdsdp_batch** o
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, lrpdhg_iterate_kernel));
     b->smem = 227 * 1024 - fa.sharedSizeBytes;   // dynamic limit next to the static part
+  }
+  // A batch with more instances than clusters of that size can be resident
+  // runs on clusters of half the size: each instance is slower, twice as many
+  // run side by side (config 5: 32 instances 12.7 -> 9.8 s, 128 instances
+  // ~43 -> 29.5 s; a further halving gains nothing, profiles/r02_cfg5_cluster_size.txt)
+  if (!rows_env && count > 1 && C >= 2) {
+    int slots = 1;
+    int rc = max_active_clusters(b, &slots);
+    if (rc) { delete b; return rc; }
+    if (count > slots) b->C = C = C / 2;
   }
   CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
   const size_t outn = (size_t)count * PDSDP_KMAX * PDSDP_OUT_LEN;

@@ -550,6 +550,33 @@ def test_batch_with_instance_switching_to_dense_path():
         assert rel(rb.y, rs.y) <= 1e-12
 
 
+def test_large_batch_runs_on_half_size_clusters():
+    """A batch with more instances than clusters can be resident is laid out
+    on clusters of half the default size (pdsdp_batch_create); the instances
+    still follow their single-solve trajectories (rounding-level differences
+    of the cluster reductions only)."""
+    from paper_1810_05231_b200.device import DeviceBatch
+    n = 260                                   # 3 CTAs of 128 rows -> clusters of 4 by default
+    few = [workloads.maxcut_problem(n, 0.05, s, signed=True) for s in range(2)]
+    b_few = DeviceBatch(few)
+    c_default = b_few.info(0)["cluster"]
+    b_few.close()
+    assert c_default == 4
+    # at most 148 / 4 = 37 clusters of 4 CTAs fit the device
+    probs = [workloads.maxcut_problem(n, 0.05, s, signed=True) for s in range(40)]
+    cfg = SolverConfig(eps_tol=1e-4, max_iter=150, initial_rank=3, window_ell=60)
+    b_many = DeviceBatch(probs)
+    assert b_many.info(0)["cluster"] == c_default // 2
+    b_many.close()
+    batch = pk.solve_lr_pd_sdp_batch(probs, cfg)
+    assert len(batch) == len(probs)
+    for p, rb in list(zip(probs, batch))[:3]:
+        rs = pk.solve_lr_pd_sdp(p, cfg)
+        assert rb.status == rs.status and rb.iterations == rs.iterations and rb.rank_path == rs.rank_path
+        assert rel(rb.X.data, rs.X.data) <= 1e-9
+        assert rel(rb.y, rs.y) <= 1e-9
+
+
 # ------------------------------------------- factored vs entrywise residual
 
 @pytest.mark.parametrize("ci,K,r", [(0, 300, 5), (1, 40, 10), (3, 30, 1), (4, 40, 1)])
