@@ -51,7 +51,7 @@ WORKLOADS = {
 FP64_DMMA_TFLOPS = 37.1   # measured on this pool's B200 (profiles/r01_fp64_cluster_probe.txt)
 # dram__bytes_read.sum + dram__bytes_write.sum of one iteration at rank 20 from the
 # last committed `ncu --set full` capture of the iteration kernel (archived, per commit)
-ARCHIVED_TRAFFIC = (3560192, "profiles/r02_iterate_kernel_ncu_raw_r20.csv (archived capture)")
+ARCHIVED_TRAFFIC = (3558656, "profiles/r02_iterate_kernel_ncu_raw_r20.csv (archived capture)")
 
 
 def env_rank():
