@@ -66,7 +66,8 @@ namespace pdsdp {
 // so the kept columns start from an extrapolation of the last blocks instead
 // of V_k: 2 V_k - V_k-1 (order 1; V_k-1 is still in F when the iteration
 // begins) or 3 V_k - 3 V_k-1 + V_k-2 (order 2; V_k-2 kept in Vp).  Only the
-// starting point changes; the block is iterated to the same tolerances.
+// starting point changes; the block is iterated to the same tolerances
+// (tightened by PDSDP_QTOL on iterations that start at order 2).
 #ifndef PDSDP_EXTRAP
 #define PDSDP_EXTRAP 2
 #endif
